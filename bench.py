@@ -1,0 +1,370 @@
+"""Benchmark: GiFt filter-bank throughput (nnz x hops / s) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+A step is one GiFt filter pass (gift.py:73-95 + the gift_place epilogue
+gift.py:112-118): the default bank 0.1 A_2^2 + 0.7 A_4^2 + 0.2 A_4^4 (6
+algorithmic SpMM hops) over the clique graph of one synthetic netlist, with
+the graph resident (built once, like SparseSymMatrix caching its degrees).
+Metric = nnz_op * 6 / step time, nnz_op = nnz(A) + N (the stored entries of
+A_sigma).
+
+Workload (BASELINE.json configs[3], quoted "at 1/2/4/8 B200"): c3, 2.18M
+movable cells + 8k macros + 8.9k pads, 2.23M nets, max_clique_pins=200,
+seeded synthetic (the paper's ISPD2014 designs are not available).  The CSR
+(~7 GB) is far larger than L2, so no explicit flush is needed between steps.
+
+`value`  : device time of K steps with every input resident in HBM.
+`e2e`    : the same metric through the C ABI call gift_filter_host with
+           pinned HOST buffers (H2D of the fp32 seed + fixed mask/positions,
+           D2H of the fp64 placement inside every step).
+`roofline`: the dominant kernel (the fused hop), algorithmic bytes
+           (8*nnz_op + 24*N + 8 per hop unit) / its mean CUDA-event time.
+`cpu_baseline`: the oracle port (oracle/gift_oracle.c, fp64 reference
+           operation order, OpenMP over rows) on a scaled sample, rank 0, N=1.
+--impl reference: the same oracle as the reference arm (the reference is
+           pure Python/scipy and cannot be installed as a GPU-box package).
+Multi-GPU (torchrun): ranks run independent replicas of the workload
+(weak scaling); the row-sharded halo-exchange path is tested on CPU (gloo).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "gift_filter_nnz_hops_per_sec"
+UNIT = "nnz*hops/s"
+HOPS = 6
+SAMPLE_SCALE = {"c0": 1.0, "c1": 0.5, "c2": 0.04, "c3": 0.03, "c4": 0.01}
+
+
+def bytes_per_hop(nnz_op: int, n: int) -> int:
+    """int32 col + fp32 value per stored entry, int64 rowptr,
+    float2 read and float2 write per row."""
+    return 8 * nnz_op + 24 * n + 8
+
+
+def peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm_gbs": float(p["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.lines: list[str] = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_sample(config: str, seed: int, scale: float, steps: int = 1):
+    """Time the oracle's gift_filter (fp64, reference order, OpenMP) on a scaled sample."""
+    from oracle import oracle as orc
+    from paper_2502_17632_b200 import synth
+
+    fd = synth.generate(config, seed=seed, scale=scale)
+    cap = fd.meta["max_clique_pins"]
+    A = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, cap)
+    deg = orc.degrees(A)
+    g = synth.signal_fp32(fd, seed=0).astype(np.float64)
+    terms = [(2.0, 2, 0.1), (4.0, 2, 0.7), (4.0, 4, 0.2)]
+    nnz_op = A.nnz + fd.num_cells
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        orc.gift_filter(A, g, terms, deg)
+        times.append(time.perf_counter() - t0)
+    return {
+        "times": times, "nnz_op": nnz_op, "n": fd.num_cells, "cores": orc.num_threads(),
+        "sample": f"{config} at scale {scale} ({fd.num_cells} cells, {fd.num_nets} nets, nnz_op {nnz_op}): "
+                  f"oracle gift_filter (2 normalisations + 6 fp64 hops, csr_matvecs order)",
+    }
+
+
+def run_reference(args) -> None:
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    scale = SAMPLE_SCALE[args.config]
+    res = cpu_sample(args.config, args.seed, scale, steps=args.warmup + args.steps)
+    t = res["times"][args.warmup:]
+    per = float(np.mean(t))
+    value = res["nnz_op"] * HOPS / per
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} (bounded sample, scale {scale})", "seed": args.seed},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": res["cores"], "kind": "port",
+                         "sample": res["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=["c0", "c1", "c2", "c3", "c4"])
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    import paper_2502_17632_b200 as gb
+    from paper_2502_17632_b200 import _lib, synth
+
+    lib = _lib.load_library()
+    t0 = time.perf_counter()
+    fd = synth.generate(args.config, seed=args.seed)
+    gen_s = time.perf_counter() - t0
+    cap = fd.meta["max_clique_pins"]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    adj = gb.build_clique_graph(fd, max_clique_pins=cap)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    n = adj.n
+    nnz_op = adj.nnz + n
+    unit_bytes = bytes_per_hop(nnz_op, n)
+
+    g32 = synth.signal_fp32(fd, seed=0)
+    mask = fd.fixed_mask().astype(np.uint8)
+    fpos = np.nan_to_num(fd.fixed_positions(), nan=0.0)
+    region = fd.region.bounds()
+    sig = np.array([t.sigma for t in gb.DEFAULT_TERMS], dtype=np.float64)
+    kk = np.array([t.k for t in gb.DEFAULT_TERMS], dtype=np.int64)
+    al = np.array([t.alpha for t in gb.DEFAULT_TERMS], dtype=np.float64)
+    dg = torch.from_numpy(g32).to(dev)
+    dmask = torch.from_numpy(mask).to(dev)
+    dpos = torch.from_numpy(fpos).to(dev)
+    dout = torch.empty((n, 2), dtype=torch.float64, device=dev)
+    ctx = _lib.context(local)
+    sp_, kp_, ap_, rp_ = (sig.ctypes.data_as(_lib.c_dp), kk.ctypes.data_as(_lib.c_i64p),
+                          al.ctypes.data_as(_lib.c_dp), region.ctypes.data_as(_lib.c_dp))
+
+    def step():
+        _lib.check(lib.gift_filter(ctx, adj.handle, 3, sp_, kp_, ap_, 2, _lib.GIFT_DTYPE_F32, _lib.dptr(dg),
+                                   _lib.GIFT_DTYPE_F64, _lib.dptr(dout), _lib.dptr(dmask), _lib.dptr(dpos), rp_,
+                                   _lib.GIFT_PREC_FP32))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, device events, max over ranks ----
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.2)
+    _lib.set_profiling(True, local)
+    _lib.drain_profile(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count(local)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = _lib.launch_count(local) - launches0
+    recs = _lib.drain_profile(local)
+    _lib.set_profiling(False, local)
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    t_rank = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_rank, op=dist.ReduceOp.MAX)
+    ms_max = float(t_rank.item())
+    per_step_ms = ms_max / args.steps
+    value = nnz_op * HOPS * args.steps * world / (ms_max / 1e3)
+
+    # ---- roofline of the dominant kernel ----
+    pk = peaks()
+    by_kind: dict[int, list] = {}
+    for kind, units, t in recs:
+        by_kind.setdefault(kind, []).append((units, t))
+    kernels = {}
+    for kind, lst in by_kind.items():
+        tot = sum(t for _, t in lst)
+        mean_ms = tot / len(lst)
+        units = lst[0][0]
+        alg = (units * unit_bytes) if kind > 0 else (n * (8 + 4 * units) + n * 4 * kind)
+        kernels[kind] = {"launches": len(lst), "mean_ms": mean_ms, "share": tot, "units": units,
+                         "bytes": alg}
+    total_prof = sum(k["share"] for k in kernels.values()) or 1.0
+    hop_kinds = [k for k in kernels if k > 0]
+    dom = max(hop_kinds, key=lambda k: kernels[k]["share"]) if hop_kinds else None
+
+    def roof(kind):
+        k = kernels[kind]
+        ach = k["bytes"] / (k["mean_ms"] / 1e3) / 1e9
+        return {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": round(ach / pk["hbm_gbs"], 4), "traffic": None,
+                "kernel": f"k_hop<FIN={kind}> ({k['units']} hop unit(s)/launch)",
+                "bytes_per_launch": k["bytes"], "mean_launch_ms": round(k["mean_ms"], 5),
+                "share_of_step": round(k["share"] / total_prof, 4), "peak_source": pk["source"]}
+
+    roofline = roof(dom) if dom is not None else None
+    kernels_report = {f"k_hop_F{k}" if k else "k_prep": roof(k) if k else
+                      {"mean_launch_ms": round(v["mean_ms"], 5), "share_of_step": round(v["share"] / total_prof, 4)}
+                      for k, v in kernels.items()}
+
+    # ---- e2e through the C ABI with pinned host buffers ----
+    h_g = torch.from_numpy(g32).pin_memory()
+    h_mask = torch.from_numpy(mask).pin_memory()
+    h_pos = torch.from_numpy(fpos).pin_memory()
+    h_out = torch.empty((n, 2), dtype=torch.float64).pin_memory()
+
+    def step_e2e():
+        _lib.check(lib.gift_filter_host(ctx, adj.handle, 3, sp_, kp_, ap_, 2, _lib.GIFT_DTYPE_F32,
+                                        _lib.c_vp(h_g.data_ptr()), _lib.GIFT_DTYPE_F64, _lib.c_vp(h_out.data_ptr()),
+                                        _lib.c_vp(h_mask.data_ptr()), _lib.c_vp(h_pos.data_ptr()), rp_,
+                                        _lib.GIFT_PREC_FP32))
+
+    for _ in range(2):
+        step_e2e()
+    k_e2e = args.e2e_steps or args.steps
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(k_e2e):
+        step_e2e()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    t_e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+    e2e_value = nnz_op * HOPS * k_e2e * world / float(t_e.item())
+    h2d = g32.nbytes + mask.nbytes + fpos.nbytes
+    d2h = n * 2 * 8
+
+    # ---- CPU baseline (rank 0, N = 1) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        scale = SAMPLE_SCALE[args.config]
+        res = cpu_sample(args.config, args.seed, scale, steps=2)
+        per = min(res["times"])
+        cpu = {"value": res["nnz_op"] * HOPS / per, "unit": UNIT, "cores": res["cores"], "kind": "port",
+               "sample": res["sample"]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {
+                "workload": f"{args.config}: {fd.meta['n_mov']} movable + {fd.meta['n_macros']} macros + "
+                            f"{fd.meta['n_pads']} pads, {fd.meta['n_nets']} nets, max_clique_pins={cap}, "
+                            f"default bank (6 hops), fp32 fused path",
+                "n": n, "nnz": adj.nnz, "nnz_op": nnz_op, "hops": HOPS, "seed": args.seed,
+                "bytes_per_hop_unit": unit_bytes,
+                "l2": "inputs larger than L2 (CSR col+w32 = %.2f GB per pass)" % (8 * adj.nnz / 1e9),
+                "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                "graph_build_s": round(build_s, 3), "generate_s": round(gen_s, 3),
+            },
+            "roofline": roofline,
+            "kernels": kernels_report,
+            "effective_bank_gbs": round(HOPS * unit_bytes / (per_step_ms / 1e3) / 1e9, 1),
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "api": "gift_filter_host (C ABI, pinned host buffers)",
+                    "ms_per_step": 1e3 * float(t_e.item()) / k_e2e},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

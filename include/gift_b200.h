@@ -1,0 +1,152 @@
+/*
+ * gift_b200.h -- C ABI of the B200-native GiFt hot path (libgiftb200.so).
+ *
+ * The reference (`giftplace`, pure Python on numpy/scipy) has no FFI; its
+ * operator API for this path is the set of Python functions re-exported at
+ * giftplace/__init__.py:26-38.  Each entry point below replaces one of them
+ * (file:line cited per function) or the scipy/numpy routine it delegates to.
+ * The Python package paper_2502_17632_b200 binds this header with ctypes
+ * (see INTEGRATION.md for the binding a maintainer would add to giftplace).
+ *
+ * Conventions
+ *  - Plain C types only.  Pointers prefixed d_ are DEVICE pointers (CUDA
+ *    global memory of the context's device); h_ are HOST pointers.
+ *  - Every function returns a status code (GIFT_OK == 0).  On failure a
+ *    thread-local message is available from gift_last_error() and, for
+ *    GIFT_ERR_ISOLATED_NODE, the node id from gift_last_error_arg().  The
+ *    Python shim re-raises the reference's exception classes:
+ *      GIFT_ERR_VALUE         -> ValueError             (graph.py:42-45,174-175,201-202; gift.py:44-45)
+ *      GIFT_ERR_DIMENSION     -> DimensionMismatchError (graph.py:98-99; gift.py:80-81)
+ *      GIFT_ERR_ISOLATED_NODE -> IsolatedNodeError(node) (graph.py:177-180)
+ *      GIFT_ERR_NON_SYMMETRIC -> NonSymmetricError      (graph.py:59-65)
+ *  - All work is enqueued on the context's CUDA stream (gift_ctx_set_stream);
+ *    functions that must return a host-visible scalar (nnz after a build, an
+ *    error found on the device) synchronise that stream.
+ *  - Deterministic: identical inputs give bit-identical outputs.
+ *    No floating-point atomics anywhere.
+ *  - Exactness: CSR structure, fp64 values and fp64 degrees are bit-identical
+ *    to the reference (scipy/numpy operation order).
+ *    GIFT_PREC_FP64_EXACT filter output is bit-identical to gift_filter /
+ *    gift_place; GIFT_PREC_FP32 is the fast fused path (<= 1e-5 rel-L2).
+ */
+#ifndef GIFT_B200_H
+#define GIFT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GIFT_OK 0
+#define GIFT_ERR_VALUE 1
+#define GIFT_ERR_DIMENSION 2
+#define GIFT_ERR_ISOLATED_NODE 3
+#define GIFT_ERR_NON_SYMMETRIC 4
+#define GIFT_ERR_TOO_LARGE 5
+#define GIFT_ERR_CUDA 6
+#define GIFT_ERR_OOM 7
+#define GIFT_ERR_INTERNAL 8
+
+#define GIFT_PREC_FP32 0        /* fused fp32 bank: pre-scaled recurrence, chains fused */
+#define GIFT_PREC_FP64_EXACT 1  /* reference operation order, fp64, bit-exact */
+
+#define GIFT_DTYPE_F32 0
+#define GIFT_DTYPE_F64 1
+
+typedef struct gift_ctx gift_ctx; /* device + stream + workspace */
+typedef struct gift_csr gift_csr; /* immutable symmetric CSR (SparseSymMatrix, graph.py:48-111) */
+
+/* ---- context --------------------------------------------------------- */
+int gift_ctx_create(int device, gift_ctx** out);
+int gift_ctx_destroy(gift_ctx* ctx);
+/* stream: a cudaStream_t (0 = legacy default stream). */
+int gift_ctx_set_stream(gift_ctx* ctx, void* stream);
+const char* gift_last_error(void);
+int64_t gift_last_error_arg(void);
+const char* gift_version(void);
+/* Number of kernels this library launched on ctx since creation (for the bench's gpu_launches). */
+int64_t gift_ctx_launch_count(const gift_ctx* ctx);
+/* Launch timing: when on, every filter-bank kernel is bracketed by CUDA
+ * events on the context stream.  gift_ctx_profile_drain synchronises, writes
+ * up to max_records (kind, units, milliseconds) triples and clears the log.
+ * kind: 0 = signal pack (z0 = s o g), F = hop kernel with F floats per row
+ * (1/2/4); units = algorithmic hops the launch performs (chains it advances). */
+int gift_ctx_set_profiling(gift_ctx* ctx, int on);
+int gift_ctx_profile_drain(gift_ctx* ctx, int max_records, int* h_kind, int* h_units, float* h_ms,
+                           int* n_records);
+
+/* ---- graph construction --------------------------------------------- */
+/* build_clique_graph(design, max_clique_pins)  graph.py:120-158.
+ * d_net_start: int64[n_nets+1] (Design.pin_table net_start, netlist.py:142-166),
+ * d_pin_cell:  int32[n_pins] cell ids in [0, n_cells).
+ * max_clique_pins <= 0 means None (no cap).  *n_skipped (host, nullable)
+ * receives the number of nets skipped by the cap (graph.py:150-151). */
+int gift_build_clique_graph(gift_ctx* ctx, int64_t n_cells, int64_t n_nets,
+                            const int64_t* d_net_start, const int32_t* d_pin_cell,
+                            int64_t max_clique_pins, gift_csr** out, int64_t* n_skipped);
+
+/* from_coo(n, rows, cols, vals)  graph.py:114-117, followed by the
+ * SparseSymMatrix checks (graph.py:55-65) when check_symmetric != 0.
+ * Duplicates summed in scipy order, explicit zeros dropped. */
+int gift_csr_from_coo(gift_ctx* ctx, int64_t n, int64_t nnz, const int64_t* d_rows,
+                      const int64_t* d_cols, const double* d_vals, int check_symmetric,
+                      gift_csr** out);
+
+int gift_csr_destroy(gift_csr* csr);
+int gift_csr_shape(const gift_csr* csr, int64_t* n, int64_t* nnz);
+/* Device views (owned by csr): indptr int64[n+1], indices int32[nnz], values fp64[nnz]
+ * (SparseSymMatrix.indptr/.indices/.values, graph.py:77-87). */
+int gift_csr_arrays(const gift_csr* csr, const int64_t** d_indptr, const int32_t** d_indices,
+                    const double** d_values);
+/* Copies to caller-allocated HOST arrays (any pointer may be NULL). */
+int gift_csr_download(gift_ctx* ctx, const gift_csr* csr, int64_t* h_indptr, int32_t* h_indices,
+                      double* h_values);
+/* SparseSymMatrix.degrees (graph.py:89-94): fp64 row sums in numpy
+ * np.add.reduceat order; computed once and cached on csr. */
+int gift_csr_degrees(gift_ctx* ctx, gift_csr* csr, const double** d_degrees);
+
+/* ---- operators ------------------------------------------------------ */
+/* normalized_augmented_adjacency(adj, sigma)  graph.py:167-188, materialised. */
+int gift_normalized_augmented_adjacency(gift_ctx* ctx, gift_csr* adj, double sigma, gift_csr** out);
+/* SparseSymMatrix.matmul(g) (graph.py:96-100): y = A x, fp64, x/y row-major
+ * [n, ncols], scipy csr_matvecs order (bit-exact). */
+int gift_csr_matmul(gift_ctx* ctx, const gift_csr* csr, int64_t ncols, const double* d_x, double* d_y);
+
+/* ---- filter bank ---------------------------------------------------- */
+/* gift_filter(adj, g, config)  gift.py:73-95, optionally fused with the
+ * gift_place epilogue gift.py:112-118 (re-pin fixed rows, np.clip movable
+ * rows to region) when d_fixed_mask != NULL.
+ *   terms: n_terms triples (h_sigma[t], h_k[t], h_alpha[t]) (FilterTerm, graph.py:33-45)
+ *   d_g:    [n, ncols] row-major, dtype in_dtype
+ *   d_out:  [n, ncols] row-major, dtype out_dtype
+ *   d_fixed_mask: uint8[n] or NULL; d_fixed_pos: fp64[n, 2] (rows read only where
+ *   fixed); h_region: fp64[4] = xmin, ymin, xmax, ymax.  The epilogue needs ncols == 2.
+ *   precision: GIFT_PREC_FP32 or GIFT_PREC_FP64_EXACT. */
+int gift_filter(gift_ctx* ctx, gift_csr* adj, int n_terms, const double* h_sigma,
+                const int64_t* h_k, const double* h_alpha, int64_t ncols, int in_dtype,
+                const void* d_g, int out_dtype, void* d_out, const uint8_t* d_fixed_mask,
+                const double* d_fixed_pos, const double* h_region, int precision);
+
+/* Same, with HOST buffers: copies h_g in, runs the bank + epilogue and copies
+ * the result out on the context stream (the end-to-end call a host
+ * integration makes; returns after the result is in h_out). */
+int gift_filter_host(gift_ctx* ctx, gift_csr* adj, int n_terms, const double* h_sigma,
+                     const int64_t* h_k, const double* h_alpha, int64_t ncols, int in_dtype,
+                     const void* h_g, int out_dtype, void* h_out, const uint8_t* h_fixed_mask,
+                     const double* h_fixed_pos, const double* h_region, int precision);
+
+/* Netlist in, positions out: H2D pin table + signal, build_clique_graph,
+ * bank, epilogue, D2H (gift.py:98-119 composed with graph.py:120-158).
+ * Returns the graph's nnz in *nnz_out (nullable). */
+int gift_place_host(gift_ctx* ctx, int64_t n_cells, int64_t n_nets, const int64_t* h_net_start,
+                    const int32_t* h_pin_cell, int64_t max_clique_pins, int n_terms,
+                    const double* h_sigma, const int64_t* h_k, const double* h_alpha,
+                    const float* h_g, const uint8_t* h_fixed_mask, const double* h_fixed_pos,
+                    const double* h_region, int out_dtype, void* h_out, int precision,
+                    int64_t* nnz_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GIFT_B200_H */

@@ -1,0 +1,168 @@
+"""ctypes binding of libgiftb200.so (the C ABI declared in include/gift_b200.h).
+
+The library is the product: there is no CPU fallback.  Loading fails loudly
+(`DeviceError`) when the shared object is missing or no CUDA device is
+visible.  Device buffers handed to the library are torch CUDA tensors
+(PyTorch is plumbing here: allocation, streams, host<->device copies).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import (
+    DeviceError,
+    DimensionMismatchError,
+    GiftPlaceError,
+    IsolatedNodeError,
+    NonSymmetricError,
+)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgiftb200.so")
+
+GIFT_OK = 0
+GIFT_ERR_VALUE = 1
+GIFT_ERR_DIMENSION = 2
+GIFT_ERR_ISOLATED_NODE = 3
+GIFT_ERR_NON_SYMMETRIC = 4
+GIFT_ERR_TOO_LARGE = 5
+GIFT_ERR_CUDA = 6
+GIFT_ERR_OOM = 7
+GIFT_ERR_INTERNAL = 8
+
+GIFT_PREC_FP32 = 0
+GIFT_PREC_FP64_EXACT = 1
+GIFT_DTYPE_F32 = 0
+GIFT_DTYPE_F64 = 1
+
+c_i64 = ctypes.c_int64
+c_int = ctypes.c_int
+c_vp = ctypes.c_void_p
+c_dp = ctypes.POINTER(ctypes.c_double)
+c_i64p = ctypes.POINTER(ctypes.c_int64)
+
+# (name, restype, argtypes) -- every symbol include/gift_b200.h declares
+SIGNATURES = [
+    ("gift_ctx_create", c_int, [c_int, ctypes.POINTER(c_vp)]),
+    ("gift_ctx_destroy", c_int, [c_vp]),
+    ("gift_ctx_set_stream", c_int, [c_vp, c_vp]),
+    ("gift_last_error", ctypes.c_char_p, []),
+    ("gift_last_error_arg", c_i64, []),
+    ("gift_version", ctypes.c_char_p, []),
+    ("gift_ctx_launch_count", c_i64, [c_vp]),
+    ("gift_ctx_set_profiling", c_int, [c_vp, c_int]),
+    ("gift_ctx_profile_drain", c_int, [c_vp, c_int, c_vp, c_vp, c_vp, ctypes.POINTER(c_int)]),
+    ("gift_build_clique_graph", c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, ctypes.POINTER(c_vp), c_i64p]),
+    ("gift_csr_from_coo", c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, ctypes.POINTER(c_vp)]),
+    ("gift_csr_destroy", c_int, [c_vp]),
+    ("gift_csr_shape", c_int, [c_vp, c_i64p, c_i64p]),
+    ("gift_csr_arrays", c_int, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
+    ("gift_csr_download", c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    ("gift_csr_degrees", c_int, [c_vp, c_vp, ctypes.POINTER(c_vp)]),
+    ("gift_normalized_augmented_adjacency", c_int, [c_vp, c_vp, ctypes.c_double, ctypes.POINTER(c_vp)]),
+    ("gift_csr_matmul", c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
+    ("gift_filter", c_int, [c_vp, c_vp, c_int, c_dp, c_i64p, c_dp, c_i64, c_int, c_vp, c_int, c_vp, c_vp, c_vp,
+                            c_dp, c_int]),
+    ("gift_filter_host", c_int, [c_vp, c_vp, c_int, c_dp, c_i64p, c_dp, c_i64, c_int, c_vp, c_int, c_vp, c_vp,
+                                 c_vp, c_dp, c_int]),
+    ("gift_place_host", c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_int, c_dp, c_i64p, c_dp, c_vp, c_vp, c_vp,
+                                c_dp, c_int, c_vp, c_int, c_i64p]),
+]
+
+_lib = None
+_lock = threading.Lock()
+_ctxs: dict[int, int] = {}
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """dlopen the library and bind every symbol (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise DeviceError(
+                    f"CUDA library {path} is missing; build it with "
+                    "`python -m paper_2502_17632_b200.build_ext` (there is no CPU fallback)")
+            lib = ctypes.CDLL(path)
+            for name, res, args in SIGNATURES:
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def check(status: int) -> None:
+    """Map a C ABI status to the reference's exception classes."""
+    if status == GIFT_OK:
+        return
+    lib = load_library()
+    msg = (lib.gift_last_error() or b"").decode(errors="replace")
+    if status == GIFT_ERR_VALUE:
+        raise ValueError(msg)
+    if status == GIFT_ERR_DIMENSION:
+        raise DimensionMismatchError(msg)
+    if status == GIFT_ERR_ISOLATED_NODE:
+        raise IsolatedNodeError(int(lib.gift_last_error_arg()))
+    if status == GIFT_ERR_NON_SYMMETRIC:
+        raise NonSymmetricError(msg)
+    if status in (GIFT_ERR_CUDA, GIFT_ERR_OOM):
+        raise DeviceError(msg)
+    raise GiftPlaceError(msg)
+
+
+def torch_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device visible: the GiFt B200 path has no CPU fallback")
+    return torch
+
+
+def context(device: int | None = None) -> int:
+    """Per-device library context bound to torch's current stream."""
+    torch = torch_cuda()
+    lib = load_library()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    ctx = _ctxs.get(dev)
+    if ctx is None:
+        h = c_vp()
+        check(lib.gift_ctx_create(dev, ctypes.byref(h)))
+        ctx = h.value
+        _ctxs[dev] = ctx
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    check(lib.gift_ctx_set_stream(ctx, c_vp(stream)))
+    return ctx
+
+
+def launch_count(device: int | None = None) -> int:
+    torch = torch_cuda()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    ctx = _ctxs.get(dev)
+    return int(load_library().gift_ctx_launch_count(ctx)) if ctx else 0
+
+
+def set_profiling(on: bool, device: int | None = None) -> None:
+    check(load_library().gift_ctx_set_profiling(context(device), 1 if on else 0))
+
+
+def drain_profile(device: int | None = None, max_records: int = 1 << 16):
+    """[(kind, units, ms)] for the launches recorded since the last drain."""
+    import numpy as np
+
+    kind = np.zeros(max_records, dtype=np.int32)
+    units = np.zeros(max_records, dtype=np.int32)
+    ms = np.zeros(max_records, dtype=np.float32)
+    n = c_int(0)
+    check(load_library().gift_ctx_profile_drain(
+        context(device), max_records, kind.ctypes.data_as(c_vp), units.ctypes.data_as(c_vp),
+        ms.ctypes.data_as(c_vp), ctypes.byref(n)))
+    k = n.value
+    return list(zip(kind[:k].tolist(), units[:k].tolist(), ms[:k].tolist()))
+
+
+def dptr(t) -> c_vp:
+    return c_vp(t.data_ptr())

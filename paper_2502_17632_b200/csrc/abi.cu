@@ -1,0 +1,363 @@
+// abi.cu -- extern "C" entry points of libgiftb200.so (include/gift_b200.h)
+// plus the context / memory / error plumbing declared in common.cuh.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace gift {
+
+// implemented in build.cu / filter.cu
+Csr* build_clique_graph(Ctx* ctx, int64_t n, int64_t n_nets, const int64_t* d_net_start, const int32_t* d_pin_cell,
+                        int64_t cap, int64_t* n_skipped);
+Csr* csr_from_coo(Ctx* ctx, int64_t n, int64_t T, const int64_t* d_rows, const int64_t* d_cols, const double* d_vals,
+                  bool check_symmetric);
+const double* csr_degrees(Ctx* ctx, Csr* c);
+Csr* normalized_augmented_adjacency(Ctx* ctx, Csr* c, double sigma);
+void csr_matmul(Ctx* ctx, const Csr* c, int64_t ncols, const double* x, double* y);
+void filter(Ctx* ctx, Csr* c, int n_terms, const double* sigma, const int64_t* k, const double* alpha, int64_t ncols,
+            int in_dtype, const void* g, int out_dtype, void* out, const uint8_t* fixed_mask, const double* fixed_pos,
+            const double* region, int precision);
+
+static thread_local Error t_err{GIFT_OK, "", -1};
+
+void set_error(int code, const std::string& msg, int64_t arg) { t_err = Error{code, msg, arg}; }
+
+int fail(int code, const std::string& msg, int64_t arg) {
+  set_error(code, msg, arg);
+  return code;
+}
+
+void throw_error(int code, const std::string& msg, int64_t arg) { throw GiftException{code, msg, arg}; }
+
+void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();  // clear sticky non-fatal state
+  const int code = (e == cudaErrorMemoryAllocation) ? GIFT_ERR_OOM : GIFT_ERR_CUDA;
+  throw_error(code, std::string(cudaGetErrorString(e)) + " in " + what + " (" + file + ":" + std::to_string(line) + ")");
+}
+
+void* dev_alloc(Ctx* ctx, size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  check_cuda(cudaMallocAsync(&p, bytes, ctx->stream), "cudaMallocAsync", __FILE__, __LINE__);
+  return p;
+}
+
+void dev_free(Ctx* ctx, void* p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+void* scratch(Ctx* ctx, int slot, size_t bytes) {
+  if (ctx->scratch_bytes[slot] < bytes) {
+    if (ctx->scratch[slot]) dev_free(ctx, ctx->scratch[slot]);
+    ctx->scratch[slot] = dev_alloc(ctx, bytes);
+    ctx->scratch_bytes[slot] = bytes;
+  }
+  return ctx->scratch[slot];
+}
+
+void* pinned(Ctx* ctx, size_t bytes) {
+  if (ctx->pinned_bytes < bytes) {
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    ctx->pinned = nullptr;
+    check_cuda(cudaMallocHost(&ctx->pinned, bytes), "cudaMallocHost", __FILE__, __LINE__);
+    ctx->pinned_bytes = bytes;
+  }
+  return ctx->pinned;
+}
+
+void* csr_alloc(Ctx* ctx, Csr* c, size_t bytes) {
+  void* p = dev_alloc(ctx, bytes);
+  c->owned.push_back(p);
+  return p;
+}
+
+void csr_destroy(Csr* c) {
+  if (!c) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();  // outstanding work on any stream may still read the arrays
+  for (void* p : c->owned) cudaFreeAsync(p, 0);  // device idle: returns blocks to the pool
+  cudaSetDevice(prev);
+  delete static_cast<gift_csr*>(c);
+}
+
+}  // namespace gift
+
+using gift::GiftException;
+
+#define GIFT_API_BEGIN try {
+#define GIFT_API_END                                     \
+  return GIFT_OK;                                        \
+  }                                                      \
+  catch (const GiftException& e) {                       \
+    return gift::fail(e.code, e.msg, e.arg);             \
+  }                                                      \
+  catch (const std::exception& e) {                      \
+    return gift::fail(GIFT_ERR_INTERNAL, e.what());      \
+  }                                                      \
+  catch (...) {                                          \
+    return gift::fail(GIFT_ERR_INTERNAL, "unknown error"); \
+  }
+
+namespace {
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+void require(bool ok, int code, const char* msg) {
+  if (!ok) gift::throw_error(code, msg);
+}
+}  // namespace
+
+extern "C" {
+
+const char* gift_last_error(void) { return gift::t_err.msg.c_str(); }
+int64_t gift_last_error_arg(void) { return gift::t_err.arg; }
+const char* gift_version(void) { return "giftb200 0.1 sm_100a"; }
+
+int gift_ctx_create(int device, gift_ctx** out) {
+  GIFT_API_BEGIN
+  require(out != nullptr, GIFT_ERR_VALUE, "null output pointer");
+  int count = 0;
+  GIFT_CUDA(cudaGetDeviceCount(&count));
+  require(device >= 0 && device < count, GIFT_ERR_VALUE, "device ordinal out of range");
+  DeviceGuard g(device);
+  GIFT_CUDA(cudaFree(nullptr));  // establish the primary context
+  cudaMemPool_t pool;
+  GIFT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = UINT64_MAX;
+  GIFT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  auto* c = new gift_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  *out = c;
+  GIFT_API_END
+}
+
+int gift_ctx_destroy(gift_ctx* ctx) {
+  GIFT_API_BEGIN
+  if (!ctx) return GIFT_OK;
+  DeviceGuard g(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (int i = 0; i < 4; ++i)
+    if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  delete ctx;
+  GIFT_API_END
+}
+
+int gift_ctx_set_stream(gift_ctx* ctx, void* stream) {
+  GIFT_API_BEGIN
+  require(ctx != nullptr, GIFT_ERR_VALUE, "null context");
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  GIFT_API_END
+}
+
+int64_t gift_ctx_launch_count(const gift_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int gift_ctx_set_profiling(gift_ctx* ctx, int on) {
+  GIFT_API_BEGIN
+  require(ctx != nullptr, GIFT_ERR_VALUE, "null context");
+  ctx->profiling = on != 0;
+  GIFT_API_END
+}
+
+int gift_ctx_profile_drain(gift_ctx* ctx, int max_records, int* h_kind, int* h_units, float* h_ms, int* n_records) {
+  GIFT_API_BEGIN
+  require(ctx != nullptr, GIFT_ERR_VALUE, "null context");
+  DeviceGuard g(ctx->device);
+  GIFT_CUDA(cudaStreamSynchronize(ctx->stream));
+  int k = 0;
+  for (auto& r : ctx->recs) {
+    if (k < max_records) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, r.a, r.b);
+      if (h_kind) h_kind[k] = r.kind;
+      if (h_units) h_units[k] = r.units;
+      if (h_ms) h_ms[k] = ms;
+      ++k;
+    }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  ctx->recs.clear();
+  if (n_records) *n_records = k;
+  GIFT_API_END
+}
+
+int gift_build_clique_graph(gift_ctx* ctx, int64_t n_cells, int64_t n_nets, const int64_t* d_net_start,
+                            const int32_t* d_pin_cell, int64_t max_clique_pins, gift_csr** out,
+                            int64_t* n_skipped) {
+  GIFT_API_BEGIN
+  require(ctx && out, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  *out = static_cast<gift_csr*>(
+      gift::build_clique_graph(ctx, n_cells, n_nets, d_net_start, d_pin_cell, max_clique_pins, n_skipped));
+  GIFT_API_END
+}
+
+int gift_csr_from_coo(gift_ctx* ctx, int64_t n, int64_t nnz, const int64_t* d_rows, const int64_t* d_cols,
+                      const double* d_vals, int check_symmetric, gift_csr** out) {
+  GIFT_API_BEGIN
+  require(ctx && out, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  *out = static_cast<gift_csr*>(gift::csr_from_coo(ctx, n, nnz, d_rows, d_cols, d_vals, check_symmetric != 0));
+  GIFT_API_END
+}
+
+int gift_csr_destroy(gift_csr* csr) {
+  GIFT_API_BEGIN
+  gift::csr_destroy(csr);
+  GIFT_API_END
+}
+
+int gift_csr_shape(const gift_csr* csr, int64_t* n, int64_t* nnz) {
+  GIFT_API_BEGIN
+  require(csr != nullptr, GIFT_ERR_VALUE, "null csr");
+  if (n) *n = csr->n;
+  if (nnz) *nnz = csr->nnz;
+  GIFT_API_END
+}
+
+int gift_csr_arrays(const gift_csr* csr, const int64_t** d_indptr, const int32_t** d_indices,
+                    const double** d_values) {
+  GIFT_API_BEGIN
+  require(csr != nullptr, GIFT_ERR_VALUE, "null csr");
+  if (d_indptr) *d_indptr = csr->indptr;
+  if (d_indices) *d_indices = csr->indices;
+  if (d_values) *d_values = csr->values;
+  GIFT_API_END
+}
+
+int gift_csr_download(gift_ctx* ctx, const gift_csr* csr, int64_t* h_indptr, int32_t* h_indices,
+                      double* h_values) {
+  GIFT_API_BEGIN
+  require(ctx && csr, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  if (h_indptr)
+    GIFT_CUDA(cudaMemcpyAsync(h_indptr, csr->indptr, (csr->n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+  if (h_indices && csr->nnz)
+    GIFT_CUDA(cudaMemcpyAsync(h_indices, csr->indices, csr->nnz * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+  if (h_values && csr->nnz)
+    GIFT_CUDA(cudaMemcpyAsync(h_values, csr->values, csr->nnz * sizeof(double), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+  GIFT_CUDA(cudaStreamSynchronize(ctx->stream));
+  GIFT_API_END
+}
+
+int gift_csr_degrees(gift_ctx* ctx, gift_csr* csr, const double** d_degrees) {
+  GIFT_API_BEGIN
+  require(ctx && csr && d_degrees, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  *d_degrees = gift::csr_degrees(ctx, csr);
+  GIFT_API_END
+}
+
+int gift_normalized_augmented_adjacency(gift_ctx* ctx, gift_csr* adj, double sigma, gift_csr** out) {
+  GIFT_API_BEGIN
+  require(ctx && adj && out, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  *out = static_cast<gift_csr*>(gift::normalized_augmented_adjacency(ctx, adj, sigma));
+  GIFT_API_END
+}
+
+int gift_csr_matmul(gift_ctx* ctx, const gift_csr* csr, int64_t ncols, const double* d_x, double* d_y) {
+  GIFT_API_BEGIN
+  require(ctx && csr, GIFT_ERR_VALUE, "null argument");
+  require(ncols >= 0, GIFT_ERR_DIMENSION, "negative column count");
+  DeviceGuard g(ctx->device);
+  gift::csr_matmul(ctx, csr, ncols, d_x, d_y);
+  GIFT_API_END
+}
+
+int gift_filter(gift_ctx* ctx, gift_csr* adj, int n_terms, const double* h_sigma, const int64_t* h_k,
+                const double* h_alpha, int64_t ncols, int in_dtype, const void* d_g, int out_dtype, void* d_out,
+                const uint8_t* d_fixed_mask, const double* d_fixed_pos, const double* h_region, int precision) {
+  GIFT_API_BEGIN
+  require(ctx && adj, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  gift::filter(ctx, adj, n_terms, h_sigma, h_k, h_alpha, ncols, in_dtype, d_g, out_dtype, d_out, d_fixed_mask,
+               d_fixed_pos, h_region, precision);
+  GIFT_API_END
+}
+
+int gift_filter_host(gift_ctx* ctx, gift_csr* adj, int n_terms, const double* h_sigma, const int64_t* h_k,
+                     const double* h_alpha, int64_t ncols, int in_dtype, const void* h_g, int out_dtype, void* h_out,
+                     const uint8_t* h_fixed_mask, const double* h_fixed_pos, const double* h_region, int precision) {
+  GIFT_API_BEGIN
+  require(ctx && adj, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const int64_t n = adj->n;
+  const size_t in_b = (size_t)(n * ncols) * (in_dtype == GIFT_DTYPE_F64 ? 8 : 4);
+  const size_t out_b = (size_t)(n * ncols) * (out_dtype == GIFT_DTYPE_F64 ? 8 : 4);
+  gift::DevBuf<char> dg(ctx, in_b), dout(ctx, out_b);
+  gift::DevBuf<uint8_t> dmask(ctx, h_fixed_mask ? n : 0);
+  gift::DevBuf<double> dpos(ctx, h_fixed_mask ? 2 * n : 0);
+  GIFT_CUDA(cudaMemcpyAsync(dg.p, h_g, in_b, cudaMemcpyHostToDevice, st));
+  if (h_fixed_mask) {
+    GIFT_CUDA(cudaMemcpyAsync(dmask.p, h_fixed_mask, n, cudaMemcpyHostToDevice, st));
+    GIFT_CUDA(cudaMemcpyAsync(dpos.p, h_fixed_pos, 2 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  gift::filter(ctx, adj, n_terms, h_sigma, h_k, h_alpha, ncols, in_dtype, dg.p, out_dtype, dout.p,
+               h_fixed_mask ? dmask.p : nullptr, h_fixed_mask ? dpos.p : nullptr, h_region, precision);
+  GIFT_CUDA(cudaMemcpyAsync(h_out, dout.p, out_b, cudaMemcpyDeviceToHost, st));
+  GIFT_CUDA(cudaStreamSynchronize(st));
+  GIFT_API_END
+}
+
+int gift_place_host(gift_ctx* ctx, int64_t n_cells, int64_t n_nets, const int64_t* h_net_start,
+                    const int32_t* h_pin_cell, int64_t max_clique_pins, int n_terms, const double* h_sigma,
+                    const int64_t* h_k, const double* h_alpha, const float* h_g, const uint8_t* h_fixed_mask,
+                    const double* h_fixed_pos, const double* h_region, int out_dtype, void* h_out, int precision,
+                    int64_t* nnz_out) {
+  GIFT_API_BEGIN
+  require(ctx && h_net_start, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = ctx->stream;
+  int64_t n_pins = h_net_start[n_nets];
+  gift::DevBuf<int64_t> dns(ctx, n_nets + 1);
+  gift::DevBuf<int32_t> dpc(ctx, n_pins);
+  GIFT_CUDA(cudaMemcpyAsync(dns.p, h_net_start, (n_nets + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  if (n_pins) GIFT_CUDA(cudaMemcpyAsync(dpc.p, h_pin_cell, n_pins * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  gift::Csr* c = gift::build_clique_graph(ctx, n_cells, n_nets, dns.p, dpc.p, max_clique_pins, nullptr);
+  dns.reset();
+  dpc.reset();
+  try {
+    const int64_t n = n_cells;
+    const size_t out_b = (size_t)(n * 2) * (out_dtype == GIFT_DTYPE_F64 ? 8 : 4);
+    gift::DevBuf<float> dg(ctx, 2 * n);
+    gift::DevBuf<char> dout(ctx, out_b);
+    gift::DevBuf<uint8_t> dmask(ctx, n);
+    gift::DevBuf<double> dpos(ctx, 2 * n);
+    GIFT_CUDA(cudaMemcpyAsync(dg.p, h_g, 2 * n * sizeof(float), cudaMemcpyHostToDevice, st));
+    if (h_fixed_mask) {
+      GIFT_CUDA(cudaMemcpyAsync(dmask.p, h_fixed_mask, n, cudaMemcpyHostToDevice, st));
+      GIFT_CUDA(cudaMemcpyAsync(dpos.p, h_fixed_pos, 2 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    gift::filter(ctx, c, n_terms, h_sigma, h_k, h_alpha, 2, GIFT_DTYPE_F32, dg.p, out_dtype, dout.p,
+                 h_fixed_mask ? dmask.p : nullptr, h_fixed_mask ? dpos.p : nullptr, h_region, precision);
+    GIFT_CUDA(cudaMemcpyAsync(h_out, dout.p, out_b, cudaMemcpyDeviceToHost, st));
+    GIFT_CUDA(cudaStreamSynchronize(st));
+    if (nnz_out) *nnz_out = c->nnz;
+  } catch (...) {
+    gift::csr_destroy(c);
+    throw;
+  }
+  gift::csr_destroy(c);
+  GIFT_API_END
+}
+
+}  // extern "C"

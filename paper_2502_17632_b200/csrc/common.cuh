@@ -1,0 +1,155 @@
+// common.cuh -- shared state, error plumbing and device-memory helpers of
+// libgiftb200.so (the C ABI in include/gift_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/gift_b200.h"
+
+namespace gift {
+
+// ---- error plumbing --------------------------------------------------------
+struct Error {
+  int code;
+  std::string msg;
+  int64_t arg;
+};
+
+void set_error(int code, const std::string& msg, int64_t arg = -1);
+int fail(int code, const std::string& msg, int64_t arg = -1);
+
+// Throwable error used inside the library; the ABI layer converts it into a
+// status code + thread-local message (no C++ exception crosses the ABI).
+struct GiftException {
+  int code;
+  std::string msg;
+  int64_t arg;
+};
+
+[[noreturn]] void throw_error(int code, const std::string& msg, int64_t arg = -1);
+void check_cuda(cudaError_t e, const char* what, const char* file, int line);
+
+#define GIFT_CUDA(x) ::gift::check_cuda((x), #x, __FILE__, __LINE__)
+#define GIFT_LAUNCH_CHECK(ctx)                                   \
+  do {                                                           \
+    ::gift::check_cuda(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
+    (ctx)->launches++;                                           \
+  } while (0)
+
+// ---- context ---------------------------------------------------------------
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = 0;
+  int64_t launches = 0;
+  int num_sms = 148;
+  // grow-only scratch arenas, reused across calls on this context
+  void* scratch[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t scratch_bytes[4] = {0, 0, 0, 0};
+  // pinned host staging for the *_host entry points
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  // launch timing (gift_ctx_set_profiling)
+  bool profiling = false;
+  struct Rec {
+    int kind;
+    int units;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+};
+
+// brackets one launch with events when ctx->profiling (see gift_ctx_set_profiling)
+struct ProfScope {
+  Ctx* ctx;
+  Ctx::Rec rec;
+  bool on;
+  ProfScope(Ctx* c, int kind, int units) : ctx(c), on(c->profiling) {
+    if (!on) return;
+    rec.kind = kind;
+    rec.units = units;
+    cudaEventCreate(&rec.a);
+    cudaEventCreate(&rec.b);
+    cudaEventRecord(rec.a, c->stream);
+  }
+  ~ProfScope() {
+    if (!on) return;
+    cudaEventRecord(rec.b, ctx->stream);
+    ctx->recs.push_back(rec);
+  }
+};
+
+// stream-ordered device allocation (default mempool, release threshold max)
+void* dev_alloc(Ctx* ctx, size_t bytes);
+void dev_free(Ctx* ctx, void* p);
+void* scratch(Ctx* ctx, int slot, size_t bytes);
+void* pinned(Ctx* ctx, size_t bytes);
+
+// RAII device buffer bound to a context stream
+template <typename T>
+struct DevBuf {
+  Ctx* ctx = nullptr;
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(Ctx* c, size_t count) : ctx(c), n(count) {
+    p = static_cast<T*>(dev_alloc(c, count * sizeof(T) + 16));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ctx(o.ctx), p(o.p), n(o.n) { o.p = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    reset();
+    ctx = o.ctx; p = o.p; n = o.n; o.p = nullptr;
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) dev_free(ctx, p);
+    p = nullptr;
+  }
+  T* release() { T* q = p; p = nullptr; return q; }
+};
+
+// ---- CSR -------------------------------------------------------------------
+// Symmetric CSR, immutable after construction (graph.py:48-111).
+// Structure and fp64 values are the reference's bit for bit; derived arrays
+// (degrees, fp32 hop weights, per-sigma scale vectors) are computed lazily
+// and cached, as SparseSymMatrix caches `degrees` (graph.py:89-94).
+struct Csr {
+  int device = 0;
+  int64_t n = 0;
+  int64_t nnz = 0;
+  int64_t* indptr = nullptr;   // [n+1]
+  int32_t* indices = nullptr;  // [nnz]
+  double* values = nullptr;    // [nnz]
+  bool has_diagonal = true;    // false when built by build_clique_graph (no self pairs)
+  double* degrees = nullptr;   // [n], lazy
+  float* w32 = nullptr;        // [nnz] fp32 weights for the fast hop, lazy
+  double mean_row = 0.0;
+  std::map<double, double*> s64;  // sigma -> 1/sqrt(d+sigma)   (fp64, exact)
+  std::map<double, float*> s32;   // sigma -> fp32 rounding of s64
+  std::vector<void*> owned;       // everything above, freed on destroy
+};
+
+void* csr_alloc(Ctx* ctx, Csr* c, size_t bytes);
+void csr_destroy(Csr* c);
+
+// ---- launch helpers --------------------------------------------------------
+inline unsigned grid_for(int64_t work, int block, int64_t cap = 148LL * 64) {
+  int64_t g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+inline int bit_length(uint64_t v) { return v == 0 ? 0 : 64 - __builtin_clzll(v); }
+
+}  // namespace gift
+
+struct gift_ctx : gift::Ctx {};
+struct gift_csr : gift::Csr {};

@@ -1,0 +1,782 @@
+// filter.cu -- degrees, normalisation and the GiFt filter bank on the GPU.
+//
+// Reference semantics (giftplace):
+//   SparseSymMatrix.degrees      graph.py:89-94   -> k_degrees (numpy pairwise order, fp64)
+//   normalized_augmented_adjacency graph.py:167-188 -> k_scale (s = 1/sqrt(d+sigma)),
+//                                                   k_normalized_fill (materialised, API only)
+//   SparseSymMatrix.matmul       graph.py:96-100  -> k_matvec_exact (csr_matvecs order)
+//   gift_filter                  gift.py:73-95    -> bank_fp64_exact / bank_fp32
+//   gift_place epilogue          gift.py:112-118  -> fused into the final hop
+//
+// The fast path (GIFT_PREC_FP32) never materialises A_sigma.  It runs the
+// pre-scaled recurrence on the raw clique weights w (one fp32 copy of the
+// CSR values serves every sigma):
+//     z_0 = s o x ;  y_h = s o (A z_{h-1} + sigma z_{h-1}) ;  z_h = s o y_h
+// (y_h == A_sigma^h x), and FUSES the sigma chains of the bank: chains are
+// packed side by side in the signal (float4 = two chains of an N x 2 signal)
+// so one pass over (col, w) advances every packed chain by one hop.  The
+// default bank (0.1 A_2^2 + 0.7 A_4^2 + 0.2 A_4^4, 6 algorithmic hops) reads
+// the matrix 4 times.  Term accumulation and the re-pin/clamp epilogue ride
+// in the epilogue of the hop that completes them.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace gift {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+// ---- numpy pairwise summation (loops_utils.h pairwise_sum), fp64 ---------
+__device__ __forceinline__ double pw_leaf(const double* __restrict__ a, int64_t n) {
+  if (n < 8) {
+    double res = -0.0;
+    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int64_t i;
+  for (i = 8; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+// explicit-stack form of: n <= 128 -> leaf; else n2 = n/2 - (n/2)%8,
+// PW(a, n2) + PW(a + n2, n - n2)
+__device__ double pw_sum(const double* __restrict__ a, int64_t n) {
+  if (n <= 128) return pw_leaf(a, n);
+  int64_t off[48], len[48];
+  double partial[48];
+  uint8_t stage[48];
+  int sp = 1;
+  off[0] = 0;
+  len[0] = n;
+  stage[0] = 0;
+  double ret = 0.0;
+  while (sp > 0) {
+    const int i = sp - 1;
+    if (len[i] <= 128) {
+      ret = pw_leaf(a + off[i], len[i]);
+      --sp;
+      continue;
+    }
+    int64_t n2 = len[i] / 2;
+    n2 -= n2 % 8;
+    if (stage[i] == 0) {
+      stage[i] = 1;
+      off[sp] = off[i];
+      len[sp] = n2;
+      stage[sp] = 0;
+      ++sp;
+    } else if (stage[i] == 1) {
+      partial[i] = ret;
+      stage[i] = 2;
+      off[sp] = off[i] + n2;
+      len[sp] = len[i] - n2;
+      stage[sp] = 0;
+      ++sp;
+    } else {
+      ret = __dadd_rn(partial[i], ret);
+      --sp;
+    }
+  }
+  return ret;
+}
+
+// np.add.reduceat(values, indptr[nonempty]) per row: v0 + PW(v[1:])
+__global__ void k_degrees(int64_t n, const int64_t* __restrict__ indptr, const double* __restrict__ values,
+                          double* __restrict__ deg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = indptr[i], L = indptr[i + 1] - a;
+    deg[i] = L == 0 ? 0.0 : __dadd_rn(values[a], pw_sum(values + a + 1, L - 1));
+  }
+}
+
+// graph.py:184: s = 1.0 / np.sqrt(deg + sigma) (three correctly rounded ops)
+__global__ void k_scale(int64_t n, const double* __restrict__ deg, double sigma, double* __restrict__ s64,
+                        float* __restrict__ s32) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(deg[i], sigma)));
+    s64[i] = s;
+    if (s32) s32[i] = __double2float_rn(s);
+  }
+}
+
+__global__ void k_first_isolated(int64_t n, const double* __restrict__ deg, unsigned long long* __restrict__ first) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (deg[i] <= 0) atomicMin(first, (unsigned long long)i);
+}
+
+__global__ void k_to_f32(int64_t m, const double* __restrict__ v, float* __restrict__ w) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    w[i] = __double2float_rn(v[i]);
+}
+
+// does row i already store a diagonal entry (only from_coo matrices can)?
+__device__ __forceinline__ bool row_has_diag(const int64_t* indptr, const int32_t* idx, int64_t i) {
+  int64_t lo = indptr[i], hi = indptr[i + 1];
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (idx[mid] < i) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo < indptr[i + 1] && idx[lo] == i;
+}
+
+__global__ void k_diag_extra(int64_t n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                             bool may_have_diag, int64_t* __restrict__ extra) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
+    extra[i] = (i < n) ? ((may_have_diag && row_has_diag(indptr, idx, i)) ? 0 : 1) : 0;
+}
+
+__global__ void k_shift_ptr(int64_t n1, const int64_t* __restrict__ indptr, const int64_t* __restrict__ off,
+                            int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n1; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = indptr[i] + off[i];
+}
+
+// graph.py:182-187: A + sigma I (diagonal enters at its sorted position as
+// 0 + sigma, or a_ii + sigma), then (a * s_i) * s_j
+__global__ void k_normalized_fill(int64_t n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                                  const double* __restrict__ val, const double* __restrict__ s, double sigma,
+                                  const int64_t* __restrict__ optr, int32_t* __restrict__ oidx,
+                                  double* __restrict__ oval) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t k = optr[i];
+    const double si = s[i];
+    bool diag_done = !(sigma > 0);
+    for (int64_t jj = indptr[i]; jj < indptr[i + 1]; ++jj) {
+      int64_t j = idx[jj];
+      if (!diag_done && j > i) {
+        oidx[k] = (int32_t)i;
+        oval[k] = __dmul_rn(__dmul_rn(sigma, si), si);
+        ++k;
+        diag_done = true;
+      }
+      double a = val[jj];
+      if (!diag_done && j == i) {
+        a = __dadd_rn(a, sigma);
+        diag_done = true;
+      }
+      oidx[k] = (int32_t)j;
+      oval[k] = __dmul_rn(__dmul_rn(a, si), s[j]);
+      ++k;
+    }
+    if (!diag_done) {
+      oidx[k] = (int32_t)i;
+      oval[k] = __dmul_rn(__dmul_rn(sigma, si), si);
+    }
+  }
+}
+
+// ---- exact fp64 SpMM: scipy csr_matvecs order ------------------------------
+// y[i, c] = 0; y[i, c] += a_ij * x[j, c] over ascending storage order, no FMA.
+// MODE 0: a_ij = stored value.  MODE 1: on-the-fly A_sigma entry
+// (a*s_i)*s_j with the sigma diagonal at its sorted position, i.e. exactly
+// the value the reference materialises (graph.py:182-187).
+template <int MODE>
+__global__ void k_matvec_exact(int64_t n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                               const double* __restrict__ val, const double* __restrict__ s, double sigma,
+                               int64_t ld, int64_t c0, int nc, const double* __restrict__ x,
+                               double* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const double si = MODE ? s[i] : 0.0;
+    bool diag_done = MODE ? !(sigma > 0) : true;
+    for (int64_t jj = indptr[i]; jj < indptr[i + 1]; ++jj) {
+      const int64_t j = idx[jj];
+      double a = val[jj];
+      if (MODE) {
+        if (!diag_done && j > i) {
+          const double d = __dmul_rn(__dmul_rn(sigma, si), si);
+          for (int c = 0; c < nc; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(d, x[i * ld + c0 + c]));
+          diag_done = true;
+        }
+        if (!diag_done && j == i) {
+          a = __dadd_rn(a, sigma);
+          diag_done = true;
+        }
+        a = __dmul_rn(__dmul_rn(a, si), s[j]);
+      }
+      for (int c = 0; c < nc; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(a, x[j * ld + c0 + c]));
+    }
+    if (MODE && !diag_done) {
+      const double d = __dmul_rn(__dmul_rn(sigma, si), si);
+      for (int c = 0; c < nc; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(d, x[i * ld + c0 + c]));
+    }
+    for (int c = 0; c < nc; ++c) y[i * ld + c0 + c] = acc[c];
+  }
+}
+
+// out += alpha * p  (numpy: temp = alpha * power; out += temp), elementwise fp64
+__global__ void k_axpy_exact(int64_t m, double alpha, const double* __restrict__ p, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __dadd_rn(out[i], __dmul_rn(alpha, p[i]));
+}
+
+__global__ void k_load_f64(int64_t m, int in_dtype, const void* __restrict__ g, double* __restrict__ x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = in_dtype == GIFT_DTYPE_F64 ? static_cast<const double*>(g)[i]
+                                      : (double)static_cast<const float*>(g)[i];
+}
+
+// np.clip for floats: MIN(MAX(x, lo), hi), NaN passes, PyArray_MAX(a,b) = a > b ? a : b
+__device__ __forceinline__ double np_clip(double x, double lo, double hi) {
+  double t = isnan(x) ? x : (x > lo ? x : lo);
+  return isnan(t) ? t : (t < hi ? t : hi);
+}
+
+struct Region4 {
+  double v[4];
+};
+
+// gift.py:112-118 on an fp64 [n, 2] result, written in out_dtype
+__global__ void k_epilogue_f64(int64_t n, int64_t ncols, const double* __restrict__ res,
+                               const uint8_t* __restrict__ fixed_mask, const double* __restrict__ fixed_pos,
+                               Region4 reg, int out_dtype, void* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * ncols;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = res[i];
+    if (fixed_mask) {
+      const int64_t r = i / 2;
+      const int c = (int)(i % 2);
+      v = fixed_mask[r] ? fixed_pos[i] : np_clip(v, reg.v[c], reg.v[c + 2]);
+    }
+    if (out_dtype == GIFT_DTYPE_F64) static_cast<double*>(out)[i] = v;
+    else static_cast<float*>(out)[i] = __double2float_rn(v);
+  }
+}
+
+// ---- fp32 fused hop ---------------------------------------------------------
+struct ChainArgs {
+  const float* s;  // fp32 s_sigma
+  float sigma;
+  int cont;        // slot of this chain in zout, -1 if the chain ends here
+  int has_term;    // a term of this chain completes at this hop
+  float alpha;     // its weight (sum if several terms share k)
+};
+
+struct HopArgs {
+  const int64_t* rowptr;
+  const int32_t* col;
+  const float* w;
+  int64_t n;
+  const float* zin;  // [n, FIN]
+  float* zout;       // [n, FOUT]
+  int wcols;         // signal columns per chain
+  int nch;           // chains packed in zin
+  ChainArgs ch[4];
+  float* acc;        // [n, wcols] fp32 bank accumulator
+  int acc_read;      // 0: first write (out = zeros + ...)
+  int is_final;
+  int out_dtype;
+  void* out;
+  int64_t out_ld;
+  int64_t out_c0;
+  const uint8_t* fixed_mask;
+  const double* fixed_pos;
+  Region4 reg;
+  int any_term;
+};
+
+template <int F>
+struct VecF;
+template <>
+struct VecF<1> {
+  float v[1];
+};
+template <>
+struct VecF<2> {
+  float v[2];
+};
+template <>
+struct VecF<4> {
+  float v[4];
+};
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// streamed once per hop: skip L1, evict first from L2
+__device__ __forceinline__ int32_t ld_stream_s32(const int32_t* p, uint64_t pol) {
+  int32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float ld_stream_f32(const float* p, uint64_t pol) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
+// gathered signal rows: L1-allocating, keep in L2
+template <int F>
+__device__ __forceinline__ VecF<F> ld_z(const float* p, uint64_t pol);
+template <>
+__device__ __forceinline__ VecF<1> ld_z<1>(const float* p, uint64_t pol) {
+  VecF<1> r;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r.v[0]) : "l"(p), "l"(pol));
+  return r;
+}
+template <>
+__device__ __forceinline__ VecF<2> ld_z<2>(const float* p, uint64_t pol) {
+  VecF<2> r;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+               : "=f"(r.v[0]), "=f"(r.v[1])
+               : "l"(p), "l"(pol));
+  return r;
+}
+template <>
+__device__ __forceinline__ VecF<4> ld_z<4>(const float* p, uint64_t pol) {
+  VecF<4> r;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+// One hop for every chain packed in zin. G lanes per row reduce with a fixed
+// xor-butterfly (deterministic order); lane 0 runs the row epilogue.
+template <int FIN, int FOUT, int G>
+__global__ void __launch_bounds__(kBlock) k_hop(HopArgs a) {
+  const int lane = threadIdx.x & (G - 1);
+  const int64_t row = (blockIdx.x * (int64_t)kBlock + threadIdx.x) / G;
+  if (row >= a.n) return;  // uniform within a row group
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  const uint64_t pol_s = policy_evict_first();
+  const uint64_t pol_z = policy_evict_last();
+  const int64_t beg = a.rowptr[row], end = a.rowptr[row + 1];
+  float acc[FIN];
+#pragma unroll
+  for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
+  for (int64_t k = beg + lane; k < end; k += G) {
+    const int32_t c = ld_stream_s32(a.col + k, pol_s);
+    const float wk = ld_stream_f32(a.w + k, pol_s);
+    const VecF<FIN> z = ld_z<FIN>(a.zin + (int64_t)c * FIN, pol_z);
+#pragma unroll
+    for (int f = 0; f < FIN; ++f) acc[f] = fmaf(wk, z.v[f], acc[f]);
+  }
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) {
+#pragma unroll
+    for (int f = 0; f < FIN; ++f) acc[f] += __shfl_xor_sync(gmask, acc[f], off, G);
+  }
+  if (lane != 0) return;
+  const VecF<FIN> zi = ld_z<FIN>(a.zin + row * FIN, pol_z);
+  float o[4] = {0.f, 0.f, 0.f, 0.f};
+  if (a.any_term && a.acc_read)
+    for (int cc = 0; cc < a.wcols; ++cc) o[cc] = a.acc[row * a.wcols + cc];
+  float zo[FOUT > 0 ? FOUT : 1];
+#pragma unroll
+  for (int f = 0; f < (FOUT > 0 ? FOUT : 1); ++f) zo[f] = 0.f;
+#pragma unroll
+  for (int f = 0; f < FIN; ++f) {
+    const int chn = f / a.wcols;
+    if (chn >= a.nch) break;
+    const int cc = f - chn * a.wcols;
+    const ChainArgs& ch = a.ch[chn];
+    const float si = ch.s[row];
+    const float y = si * (acc[f] + ch.sigma * zi.v[f]);
+    if (FOUT > 0 && ch.cont >= 0) zo[(ch.cont * a.wcols + cc) % (FOUT > 0 ? FOUT : 1)] = si * y;
+    if (ch.has_term) o[cc] = fmaf(ch.alpha, y, o[cc]);
+  }
+  if constexpr (FOUT == 4) *reinterpret_cast<float4*>(a.zout + row * 4) = make_float4(zo[0], zo[1], zo[2], zo[3]);
+  else if constexpr (FOUT == 2) *reinterpret_cast<float2*>(a.zout + row * 2) = make_float2(zo[0], zo[1]);
+  else if constexpr (FOUT == 1) a.zout[row] = zo[0];
+  if (!a.any_term) return;
+  if (!a.is_final) {
+    for (int cc = 0; cc < a.wcols; ++cc) a.acc[row * a.wcols + cc] = o[cc];
+    return;
+  }
+  for (int cc = 0; cc < a.wcols; ++cc) {
+    double v = (double)o[cc];
+    if (a.fixed_mask) v = a.fixed_mask[row] ? a.fixed_pos[row * 2 + cc] : np_clip(v, a.reg.v[cc], a.reg.v[cc + 2]);
+    const int64_t oi = row * a.out_ld + a.out_c0 + cc;
+    if (a.out_dtype == GIFT_DTYPE_F64) static_cast<double*>(a.out)[oi] = v;
+    else static_cast<float*>(a.out)[oi] = __double2float_rn(v);
+  }
+}
+
+// z0[i, chn*wcols + cc] = s_chn[i] * g[i, c0 + cc]
+template <int F>
+__global__ void k_prep(int64_t n, int wcols, int nch, const float* s0, const float* s1, const float* s2,
+                       const float* s3, int in_dtype, const void* __restrict__ g, int64_t ld, int64_t c0,
+                       float* __restrict__ z) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float v[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      const int chn = f / wcols, cc = f - chn * wcols;
+      float x = 0.f, s = 0.f;
+      if (chn < nch) {
+        const int64_t gi = i * ld + c0 + cc;
+        x = in_dtype == GIFT_DTYPE_F64 ? (float)static_cast<const double*>(g)[gi] : static_cast<const float*>(g)[gi];
+        s = (chn == 0 ? s0 : chn == 1 ? s1 : chn == 2 ? s2 : s3)[i];
+      }
+      v[f] = s * x;
+    }
+    if constexpr (F == 4) *reinterpret_cast<float4*>(z + i * 4) = make_float4(v[0], v[1], v[2], v[3]);
+    else if constexpr (F == 2) *reinterpret_cast<float2*>(z + i * 2) = make_float2(v[0], v[1]);
+    else z[i] = v[0];
+  }
+}
+
+int pow2_ceil(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+template <int FIN, int FOUT>
+void launch_hop_g(Ctx* ctx, const HopArgs& a, int G) {
+  const int64_t threads = a.n * (int64_t)G;
+  const unsigned grid = (unsigned)((threads + kBlock - 1) / kBlock);
+  cudaStream_t st = ctx->stream;
+  switch (G) {
+    case 4: k_hop<FIN, FOUT, 4><<<grid, kBlock, 0, st>>>(a); break;
+    case 8: k_hop<FIN, FOUT, 8><<<grid, kBlock, 0, st>>>(a); break;
+    case 16: k_hop<FIN, FOUT, 16><<<grid, kBlock, 0, st>>>(a); break;
+    default: k_hop<FIN, FOUT, 32><<<grid, kBlock, 0, st>>>(a); break;
+  }
+  GIFT_LAUNCH_CHECK(ctx);
+}
+
+template <int FIN>
+void launch_hop_out(Ctx* ctx, const HopArgs& a, int fout, int G) {
+  switch (fout) {
+    case 0: launch_hop_g<FIN, 0>(ctx, a, G); break;
+    case 1: launch_hop_g<FIN, 1>(ctx, a, G); break;
+    case 2: launch_hop_g<FIN, 2>(ctx, a, G); break;
+    default: launch_hop_g<FIN, 4>(ctx, a, G); break;
+  }
+}
+
+void launch_hop(Ctx* ctx, const HopArgs& a, int fin, int fout, int G) {
+  ProfScope prof(ctx, fin, a.nch);
+  switch (fin) {
+    case 1: launch_hop_out<1>(ctx, a, fout, G); break;
+    case 2: launch_hop_out<2>(ctx, a, fout, G); break;
+    default: launch_hop_out<4>(ctx, a, fout, G); break;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+const double* csr_degrees(Ctx* ctx, Csr* c) {
+  if (!c->degrees) {
+    c->degrees = static_cast<double*>(csr_alloc(ctx, c, (c->n > 0 ? c->n : 1) * sizeof(double)));
+    if (c->n > 0) {
+      k_degrees<<<grid_for(c->n, kBlock, 1LL << 30), kBlock, 0, ctx->stream>>>(c->n, c->indptr, c->values,
+                                                                             c->degrees);
+      GIFT_LAUNCH_CHECK(ctx);
+    }
+  }
+  return c->degrees;
+}
+
+static const float* csr_w32(Ctx* ctx, Csr* c) {
+  if (!c->w32) {
+    c->w32 = static_cast<float*>(csr_alloc(ctx, c, (c->nnz > 0 ? c->nnz : 1) * sizeof(float)));
+    if (c->nnz > 0) {
+      k_to_f32<<<grid_for(c->nnz, kBlock), kBlock, 0, ctx->stream>>>(c->nnz, c->values, c->w32);
+      GIFT_LAUNCH_CHECK(ctx);
+    }
+  }
+  return c->w32;
+}
+
+// sigma validation + isolated-node check (graph.py:174-180); returns s64
+static const double* csr_scale(Ctx* ctx, Csr* c, double sigma) {
+  if (!(sigma >= 0)) throw_error(GIFT_ERR_VALUE, "sigma must be >= 0, got " + std::to_string(sigma));
+  auto it = c->s64.find(sigma);
+  if (it != c->s64.end()) return it->second;
+  const double* deg = csr_degrees(ctx, c);
+  if (sigma == 0 && c->n > 0) {
+    DevBuf<unsigned long long> first(ctx, 1);
+    GIFT_CUDA(cudaMemsetAsync(first.p, 0xff, sizeof(unsigned long long), ctx->stream));
+    k_first_isolated<<<grid_for(c->n, kBlock), kBlock, 0, ctx->stream>>>(c->n, deg, first.p);
+    GIFT_LAUNCH_CHECK(ctx);
+    unsigned long long h;
+    GIFT_CUDA(cudaMemcpyAsync(&h, first.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    GIFT_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h != ~0ULL) {
+      throw_error(GIFT_ERR_ISOLATED_NODE,
+                  "node " + std::to_string(h) +
+                      " has degree 0; normalization with sigma=0 is undefined (use sigma > 0 to absorb isolated nodes)",
+                  (int64_t)h);
+    }
+  }
+  double* s64 = static_cast<double*>(csr_alloc(ctx, c, (c->n > 0 ? c->n : 1) * sizeof(double)));
+  float* s32 = static_cast<float*>(csr_alloc(ctx, c, (c->n > 0 ? c->n : 1) * sizeof(float)));
+  if (c->n > 0) {
+    k_scale<<<grid_for(c->n, kBlock), kBlock, 0, ctx->stream>>>(c->n, deg, sigma, s64, s32);
+    GIFT_LAUNCH_CHECK(ctx);
+  }
+  c->s64[sigma] = s64;
+  c->s32[sigma] = s32;
+  return s64;
+}
+
+Csr* normalized_augmented_adjacency(Ctx* ctx, Csr* c, double sigma) {
+  const double* s = csr_scale(ctx, c, sigma);
+  cudaStream_t st = ctx->stream;
+  const int64_t n = c->n;
+  DevBuf<int64_t> extra(ctx, n + 1), off(ctx, n + 1);
+  int64_t add = 0;
+  if (sigma > 0) {
+    k_diag_extra<<<grid_for(n + 1, kBlock), kBlock, 0, st>>>(n, c->indptr, c->indices, c->has_diagonal, extra.p);
+    GIFT_LAUNCH_CHECK(ctx);
+    size_t bytes = 0;
+    GIFT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, extra.p, off.p, n + 1, st));
+    DevBuf<char> tmp(ctx, bytes);
+    GIFT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, extra.p, off.p, n + 1, st));
+    ctx->launches += 2;
+    GIFT_CUDA(cudaMemcpyAsync(&add, off.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GIFT_CUDA(cudaStreamSynchronize(st));
+  } else {
+    GIFT_CUDA(cudaMemsetAsync(off.p, 0, (n + 1) * sizeof(int64_t), st));
+  }
+  Csr* o = new gift_csr();
+  o->device = ctx->device;
+  o->n = n;
+  o->nnz = c->nnz + add;
+  o->indptr = static_cast<int64_t*>(csr_alloc(ctx, o, (n + 1) * sizeof(int64_t)));
+  o->indices = static_cast<int32_t*>(csr_alloc(ctx, o, (o->nnz > 0 ? o->nnz : 1) * sizeof(int32_t)));
+  o->values = static_cast<double*>(csr_alloc(ctx, o, (o->nnz > 0 ? o->nnz : 1) * sizeof(double)));
+  o->has_diagonal = c->has_diagonal || sigma > 0;
+  o->mean_row = n > 0 ? (double)o->nnz / n : 0.0;
+  k_shift_ptr<<<grid_for(n + 1, kBlock), kBlock, 0, st>>>(n + 1, c->indptr, off.p, o->indptr);
+  GIFT_LAUNCH_CHECK(ctx);
+  if (n > 0) {
+    k_normalized_fill<<<grid_for(n, kBlock), kBlock, 0, st>>>(n, c->indptr, c->indices, c->values, s, sigma,
+                                                              o->indptr, o->indices, o->values);
+    GIFT_LAUNCH_CHECK(ctx);
+  }
+  return o;
+}
+
+void csr_matmul(Ctx* ctx, const Csr* c, int64_t ncols, const double* x, double* y) {
+  if (c->n == 0 || ncols == 0) return;
+  for (int64_t c0 = 0; c0 < ncols; c0 += 4) {
+    const int nc = (int)std::min<int64_t>(4, ncols - c0);
+    k_matvec_exact<0><<<grid_for(c->n, kBlock, 1LL << 30), kBlock, 0, ctx->stream>>>(
+        c->n, c->indptr, c->indices, c->values, nullptr, 0.0, ncols, c0, nc, x, y);
+    GIFT_LAUNCH_CHECK(ctx);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Bank planning shared by both precisions: terms grouped by sigma in
+// first-appearance order, each group's terms sorted by k (stable), as
+// gift.py:83-93 does.
+struct TermGroup {
+  double sigma;
+  std::vector<std::pair<int64_t, double>> terms;  // (k, alpha), stable-sorted by k
+  int64_t maxk;
+};
+
+static std::vector<TermGroup> plan_groups(int n_terms, const double* sigma, const int64_t* k, const double* alpha) {
+  if (n_terms <= 0) throw_error(GIFT_ERR_VALUE, "filter needs at least one term");
+  std::vector<TermGroup> groups;
+  for (int t = 0; t < n_terms; ++t) {
+    if (!(sigma[t] >= 0)) throw_error(GIFT_ERR_VALUE, "sigma must be >= 0, got " + std::to_string(sigma[t]));
+    if (k[t] < 1) throw_error(GIFT_ERR_VALUE, "power k must be >= 1, got " + std::to_string(k[t]));
+    auto it = std::find_if(groups.begin(), groups.end(), [&](const TermGroup& g) { return g.sigma == sigma[t]; });
+    if (it == groups.end()) {
+      groups.push_back({sigma[t], {}, 0});
+      it = groups.end() - 1;
+    }
+    it->terms.push_back({k[t], alpha[t]});
+  }
+  for (auto& g : groups) {
+    std::stable_sort(g.terms.begin(), g.terms.end(),
+                     [](const std::pair<int64_t, double>& a, const std::pair<int64_t, double>& b) {
+                       return a.first < b.first;
+                     });
+    g.maxk = g.terms.back().first;
+  }
+  return groups;
+}
+
+// GIFT_PREC_FP64_EXACT: the reference's operation order, bit for bit.
+static void bank_fp64_exact(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, int64_t ncols, int in_dtype,
+                            const void* g, int out_dtype, void* out, const uint8_t* fixed_mask,
+                            const double* fixed_pos, const double* region) {
+  cudaStream_t st = ctx->stream;
+  const int64_t n = c->n, m = n * ncols;
+  for (auto& grp : groups) csr_scale(ctx, c, grp.sigma);  // raise before any work, like the reference would
+  if (m == 0) return;
+  DevBuf<double> x(ctx, m), pa(ctx, m), pb(ctx, m), acc(ctx, m);
+  k_load_f64<<<grid_for(m, kBlock), kBlock, 0, st>>>(m, in_dtype, g, x.p);
+  GIFT_LAUNCH_CHECK(ctx);
+  GIFT_CUDA(cudaMemsetAsync(acc.p, 0, m * sizeof(double), st));
+  for (auto& grp : groups) {
+    const double* s = c->s64[grp.sigma];
+    const double* power = x.p;
+    int64_t done = 0;
+    for (auto& term : grp.terms) {
+      for (int64_t h = done; h < term.first; ++h) {
+        double* dst = (power == pa.p) ? pb.p : pa.p;
+        for (int64_t c0 = 0; c0 < ncols; c0 += 4) {
+          const int nc = (int)std::min<int64_t>(4, ncols - c0);
+          k_matvec_exact<1><<<grid_for(n, kBlock, 1LL << 30), kBlock, 0, st>>>(
+              n, c->indptr, c->indices, c->values, s, grp.sigma, ncols, c0, nc, power, dst);
+          GIFT_LAUNCH_CHECK(ctx);
+        }
+        power = dst;
+      }
+      done = std::max(done, term.first);
+      k_axpy_exact<<<grid_for(m, kBlock), kBlock, 0, st>>>(m, term.second, power, acc.p);
+      GIFT_LAUNCH_CHECK(ctx);
+    }
+  }
+  Region4 reg{};
+  if (region) memcpy(reg.v, region, sizeof(reg.v));
+  k_epilogue_f64<<<grid_for(m, kBlock), kBlock, 0, st>>>(n, ncols, acc.p, fixed_mask, fixed_pos, reg, out_dtype, out);
+  GIFT_LAUNCH_CHECK(ctx);
+}
+
+static int pick_group_lanes(double mean_row) {
+  if (mean_row < 12) return 4;
+  if (mean_row < 40) return 8;
+  if (mean_row < 100) return 16;
+  return 32;
+}
+
+// GIFT_PREC_FP32: fused pre-scaled bank.
+static void bank_fp32(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, int64_t ncols, int in_dtype,
+                      const void* g, int out_dtype, void* out, const uint8_t* fixed_mask, const double* fixed_pos,
+                      const double* region) {
+  const int64_t n = c->n;
+  for (auto& grp : groups) csr_scale(ctx, c, grp.sigma);
+  if (n == 0 || ncols == 0) return;
+  const float* w = csr_w32(ctx, c);
+  const int G = pick_group_lanes(c->mean_row);
+  Region4 reg{};
+  if (region) memcpy(reg.v, region, sizeof(reg.v));
+  // column slices of <= 4 columns; chains of a slice packed <= 4 floats per row
+  for (int64_t c0 = 0; c0 < ncols; c0 += 4) {
+    const int wcols = (int)std::min<int64_t>(4, ncols - c0);
+    const int per = std::max(1, 4 / wcols);
+    float* zA = static_cast<float*>(scratch(ctx, 0, n * 4 * sizeof(float) + 64));
+    float* zB = static_cast<float*>(scratch(ctx, 1, n * 4 * sizeof(float) + 64));
+    float* accb = static_cast<float*>(scratch(ctx, 2, n * 4 * sizeof(float) + 64));
+    bool acc_written = false;
+    for (size_t g0 = 0; g0 < groups.size(); g0 += per) {
+      const int nch = (int)std::min<size_t>(per, groups.size() - g0);
+      const bool last_pack = g0 + nch >= groups.size();
+      const float* sp[4] = {nullptr, nullptr, nullptr, nullptr};
+      int64_t maxk = 0;
+      for (int j = 0; j < nch; ++j) {
+        sp[j] = c->s32[groups[g0 + j].sigma];
+        maxk = std::max(maxk, groups[g0 + j].maxk);
+      }
+      const int F0 = pow2_ceil(wcols * nch);
+      {
+        ProfScope prof(ctx, 0, nch);
+        const unsigned grid = grid_for(n, kBlock, 1LL << 30);
+        switch (F0) {
+          case 1: k_prep<1><<<grid, kBlock, 0, ctx->stream>>>(n, wcols, nch, sp[0], sp[1], sp[2], sp[3], in_dtype, g, ncols, c0, zA); break;
+          case 2: k_prep<2><<<grid, kBlock, 0, ctx->stream>>>(n, wcols, nch, sp[0], sp[1], sp[2], sp[3], in_dtype, g, ncols, c0, zA); break;
+          default: k_prep<4><<<grid, kBlock, 0, ctx->stream>>>(n, wcols, nch, sp[0], sp[1], sp[2], sp[3], in_dtype, g, ncols, c0, zA); break;
+        }
+        GIFT_LAUNCH_CHECK(ctx);
+      }
+      // active chains (indices into groups) in packing order
+      std::vector<int> active;
+      for (int j = 0; j < nch; ++j) active.push_back((int)g0 + j);
+      float* zin = zA;
+      float* zout = zB;
+      for (int64_t h = 1; h <= maxk; ++h) {
+        HopArgs a{};
+        a.rowptr = c->indptr;
+        a.col = c->indices;
+        a.w = w;
+        a.n = n;
+        a.zin = zin;
+        a.zout = zout;
+        a.wcols = wcols;
+        a.nch = (int)active.size();
+        std::vector<int> next;
+        for (size_t j = 0; j < active.size(); ++j) {
+          const TermGroup& grp = groups[active[j]];
+          ChainArgs& ch = a.ch[j];
+          ch.s = c->s32[grp.sigma];
+          ch.sigma = (float)grp.sigma;
+          double al = 0.0;
+          int has = 0;
+          for (auto& t : grp.terms)
+            if (t.first == h) {
+              al += t.second;
+              has = 1;
+            }
+          ch.has_term = has;
+          ch.alpha = (float)al;
+          a.any_term |= has;
+          if (grp.maxk > h) {
+            ch.cont = (int)next.size();
+            next.push_back(active[j]);
+          } else {
+            ch.cont = -1;
+          }
+        }
+        const int fin = pow2_ceil(wcols * (int)active.size());
+        const int fout = next.empty() ? 0 : pow2_ceil(wcols * (int)next.size());
+        a.acc = accb;
+        a.acc_read = acc_written ? 1 : 0;
+        a.is_final = (last_pack && h == maxk) ? 1 : 0;
+        a.out_dtype = out_dtype;
+        a.out = out;
+        a.out_ld = ncols;
+        a.out_c0 = c0;
+        a.fixed_mask = fixed_mask;
+        a.fixed_pos = fixed_pos;
+        a.reg = reg;
+        launch_hop(ctx, a, fin, fout, G);
+        if (a.any_term) acc_written = true;
+        active.swap(next);
+        std::swap(zin, zout);
+      }
+    }
+  }
+}
+
+void filter(Ctx* ctx, Csr* c, int n_terms, const double* sigma, const int64_t* k, const double* alpha, int64_t ncols,
+            int in_dtype, const void* g, int out_dtype, void* out, const uint8_t* fixed_mask, const double* fixed_pos,
+            const double* region, int precision) {
+  if (ncols < 0) throw_error(GIFT_ERR_DIMENSION, "negative column count");
+  if (fixed_mask && ncols != 2) throw_error(GIFT_ERR_DIMENSION, "the placement epilogue needs an N x 2 signal");
+  if (fixed_mask && !region) throw_error(GIFT_ERR_VALUE, "region required with a fixed mask");
+  if (in_dtype != GIFT_DTYPE_F32 && in_dtype != GIFT_DTYPE_F64) throw_error(GIFT_ERR_VALUE, "bad input dtype");
+  if (out_dtype != GIFT_DTYPE_F32 && out_dtype != GIFT_DTYPE_F64) throw_error(GIFT_ERR_VALUE, "bad output dtype");
+  auto groups = plan_groups(n_terms, sigma, k, alpha);
+  if (precision == GIFT_PREC_FP64_EXACT)
+    bank_fp64_exact(ctx, c, groups, ncols, in_dtype, g, out_dtype, out, fixed_mask, fixed_pos, region);
+  else if (precision == GIFT_PREC_FP32)
+    bank_fp32(ctx, c, groups, ncols, in_dtype, g, out_dtype, out, fixed_mask, fixed_pos, region);
+  else
+    throw_error(GIFT_ERR_VALUE, "unknown precision");
+}
+
+}  // namespace gift

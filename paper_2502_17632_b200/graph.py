@@ -1,0 +1,296 @@
+"""Clique-model circuit graph and its operators, resident on the B200.
+
+Drop-in for the hot-path half of `giftplace/graph.py`:
+
+    FilterTerm                      graph.py:33-45
+    SparseSymMatrix                 graph.py:48-111   (GPU-resident CSR; host mirrors are lazy)
+    from_coo                        graph.py:114-117
+    build_clique_graph              graph.py:120-158
+    normalized_augmented_adjacency  graph.py:167-188
+    apply_operator_power            graph.py:196-206
+
+Every numeric step runs in libgiftb200.so (CUDA, sm_100a).  Structure, fp64
+values and fp64 degrees are bit-identical to the reference; `matmul` and
+`apply_operator_power` reproduce scipy's csr_matvecs summation order in
+fp64, so they are bit-identical too.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import logging
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import DimensionMismatchError, NonSymmetricError, TooLargeForDenseError
+from .netlist import pin_arrays
+
+log = logging.getLogger(__name__)
+
+DENSE_LIMIT = 2000  # max n for dense conversions (graph.py:30)
+
+
+@dataclass(frozen=True)
+class FilterTerm:
+    """One alpha * (A_sigma)^k term of the multi-frequency filter."""
+
+    sigma: float
+    k: int
+    alpha: float
+
+    def __post_init__(self) -> None:
+        if self.sigma < 0:
+            raise ValueError(f"sigma must be >= 0, got {self.sigma}")
+        if self.k < 1:
+            raise ValueError(f"power k must be >= 1, got {self.k}")
+
+
+class SparseSymMatrix:
+    """Immutable symmetric CSR living in device memory.
+
+    Construct from any scipy sparse matrix / dense array (canonicalised and
+    symmetry-checked on the GPU exactly as graph.py:55-65 does), or get one
+    from `build_clique_graph`, `from_coo` or `normalized_augmented_adjacency`.
+    `indptr` / `indices` / `values` / `degrees` are numpy mirrors copied from
+    the device on first access (scipy's index dtype rule: int32 iff
+    max(nnz, n) < 2**31).
+    """
+
+    def __init__(self, csr, check: bool = True):
+        import scipy.sparse as sp
+
+        m = sp.csr_matrix(csr)
+        if m.shape[0] != m.shape[1]:
+            raise NonSymmetricError(f"matrix is {m.shape[0]}x{m.shape[1]}, not square")
+        n = m.shape[0]
+        counts = np.diff(m.indptr).astype(np.int64)
+        rows = np.repeat(np.arange(n, dtype=np.int64), counts)
+        h = _coo_handle(n, rows, m.indices.astype(np.int64), m.data.astype(np.float64), check)
+        self._init_handle(h)
+
+    @classmethod
+    def _from_handle(cls, handle: int) -> "SparseSymMatrix":
+        obj = cls.__new__(cls)
+        obj._init_handle(handle)
+        return obj
+
+    def _init_handle(self, handle: int) -> None:
+        lib = _lib.load_library()
+        self._h = handle
+        self._lib = lib
+        n = ctypes.c_int64()
+        nnz = ctypes.c_int64()
+        _lib.check(lib.gift_csr_shape(handle, ctypes.byref(n), ctypes.byref(nnz)))
+        self._n = int(n.value)
+        self._nnz = int(nnz.value)
+        self._host = None
+        self._degrees = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                self._lib.gift_csr_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def handle(self) -> int:
+        """Opaque gift_csr* for the C ABI."""
+        return self._h
+
+    @property
+    def n(self) -> int:
+        return self._n
+
+    @property
+    def nnz(self) -> int:
+        return self._nnz
+
+    def _mirror(self):
+        if self._host is None:
+            indptr = np.empty(self._n + 1, dtype=np.int64)
+            indices = np.empty(max(self._nnz, 1), dtype=np.int32)
+            values = np.empty(max(self._nnz, 1), dtype=np.float64)
+            ctx = _lib.context()
+            _lib.check(self._lib.gift_csr_download(
+                ctx, self._h, indptr.ctypes.data_as(ctypes.c_void_p),
+                indices.ctypes.data_as(ctypes.c_void_p), values.ctypes.data_as(ctypes.c_void_p)))
+            indices = indices[: self._nnz]
+            values = values[: self._nnz]
+            if max(self._nnz, self._n) < 2**31:
+                indptr = indptr.astype(np.int32)
+            else:
+                indices = indices.astype(np.int64)
+            self._host = (indptr, indices, values)
+        return self._host
+
+    @property
+    def indptr(self) -> np.ndarray:
+        return self._mirror()[0]
+
+    @property
+    def indices(self) -> np.ndarray:
+        return self._mirror()[1]
+
+    @property
+    def values(self) -> np.ndarray:
+        return self._mirror()[2]
+
+    def device_arrays(self) -> tuple[int, int, int]:
+        """Raw device pointers (indptr int64*, indices int32*, values double*)."""
+        a, b, c = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(self._lib.gift_csr_arrays(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value or 0, b.value or 0, c.value or 0
+
+    @property
+    def degrees(self) -> np.ndarray:
+        """Row sums d_i = sum_j w_ij (numpy reduceat order, computed on the GPU and cached)."""
+        if self._degrees is None:
+            ctx = _lib.context()
+            p = ctypes.c_void_p()
+            _lib.check(self._lib.gift_csr_degrees(ctx, self._h, ctypes.byref(p)))
+            out = np.empty(self._n, dtype=np.float64)
+            if self._n:
+                _memcpy_d2h(out, p.value)
+            self._degrees = out
+        return self._degrees
+
+    def matmul(self, g: np.ndarray) -> np.ndarray:
+        g = np.asarray(g, dtype=float)
+        if g.shape[0] != self.n:
+            raise DimensionMismatchError(f"signal has {g.shape[0]} rows, operator expects {self.n}")
+        return _matmul_power(self, g, 1)
+
+    def to_dense(self, limit: int = DENSE_LIMIT) -> np.ndarray:
+        if self.n > limit:
+            raise TooLargeForDenseError(self.n, limit)
+        return self.to_scipy().toarray()
+
+    def to_scipy(self):
+        import scipy.sparse as sp
+
+        indptr, indices, values = self._mirror()
+        return sp.csr_matrix((values, indices, indptr), shape=(self.n, self.n))
+
+    def __repr__(self) -> str:
+        return f"SparseSymMatrix(n={self.n}, nnz={self.nnz}, device=cuda)"
+
+
+class _DeviceView:
+    """__cuda_array_interface__ over library-owned device memory (no copy, no ownership)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {
+            "shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3, "strides": None,
+        }
+
+
+def _memcpy_d2h(dst: np.ndarray, src_ptr: int) -> None:
+    """Device -> host copy of dst.nbytes through torch (plumbing only)."""
+    torch = _lib.torch_cuda()
+    if dst.nbytes == 0:
+        return
+    src = torch.as_tensor(_DeviceView(src_ptr, dst.nbytes), device="cuda")
+    torch.from_numpy(dst.view(np.uint8).reshape(-1)).copy_(src)
+
+
+def _coo_handle(n: int, rows, cols, vals, check: bool) -> int:
+    torch = _lib.torch_cuda()
+    lib = _lib.load_library()
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    cols = np.ascontiguousarray(cols, dtype=np.int64)
+    vals = np.ascontiguousarray(vals, dtype=np.float64)
+    if not (len(rows) == len(cols) == len(vals)):
+        raise ValueError("row, column, and data array must all be the same length")
+    ctx = _lib.context()
+    dr = torch.from_numpy(rows).cuda()
+    dc = torch.from_numpy(cols).cuda()
+    dv = torch.from_numpy(vals).cuda()
+    h = ctypes.c_void_p()
+    _lib.check(lib.gift_csr_from_coo(ctx, int(n), len(rows), _lib.dptr(dr), _lib.dptr(dc), _lib.dptr(dv),
+                                     1 if check else 0, ctypes.byref(h)))
+    return h.value
+
+
+def from_coo(n: int, rows, cols, vals) -> SparseSymMatrix:
+    """Build a SparseSymMatrix from coordinate triplets (duplicates summed)."""
+    return SparseSymMatrix._from_handle(_coo_handle(n, rows, cols, vals, True))
+
+
+def build_clique_graph(design, max_clique_pins: int | None = None) -> SparseSymMatrix:
+    """Expand every net into a clique with edge weight 2/M (M = pin count), on the GPU.
+
+    Same contract as graph.py:120-158: weights of parallel nets accumulate,
+    pins of one net on the same cell produce no edge, nets with < 2 pins are
+    ignored, nets above `max_clique_pins` are skipped (and logged).
+    Accepts a `Design` (object model) or a `FlatDesign` (array native).
+    """
+    torch = _lib.torch_cuda()
+    lib = _lib.load_library()
+    net_start, pin_cell = pin_arrays(design)
+    n = int(design.num_cells)
+    ctx = _lib.context()
+    d_ns = torch.from_numpy(np.ascontiguousarray(net_start, dtype=np.int64)).cuda()
+    d_pc = torch.from_numpy(np.ascontiguousarray(pin_cell, dtype=np.int32)).cuda()
+    cap = int(max_clique_pins) if max_clique_pins is not None else -1
+    h = ctypes.c_void_p()
+    skipped = ctypes.c_int64(0)
+    _lib.check(lib.gift_build_clique_graph(ctx, n, len(net_start) - 1, _lib.dptr(d_ns), _lib.dptr(d_pc), cap,
+                                           ctypes.byref(h), ctypes.byref(skipped)))
+    if skipped.value:
+        log.info("clique expansion skipped %d nets with more than %d pins", skipped.value, max_clique_pins)
+    return SparseSymMatrix._from_handle(h.value)
+
+
+def normalized_augmented_adjacency(adj: SparseSymMatrix, sigma: float) -> SparseSymMatrix:
+    """(D+sigma*I)^(-1/2) (A+sigma*I) (D+sigma*I)^(-1/2), materialised on the GPU.
+
+    sigma < 0 raises ValueError; sigma == 0 with an isolated node raises
+    IsolatedNodeError(first such node) (graph.py:174-180)."""
+    if sigma < 0:
+        raise ValueError(f"sigma must be >= 0, got {sigma}")
+    adj = as_device_matrix(adj)
+    lib = _lib.load_library()
+    ctx = _lib.context()
+    h = ctypes.c_void_p()
+    _lib.check(lib.gift_normalized_augmented_adjacency(ctx, adj.handle, float(sigma), ctypes.byref(h)))
+    return SparseSymMatrix._from_handle(h.value)
+
+
+def _matmul_power(op: SparseSymMatrix, g: np.ndarray, k: int) -> np.ndarray:
+    """k exact fp64 products on the device; one upload, one download."""
+    torch = _lib.torch_cuda()
+    lib = _lib.load_library()
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    ncols = 1 if g.ndim == 1 else int(np.prod(g.shape[1:]))
+    ctx = _lib.context()
+    x = torch.from_numpy(g.reshape(op.n, ncols)).cuda()
+    y = torch.empty_like(x)
+    for _ in range(k):
+        _lib.check(lib.gift_csr_matmul(ctx, op.handle, ncols, _lib.dptr(x), _lib.dptr(y)))
+        x, y = y, x
+    return x.cpu().numpy().reshape(g.shape)
+
+
+def apply_operator_power(op: SparseSymMatrix, g: np.ndarray, k: int) -> np.ndarray:
+    """Apply op k times to each column of g (op^k never materialised); fp64, reference order."""
+    if k < 1:
+        raise ValueError(f"power k must be >= 1, got {k}")
+    op = as_device_matrix(op)
+    g = np.asarray(g, dtype=float)
+    if g.shape[0] != op.n:
+        raise DimensionMismatchError(f"signal has {g.shape[0]} rows, operator expects {op.n}")
+    return _matmul_power(op, g, int(k))
+
+
+def as_device_matrix(adj) -> SparseSymMatrix:
+    """Accept our SparseSymMatrix, or anything with to_scipy() (e.g. the reference's)."""
+    if isinstance(adj, SparseSymMatrix):
+        return adj
+    if hasattr(adj, "to_scipy"):
+        return SparseSymMatrix(adj.to_scipy(), check=False)
+    return SparseSymMatrix(adj)

@@ -1,0 +1,341 @@
+"""GPU parity: the CUDA path (through libgiftb200.so) against the reference's
+golden vectors and the CPU oracle on identical seeded inputs.
+
+Bars (north star): CSR structure, fp64 values and fp64 degrees bit-exact;
+fp32 filtered positions within 1e-5 relative L2 (checked both on absolute
+coordinates and centred on the die centre); the fp64 mode bit-exact.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import assert_bits_equal, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5  # north_star: positions within 1e-5 relative L2 in fp32
+DEFAULT = [(2.0, 2, 0.1), (4.0, 2, 0.7), (4.0, 4, 0.2)]
+
+NETLIST_CASES = ["kat_two_pin", "kat_three_pin", "kat_parallel", "kat_degenerate", "kat_self_pairs",
+                 "kat_cap", "kat_tri", "kat_brute", "dupnets"]
+COO_CASES = ["rand_graph0", "rand_graph1", "rand_graph2", "rand_coo0", "rand_coo1", "rand_coo2", "adversary"]
+
+
+@pytest.fixture(scope="module")
+def gb():
+    import paper_2502_17632_b200 as gb
+
+    return gb
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def flat(gb, ns, pc, n):
+    return gb.FlatDesign(ns, pc, np.zeros(n, bool), np.full((n, 2), np.nan), gb.Region(0.0, 0.0, 10.0, 10.0))
+
+
+def csr_equal(adj, indptr, indices, values, what):
+    assert adj.nnz == len(indices), f"{what}: nnz {adj.nnz} != {len(indices)}"
+    assert np.array_equal(np.asarray(adj.indptr, np.int64), indptr), f"{what}: indptr"
+    assert np.array_equal(np.asarray(adj.indices, np.int64), indices), f"{what}: indices"
+    assert_bits_equal(adj.values, values, f"{what}: values")
+
+
+# ---------------------------------------------------------------- golden --
+
+@pytest.mark.parametrize("case", NETLIST_CASES)
+def test_build_clique_graph_matches_reference(gb, golden, case):
+    n, cap = (int(x) for x in golden[f"{case}__n"])
+    adj = gb.build_clique_graph(flat(gb, golden[f"{case}__net_start"], golden[f"{case}__pin_cell"], n),
+                                max_clique_pins=None if cap < 0 else cap)
+    csr_equal(adj, golden[f"{case}__indptr"], golden[f"{case}__indices"], golden[f"{case}__values"], case)
+    assert_bits_equal(adj.degrees, golden[f"{case}__degrees"], f"{case}: degrees")
+
+
+@pytest.mark.parametrize("case", COO_CASES)
+def test_from_coo_matches_reference(gb, golden, case):
+    coo = golden[f"{case}__coo"]
+    n = int(golden[f"{case}__n"][0])
+    adj = gb.from_coo(n, coo[0].astype(np.int64), coo[1].astype(np.int64), coo[2])
+    csr_equal(adj, golden[f"{case}__indptr"], golden[f"{case}__indices"], golden[f"{case}__values"], case)
+    if f"{case}__degrees" in golden:
+        assert_bits_equal(adj.degrees, golden[f"{case}__degrees"], f"{case}: degrees")
+
+
+@pytest.mark.parametrize("case", NETLIST_CASES)
+@pytest.mark.parametrize("sigma", [0.0, 1.0, 2.0, 4.0])
+def test_normalized_augmented_adjacency_matches_reference(gb, golden, case, sigma):
+    n, cap = (int(x) for x in golden[f"{case}__n"])
+    adj = gb.build_clique_graph(flat(gb, golden[f"{case}__net_start"], golden[f"{case}__pin_cell"], n),
+                                max_clique_pins=None if cap < 0 else cap)
+    key = f"{case}__norm{sigma:g}"
+    if f"{key}__isolated" in golden:
+        with pytest.raises(gb.IsolatedNodeError) as exc:
+            gb.normalized_augmented_adjacency(adj, sigma)
+        assert exc.value.node == int(golden[f"{key}__isolated"][0])
+        assert str(exc.value.node) in str(exc.value)
+        return
+    op = gb.normalized_augmented_adjacency(adj, sigma)
+    csr_equal(op, golden[f"{key}__indptr"], golden[f"{key}__indices"], golden[f"{key}__values"], key)
+
+
+@pytest.mark.parametrize("case", NETLIST_CASES + ["rand_graph0", "rand_graph1", "rand_graph2"])
+def test_gift_filter_fp64_bit_exact_and_fp32_tolerance(gb, golden, case):
+    if f"{case}__filter" not in golden:
+        pytest.skip("reference raised (isolated node, sigma > 0 never does)")
+    if "__coo" in "".join(k for k in golden if k.startswith(case + "__")):
+        coo = golden[f"{case}__coo"]
+        adj = gb.from_coo(int(golden[f"{case}__n"][0]), coo[0].astype(np.int64), coo[1].astype(np.int64), coo[2])
+    else:
+        n, cap = (int(x) for x in golden[f"{case}__n"])
+        adj = gb.build_clique_graph(flat(gb, golden[f"{case}__net_start"], golden[f"{case}__pin_cell"], n),
+                                    max_clique_pins=None if cap < 0 else cap)
+    g = golden[f"{case}__g"]
+    ref = golden[f"{case}__filter"]
+    exact = gb.gift_filter(adj, g, gb.GiftConfig(precision="fp64"))
+    assert_bits_equal(exact, ref, f"{case}: fp64 filter")
+    fast = gb.gift_filter(adj, g)
+    assert fast.dtype == np.float64 and fast.shape == ref.shape
+    assert rel_l2(fast, ref) <= FP32_TOL
+
+
+@pytest.mark.parametrize("case", ["rand_graph0", "rand_graph1", "rand_graph2"])
+def test_custom_terms_and_operator_power(gb, golden, case):
+    coo = golden[f"{case}__coo"]
+    adj = gb.from_coo(int(golden[f"{case}__n"][0]), coo[0].astype(np.int64), coo[1].astype(np.int64), coo[2])
+    g = golden[f"{case}__g"]
+    terms = (gb.FilterTerm(sigma=1.0, k=1, alpha=0.5), gb.FilterTerm(sigma=1.0, k=3, alpha=0.5))
+    assert_bits_equal(gb.gift_filter(adj, g, gb.GiftConfig(terms=terms, precision="fp64")),
+                      golden[f"{case}__filter_custom"], "custom terms fp64")
+    assert rel_l2(gb.gift_filter(adj, g, gb.GiftConfig(terms=terms)), golden[f"{case}__filter_custom"]) <= FP32_TOL
+    op = gb.normalized_augmented_adjacency(adj, 4.0)
+    assert_bits_equal(gb.apply_operator_power(op, g, 3), golden[f"{case}__pow3"], "A_4^3 g")
+
+
+def test_c0_matches_reference_hashes(gb, golden, golden_meta):
+    from paper_2502_17632_b200 import synth
+
+    meta = golden_meta["cases"]["c0"]
+    fd = synth.generate("c0", seed=1)
+    adj = gb.build_clique_graph(fd, max_clique_pins=fd.meta["max_clique_pins"])
+    assert adj.nnz == meta["nnz"]
+    assert sha(np.asarray(adj.indptr, np.int64)) == meta["indptr_sha"]
+    assert sha(np.asarray(adj.indices, np.int64)) == meta["indices_sha"]
+    assert sha(np.asarray(adj.values, np.float64)) == meta["values_sha"]
+    assert sha(np.asarray(adj.degrees, np.float64)) == meta["degrees_sha"]
+    cfg = gb.GiftConfig(seed=0, jitter_scale=10.0)
+    g0 = gb.initial_signal(fd, cfg)
+    assert sha(g0) == meta["g0_sha"]
+    g32 = g0.astype(np.float32)
+    # fp64 mode on the fp32-rounded seed == reference gift_filter on the same values
+    exact = gb.gift_filter(adj, g32.astype(np.float64), gb.GiftConfig(precision="fp64"))
+    assert sha(exact) == meta["filter_g32_sha"]
+    placed_exact, timings = gb.gift_place(fd, adj, gb.GiftConfig(seed=0, jitter_scale=10.0, precision="fp64"))
+    assert sha(placed_exact) == meta["place_sha"]
+    assert timings["filter"] >= 0.0
+    rows = golden["c0__sample_rows"]
+    fast = gb.gift_filter(adj, g32)
+    ref_rows = golden["c0__filter_g32_sample"]
+    assert rel_l2(fast[rows], ref_rows) <= FP32_TOL
+    placed, _ = gb.gift_place(fd, adj, cfg)
+    assert rel_l2(placed[rows], golden["c0__place_sample"]) <= FP32_TOL
+
+
+# ---------------------------------------------------------------- oracle --
+
+def _oracle_parity(gb, orc, fd, cap, seed=0, check_place=True):
+    adj = gb.build_clique_graph(fd, max_clique_pins=cap)
+    ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, cap)
+    csr_equal(adj, ref.indptr, ref.indices, ref.data, fd.meta.get("config", "design"))
+    deg = orc.degrees(ref)
+    assert_bits_equal(adj.degrees, deg, "degrees")
+    g32 = gb.initial_signal(fd, gb.GiftConfig(seed=seed, jitter_scale=10.0)).astype(np.float32)
+    g = g32.astype(np.float64)
+    want = orc.gift_filter(ref, g, DEFAULT, deg)
+    got = gb.gift_filter(adj, g32)
+    centre = np.array(fd.region.center)
+    assert rel_l2(got, want) <= FP32_TOL
+    assert rel_l2(got - centre, want - centre) <= FP32_TOL
+    if check_place:
+        r = fd.region
+        want_p = orc.place_epilogue(want, fd.fixed_mask(), fd.fixed_positions(), [r.xmin, r.ymin, r.xmax, r.ymax])
+        got_p, _ = gb.gift_place(fd, adj, gb.GiftConfig(seed=seed, jitter_scale=10.0))
+        assert rel_l2(got_p, want_p) <= FP32_TOL
+        mask = fd.fixed_mask()
+        assert np.array_equal(got_p[mask], fd.fixed_positions()[mask])
+        assert got_p[~mask, 0].min() >= r.xmin and got_p[~mask, 0].max() <= r.xmax
+        exact_p, _ = gb.gift_place(fd, adj, gb.GiftConfig(seed=seed, jitter_scale=10.0, precision="fp64"))
+        g0 = gb.initial_signal(fd, gb.GiftConfig(seed=seed, jitter_scale=10.0))
+        want_exact = orc.place_epilogue(orc.gift_filter(ref, g0, DEFAULT, deg), mask, fd.fixed_positions(),
+                                        [r.xmin, r.ymin, r.xmax, r.ymax])
+        assert_bits_equal(exact_p, want_exact, "fp64 gift_place")
+    return adj, ref
+
+
+def test_c1_full_size_matches_oracle(gb, orc):
+    from paper_2502_17632_b200 import synth
+
+    fd = synth.generate("c1", seed=1)
+    _oracle_parity(gb, orc, fd, None)
+
+
+@pytest.mark.parametrize("config,scale,cap", [("c2", 0.05, 200), ("c3", 0.03, 200), ("c4", 0.004, 100),
+                                              ("c2", 0.01, None)])
+def test_heavy_tail_configs_scaled_match_oracle(gb, orc, config, scale, cap):
+    from paper_2502_17632_b200 import synth
+
+    fd = synth.generate(config, seed=2, scale=scale, window=600)
+    _oracle_parity(gb, orc, fd, cap, check_place=(config != "c4"))
+
+
+def test_place_host_abi_end_to_end(gb, orc):
+    """gift_place_host: host netlist + host fp32 seed in, host positions out."""
+    from paper_2502_17632_b200 import synth
+
+    fd = synth.generate("c0", seed=3)
+    g32 = synth.signal_fp32(fd, seed=5)
+    r = fd.region
+    out, nnz = gb.gift_place_arrays(fd.net_start, fd.pin_cell, g32, fd.fixed_mask(), fd.fixed_positions(),
+                                    r.bounds(), precision="fp64")
+    ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, None)
+    assert nnz == ref.nnz
+    want = orc.place_epilogue(orc.gift_filter(ref, g32.astype(np.float64), DEFAULT), fd.fixed_mask(),
+                              fd.fixed_positions(), r.bounds())
+    assert_bits_equal(out, want, "gift_place_host fp64")
+    out32, _ = gb.gift_place_arrays(fd.net_start, fd.pin_cell, g32, fd.fixed_mask(), fd.fixed_positions(),
+                                    r.bounds())
+    assert rel_l2(out32, want) <= FP32_TOL
+
+
+@pytest.mark.parametrize("ncols", [1, 3, 5])
+def test_signal_widths(gb, orc, ncols):
+    from paper_2502_17632_b200 import synth
+
+    fd = synth.generate("c0", seed=4, scale=0.2)
+    adj = gb.build_clique_graph(fd)
+    ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, None)
+    g = np.random.default_rng(ncols).standard_normal((fd.num_cells, ncols)) * 10 + 3
+    if ncols == 1:
+        g = g[:, 0]
+    want = orc.gift_filter(ref, g, DEFAULT)
+    assert_bits_equal(gb.gift_filter(adj, g, gb.GiftConfig(precision="fp64")), want, "fp64")
+    got = gb.gift_filter(adj, g)
+    assert got.shape == want.shape
+    assert rel_l2(got, want) <= FP32_TOL
+
+
+def test_many_sigma_groups_pack_split(gb, orc):
+    """5 terms over 3 sigmas: chains packed 2 + 1, terms sharing k, k order shuffled."""
+    from paper_2502_17632_b200 import synth
+
+    fd = synth.generate("c0", seed=5, scale=0.3)
+    adj = gb.build_clique_graph(fd)
+    ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, None)
+    terms = [(1.0, 3, 0.25), (3.0, 1, 0.2), (1.0, 1, 0.15), (0.5, 2, 0.3), (3.0, 1, 0.1)]
+    g = synth.signal_fp32(fd, seed=1).astype(np.float64)
+    want = orc.gift_filter(ref, g, terms)
+    cfg_terms = tuple(gb.FilterTerm(*t) for t in terms)
+    assert_bits_equal(gb.gift_filter(adj, g, gb.GiftConfig(terms=cfg_terms, precision="fp64")), want, "fp64")
+    assert rel_l2(gb.gift_filter(adj, g, gb.GiftConfig(terms=cfg_terms)), want) <= FP32_TOL
+
+
+def test_fp32_path_is_deterministic(gb):
+    from paper_2502_17632_b200 import synth
+
+    fd = synth.generate("c1", seed=1, scale=0.2)
+    adj = gb.build_clique_graph(fd)
+    g = synth.signal_fp32(fd, seed=2)
+    a = gb.gift_filter(adj, g)
+    b = gb.gift_filter(adj, g)
+    assert np.array_equal(a.view(np.int64), b.view(np.int64))
+    adj2 = gb.build_clique_graph(fd)
+    assert np.array_equal(adj.values.view(np.int64), adj2.values.view(np.int64))
+
+
+# ------------------------------------------------- reference KAT behaviour --
+
+def test_reference_kats(gb):
+    d = lambda n, nets: flat(gb, *_flat(nets), n)  # noqa: E731
+    assert gb.build_clique_graph(d(2, [[0, 1]])).to_dense().tolist() == [[0.0, 1.0], [1.0, 0.0]]
+    dense = gb.build_clique_graph(d(3, [[0, 1, 2]])).to_dense()
+    assert np.abs(dense - (2.0 / 3.0) * (np.ones((3, 3)) - np.eye(3))).max() < 1e-15
+    assert gb.build_clique_graph(d(2, [[0, 1], [0, 1]])).to_dense()[0, 1] == 2.0
+    dense = gb.build_clique_graph(d(3, [[0], [], [1, 2]])).to_dense()
+    assert dense[0].tolist() == [0.0, 0.0, 0.0] and dense[1, 2] == 1.0
+    dense = gb.build_clique_graph(d(2, [[0, 0, 1]])).to_dense()
+    assert dense[0, 0] == 0.0 and dense[0, 1] == pytest.approx(4.0 / 3.0)
+    assert gb.build_clique_graph(d(5, [[0, 1, 2, 3, 4], [0, 1]]), max_clique_pins=3).nnz == 2
+    adj = gb.from_coo(2, [0, 1, 0, 1], [1, 0, 1, 0], [1.0, 1.0, 2.0, 2.0])
+    assert adj.nnz == 2 and adj.to_dense()[0, 1] == 3.0
+    assert gb.from_coo(3, [0, 1, 1, 2], [1, 0, 2, 1], [2.0, 2.0, 0.5, 0.5]).degrees.tolist() == [2.0, 2.5, 0.5]
+    two = gb.from_coo(2, [0, 1], [1, 0], [1.0, 1.0])
+    out = gb.normalized_augmented_adjacency(two, 2.0).to_dense()
+    assert np.abs(out - np.array([[2.0, 1.0], [1.0, 2.0]]) / 3.0).max() < 1e-12
+    iso = gb.from_coo(3, [0, 1], [1, 0], [1.0, 1.0])
+    assert gb.normalized_augmented_adjacency(iso, 1.0).to_dense()[2, 2] == 1.0
+    op = gb.normalized_augmented_adjacency(two, 2.0)
+    assert np.abs(gb.apply_operator_power(op, np.array([0.0, 3.0]), 2) - [4 / 3, 5 / 3]).max() < 1e-12
+    one = gb.GiftConfig(terms=(gb.FilterTerm(sigma=2.0, k=2, alpha=1.0),))
+    assert np.abs(gb.gift_filter(two, np.array([0.0, 3.0]), one) - [4 / 3, 5 / 3]).max() < 1e-6
+    ring = gb.from_coo(4, [0, 1, 1, 2, 2, 3, 3, 0], [1, 0, 2, 1, 3, 2, 0, 3], np.ones(8))
+    g = np.full((4, 2), 7.5)
+    assert np.abs(gb.gift_filter(ring, g, gb.GiftConfig(precision="fp64")) - g).max() < 1e-12
+    assert np.abs(gb.gift_filter(ring, g) - g).max() < 1e-5
+    assert np.all(gb.gift_filter(ring, np.zeros((4, 2))) == 0.0)
+
+
+def test_errors_match_reference_classes(gb):
+    two = gb.from_coo(2, [0, 1], [1, 0], [1.0, 1.0])
+    with pytest.raises(gb.DimensionMismatchError):
+        two.matmul(np.zeros((3, 2)))
+    with pytest.raises(gb.DimensionMismatchError):
+        gb.gift_filter(two, np.zeros((3, 2)))
+    with pytest.raises(gb.TooLargeForDenseError):
+        gb.from_coo(5, [0, 1], [1, 0], [1.0, 1.0]).to_dense(limit=4)
+    with pytest.raises(ValueError):
+        gb.normalized_augmented_adjacency(two, -0.5)
+    with pytest.raises(ValueError):
+        gb.apply_operator_power(two, np.zeros(2), 0)
+    with pytest.raises(ValueError):
+        gb.GiftConfig(terms=())
+    with pytest.raises(gb.NonSymmetricError):
+        gb.from_coo(2, [0], [1], [1.0])
+    import scipy.sparse as sp
+
+    with pytest.raises(gb.NonSymmetricError):
+        gb.SparseSymMatrix(sp.csr_matrix(np.array([[0.0, 1.0], [0.5, 0.0]])))
+    with pytest.raises(gb.NonSymmetricError):
+        gb.SparseSymMatrix(sp.csr_matrix(np.ones((2, 3))))
+    iso = gb.from_coo(3, [0, 1], [1, 0], [1.0, 1.0])
+    with pytest.raises(gb.IsolatedNodeError) as exc:
+        gb.normalized_augmented_adjacency(iso, 0.0)
+    assert "2" in str(exc.value)
+    with pytest.raises(gb.IsolatedNodeError):
+        gb.gift_filter(iso, np.zeros((3, 2)), gb.GiftConfig(terms=(gb.FilterTerm(0.0, 1, 1.0),)))
+    with pytest.raises(ValueError):
+        gb.from_coo(2, [0, 5], [1, 0], [1.0, 1.0])
+
+
+def test_empty_and_isolated_graphs(gb):
+    empty = gb.build_clique_graph(flat(gb, np.zeros(1, np.int64), np.zeros(0, np.int64), 4))
+    assert empty.nnz == 0 and empty.degrees.tolist() == [0.0] * 4
+    g = np.arange(8, dtype=float).reshape(4, 2)
+    out = gb.gift_filter(empty, g, gb.GiftConfig(precision="fp64"))
+    # isolated rows: A_sigma = [1] exactly for sigma in {4}, 0.9999999999999998 for sigma 2
+    ref_factor = 0.1 * (0.9999999999999998 ** 2) + 0.7 + 0.2
+    assert np.abs(out - g * ref_factor).max() < 1e-12
+    assert np.abs(gb.gift_filter(empty, g) - out).max() < 1e-5
+
+
+def _flat(nets):
+    counts = np.array([len(p) for p in nets], dtype=np.int64)
+    ns = np.zeros(len(nets) + 1, dtype=np.int64)
+    np.cumsum(counts, out=ns[1:])
+    pc = np.array([c for p in nets for c in p], dtype=np.int64)
+    return ns, pc
