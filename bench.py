@@ -24,8 +24,11 @@ seeded synthetic (the paper's ISPD2014 designs are not available).  The CSR
            operation order, OpenMP over rows) on a scaled sample, rank 0, N=1.
 --impl reference: the same oracle as the reference arm (the reference is
            pure Python/scipy and cannot be installed as a GPU-box package).
-Multi-GPU (torchrun): ranks run independent replicas of the workload
-(weak scaling); the row-sharded halo-exchange path is tested on CPU (gloo).
+Multi-GPU (torchrun, N > 1): the SAME graph is row-sharded over the N ranks
+(strong scaling, paper_2502_17632_b200/shard.py): nnz-balanced row blocks,
+per-hop ghost exchange by NCCL all_to_all overlapped with the local part of
+the hop; `value` counts the one graph's nnz_op * 6 per step over the max-rank
+time.
 """
 
 from __future__ import annotations
@@ -218,18 +221,29 @@ def main() -> None:
     sig = np.array([t.sigma for t in gb.DEFAULT_TERMS], dtype=np.float64)
     kk = np.array([t.k for t in gb.DEFAULT_TERMS], dtype=np.int64)
     al = np.array([t.alpha for t in gb.DEFAULT_TERMS], dtype=np.float64)
-    dg = torch.from_numpy(g32).to(dev)
-    dmask = torch.from_numpy(mask).to(dev)
-    dpos = torch.from_numpy(fpos).to(dev)
-    dout = torch.empty((n, 2), dtype=torch.float64, device=dev)
     ctx = _lib.context(local)
     sp_, kp_, ap_, rp_ = (sig.ctypes.data_as(_lib.c_dp), kk.ctypes.data_as(_lib.c_i64p),
                           al.ctypes.data_as(_lib.c_dp), region.ctypes.data_as(_lib.c_dp))
+    if world == 1:
+        r0, r1 = 0, n
+    else:
+        from paper_2502_17632_b200 import shard
 
-    def step():
-        _lib.check(lib.gift_filter(ctx, adj.handle, 3, sp_, kp_, ap_, 2, _lib.GIFT_DTYPE_F32, _lib.dptr(dg),
-                                   _lib.GIFT_DTYPE_F64, _lib.dptr(dout), _lib.dptr(dmask), _lib.dptr(dpos), rp_,
-                                   _lib.GIFT_PREC_FP32))
+        sf = shard.cuda_sharded_filter(adj, world, rank, local)
+        r0, r1 = sf.plan.r0, sf.plan.r1
+    dg = torch.from_numpy(np.ascontiguousarray(g32[r0:r1])).to(dev)
+    dmask = torch.from_numpy(np.ascontiguousarray(mask[r0:r1])).to(dev)
+    dpos = torch.from_numpy(np.ascontiguousarray(fpos[r0:r1])).to(dev)
+    dout = torch.empty((r1 - r0, 2), dtype=torch.float64, device=dev)
+
+    if world == 1:
+        def step():
+            _lib.check(lib.gift_filter(ctx, adj.handle, 3, sp_, kp_, ap_, 2, _lib.GIFT_DTYPE_F32, _lib.dptr(dg),
+                                       _lib.GIFT_DTYPE_F64, _lib.dptr(dout), _lib.dptr(dmask), _lib.dptr(dpos),
+                                       rp_, _lib.GIFT_PREC_FP32))
+    else:
+        def step():
+            sf.run(dg, gb.DEFAULT_TERMS, dout, fixed_mask=dmask, fixed_pos=dpos, region=region)
 
     for _ in range(args.warmup):
         step()
@@ -264,21 +278,22 @@ def main() -> None:
         dist.all_reduce(t_rank, op=dist.ReduceOp.MAX)
     ms_max = float(t_rank.item())
     per_step_ms = ms_max / args.steps
-    value = nnz_op * HOPS * args.steps * world / (ms_max / 1e3)
+    # one graph per step whatever N is (row-sharded): strong scaling
+    value = nnz_op * HOPS * args.steps / (ms_max / 1e3)
 
-    # ---- roofline of the dominant kernel ----
+    # ---- roofline of the dominant kernel (rank-local bytes when sharded) ----
     pk = peaks()
+    local_nnz_op = int(np.asarray(adj.indptr[r1], dtype=np.int64) - np.asarray(adj.indptr[r0], dtype=np.int64)) \
+        + (r1 - r0)
+    local_unit_bytes = bytes_per_hop(local_nnz_op, r1 - r0)
     by_kind: dict[int, list] = {}
     for kind, units, t in recs:
         by_kind.setdefault(kind, []).append((units, t))
     kernels = {}
     for kind, lst in by_kind.items():
         tot = sum(t for _, t in lst)
-        mean_ms = tot / len(lst)
-        units = lst[0][0]
-        alg = (units * unit_bytes) if kind > 0 else (n * (8 + 4 * units) + n * 4 * kind)
-        kernels[kind] = {"launches": len(lst), "mean_ms": mean_ms, "share": tot, "units": units,
-                         "bytes": alg}
+        kernels[kind] = {"launches": len(lst), "mean_ms": tot / len(lst), "share": tot, "units": lst[0][0],
+                         "bytes": lst[0][0] * local_unit_bytes}
     total_prof = sum(k["share"] for k in kernels.values()) or 1.0
     hop_kinds = [k for k in kernels if k > 0]
     dom = max(hop_kinds, key=lambda k: kernels[k]["share"]) if hop_kinds else None
@@ -292,22 +307,36 @@ def main() -> None:
                 "bytes_per_launch": k["bytes"], "mean_launch_ms": round(k["mean_ms"], 5),
                 "share_of_step": round(k["share"] / total_prof, 4), "peak_source": pk["source"]}
 
-    roofline = roof(dom) if dom is not None else None
-    kernels_report = {f"k_hop_F{k}" if k else "k_prep": roof(k) if k else
-                      {"mean_launch_ms": round(v["mean_ms"], 5), "share_of_step": round(v["share"] / total_prof, 4)}
+    roofline = roof(dom) if (dom is not None and world == 1) else None
+    kernels_report = {f"k_hop_F{k}" if k else "k_prep": roof(k) if (k and world == 1) else
+                      {"mean_launch_ms": round(v["mean_ms"], 5), "launches": v["launches"],
+                       "share_of_step": round(v["share"] / total_prof, 4)}
                       for k, v in kernels.items()}
 
-    # ---- e2e through the C ABI with pinned host buffers ----
-    h_g = torch.from_numpy(g32).pin_memory()
-    h_mask = torch.from_numpy(mask).pin_memory()
-    h_pos = torch.from_numpy(fpos).pin_memory()
-    h_out = torch.empty((n, 2), dtype=torch.float64).pin_memory()
+    # ---- e2e: host buffers in, host placement out, every step ----
+    h_g = torch.from_numpy(np.ascontiguousarray(g32[r0:r1])).pin_memory()
+    h_mask = torch.from_numpy(np.ascontiguousarray(mask[r0:r1])).pin_memory()
+    h_pos = torch.from_numpy(np.ascontiguousarray(fpos[r0:r1])).pin_memory()
+    h_out = torch.empty((r1 - r0, 2), dtype=torch.float64).pin_memory()
 
-    def step_e2e():
-        _lib.check(lib.gift_filter_host(ctx, adj.handle, 3, sp_, kp_, ap_, 2, _lib.GIFT_DTYPE_F32,
-                                        _lib.c_vp(h_g.data_ptr()), _lib.GIFT_DTYPE_F64, _lib.c_vp(h_out.data_ptr()),
-                                        _lib.c_vp(h_mask.data_ptr()), _lib.c_vp(h_pos.data_ptr()), rp_,
-                                        _lib.GIFT_PREC_FP32))
+    if world == 1:
+        e2e_api = "gift_filter_host (C ABI, pinned host buffers)"
+
+        def step_e2e():
+            _lib.check(lib.gift_filter_host(ctx, adj.handle, 3, sp_, kp_, ap_, 2, _lib.GIFT_DTYPE_F32,
+                                            _lib.c_vp(h_g.data_ptr()), _lib.GIFT_DTYPE_F64,
+                                            _lib.c_vp(h_out.data_ptr()), _lib.c_vp(h_mask.data_ptr()),
+                                            _lib.c_vp(h_pos.data_ptr()), rp_, _lib.GIFT_PREC_FP32))
+    else:
+        e2e_api = "ShardedFilter.run with per-rank pinned H2D/D2H"
+
+        def step_e2e():
+            dg.copy_(h_g, non_blocking=True)
+            dmask.copy_(h_mask, non_blocking=True)
+            dpos.copy_(h_pos, non_blocking=True)
+            step()
+            h_out.copy_(dout, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
 
     for _ in range(2):
         step_e2e()
@@ -323,9 +352,10 @@ def main() -> None:
     t_e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
-    e2e_value = nnz_op * HOPS * k_e2e * world / float(t_e.item())
-    h2d = g32.nbytes + mask.nbytes + fpos.nbytes
-    d2h = n * 2 * 8
+    e2e_value = nnz_op * HOPS * k_e2e / float(t_e.item())
+    h2d = (g32.nbytes + mask.nbytes + fpos.nbytes) // 1 if world == 1 else \
+        int(h_g.numel() * 4 + h_mask.numel() + h_pos.numel() * 8)
+    d2h = (r1 - r0) * 2 * 8
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
@@ -339,8 +369,9 @@ def main() -> None:
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong" if world > 1 else "weak",
             "config": {
                 "workload": f"{args.config}: {fd.meta['n_mov']} movable + {fd.meta['n_macros']} macros + "
                             f"{fd.meta['n_pads']} pads, {fd.meta['n_nets']} nets, max_clique_pins={cap}, "
@@ -348,7 +379,8 @@ def main() -> None:
                 "n": n, "nnz": adj.nnz, "nnz_op": nnz_op, "hops": HOPS, "seed": args.seed,
                 "bytes_per_hop_unit": unit_bytes,
                 "l2": "inputs larger than L2 (CSR col+w32 = %.2f GB per pass)" % (8 * adj.nnz / 1e9),
-                "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                "parallelism": f"row-sharded x{world} (NCCL ghost all_to_all per hop)" if world > 1
+                else "single GPU",
                 "graph_build_s": round(build_s, 3), "generate_s": round(gen_s, 3),
             },
             "roofline": roofline,
@@ -356,7 +388,7 @@ def main() -> None:
             "effective_bank_gbs": round(HOPS * unit_bytes / (per_step_ms / 1e3) / 1e9, 1),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "api": "gift_filter_host (C ABI, pinned host buffers)",
+                    "api": e2e_api,
                     "ms_per_step": 1e3 * float(t_e.item()) / k_e2e},
             "gpu_launches": int(launches),
             "clocks": clk,

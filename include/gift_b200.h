@@ -146,6 +146,52 @@ int gift_place_host(gift_ctx* ctx, int64_t n_cells, int64_t n_nets, const int64_
                     const double* h_region, int out_dtype, void* h_out, int precision,
                     int64_t* nnz_out);
 
+/* ---- stepped bank (host-driven, e.g. row-sharded over ranks) ---------- */
+/* The fused fp32 bank of gift_filter, exposed one kernel at a time so a host
+ * driver can interleave a halo exchange between hops (paper_2502_17632_b200/
+ * shard.py).  Rows of the CSR are the rows a rank owns; column ids index a
+ * signal buffer that holds the owned rows first and then the ghost rows the
+ * exchange writes. */
+typedef struct gift_chain_desc {
+  const float* s;  /* fp32 s_sigma = 1/sqrt(d + sigma) of the rows processed (indexed by row) */
+  double sigma;
+  int cont;        /* slot of this chain in zout, -1 when the chain ends at this hop */
+  int has_term;    /* a FilterTerm of this chain completes at this hop */
+  double alpha;    /* its weight */
+} gift_chain_desc;
+
+typedef struct gift_hop_desc {
+  int64_t row_begin, row_end; /* rows processed */
+  int fin, fout;              /* floats per signal row in / out (1, 2, 4; fout 0 = none) */
+  int wcols, nch;             /* signal columns per chain, chains packed in zin */
+  const float* zin;           /* [*, fin], indexed by column id */
+  float* zout;                /* [*, fout], indexed by row */
+  const float* part_in;       /* split hop: partial row sums [*, fin] added first, or NULL */
+  float* part_out;            /* split hop: write raw row sums here, no epilogue, or NULL */
+  gift_chain_desc chain[4];
+  float* acc;                 /* [*, wcols] fp32 bank accumulator */
+  int acc_read, is_final;
+  int out_dtype;
+  void* out;
+  int64_t out_ld, out_c0;
+  const uint8_t* fixed_mask;
+  const double* fixed_pos;
+  double region[4];
+} gift_hop_desc;
+
+int gift_csr_scale(gift_ctx* ctx, gift_csr* csr, double sigma, const double** d_s64, const float** d_s32);
+int gift_csr_weights32(gift_ctx* ctx, gift_csr* csr, const float** d_w32);
+/* A (possibly rectangular) row block: copies caller arrays, no canonicalisation. */
+int gift_csr_from_arrays(gift_ctx* ctx, int64_t n_rows, int64_t nnz, const int64_t* d_indptr,
+                         const int32_t* d_indices, const double* d_values, gift_csr** out);
+int gift_hop_fp32(gift_ctx* ctx, gift_csr* csr, const gift_hop_desc* desc);
+/* z[i, j*wcols + c] = s_j[i] * g[i*ld + c0 + c] for j < nch, c < wcols; F floats per row. */
+int gift_pack_fp32(gift_ctx* ctx, int64_t n, int wcols, int nch, const float* const* h_s, int in_dtype,
+                   const void* d_g, int64_t ld, int64_t c0, int F, float* d_z);
+/* dst[r, :] = src[idx[r], :] for F floats per row (halo send buffers). */
+int gift_gather_rows_f32(gift_ctx* ctx, int64_t n_idx, int F, const int64_t* d_idx, const float* d_src,
+                         float* d_dst);
+
 #ifdef __cplusplus
 }
 #endif

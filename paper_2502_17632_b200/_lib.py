@@ -70,6 +70,13 @@ SIGNATURES = [
                                  c_vp, c_dp, c_int]),
     ("gift_place_host", c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_int, c_dp, c_i64p, c_dp, c_vp, c_vp, c_vp,
                                 c_dp, c_int, c_vp, c_int, c_i64p]),
+    # stepped bank (shard.py)
+    ("gift_csr_scale", c_int, [c_vp, c_vp, ctypes.c_double, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
+    ("gift_csr_weights32", c_int, [c_vp, c_vp, ctypes.POINTER(c_vp)]),
+    ("gift_csr_from_arrays", c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, ctypes.POINTER(c_vp)]),
+    ("gift_hop_fp32", c_int, [c_vp, c_vp, c_vp]),
+    ("gift_pack_fp32", c_int, [c_vp, c_i64, c_int, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_int, c_vp]),
+    ("gift_gather_rows_f32", c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp]),
 ]
 
 _lib = None

@@ -2,6 +2,7 @@
 // plus the context / memory / error plumbing declared in common.cuh.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -20,6 +21,15 @@ void csr_matmul(Ctx* ctx, const Csr* c, int64_t ncols, const double* x, double* 
 void filter(Ctx* ctx, Csr* c, int n_terms, const double* sigma, const int64_t* k, const double* alpha, int64_t ncols,
             int in_dtype, const void* g, int out_dtype, void* out, const uint8_t* fixed_mask, const double* fixed_pos,
             const double* region, int precision);
+
+void scale_vectors(Ctx* ctx, Csr* c, double sigma, const double** s64, const float** s32);
+const float* weights32(Ctx* ctx, Csr* c);
+void hop_fp32(Ctx* ctx, Csr* c, const gift_hop_desc* d);
+void pack_fp32(Ctx* ctx, int64_t n, int wcols, int nch, const float* const* s, int in_dtype, const void* g,
+               int64_t ld, int64_t c0, int F, float* z);
+void gather_rows_f32(Ctx* ctx, int64_t n_idx, int F, const int64_t* idx, const float* src, float* dst);
+Csr* csr_from_arrays(Ctx* ctx, int64_t n_rows, int64_t nnz, const int64_t* d_indptr, const int32_t* d_indices,
+                     const double* d_values);
 
 static thread_local Error t_err{GIFT_OK, "", -1};
 
@@ -70,7 +80,7 @@ void* pinned(Ctx* ctx, size_t bytes) {
 }
 
 void* csr_alloc(Ctx* ctx, Csr* c, size_t bytes) {
-  void* p = dev_alloc(ctx, bytes);
+  void* p = dev_alloc(ctx, bytes + 64);  // vector loads may read up to 3 elements past the end
   c->owned.push_back(p);
   return p;
 }
@@ -357,6 +367,59 @@ int gift_place_host(gift_ctx* ctx, int64_t n_cells, int64_t n_nets, const int64_
     throw;
   }
   gift::csr_destroy(c);
+  GIFT_API_END
+}
+
+int gift_csr_scale(gift_ctx* ctx, gift_csr* csr, double sigma, const double** d_s64, const float** d_s32) {
+  GIFT_API_BEGIN
+  require(ctx && csr, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  gift::scale_vectors(ctx, csr, sigma, d_s64, d_s32);
+  GIFT_API_END
+}
+
+int gift_csr_weights32(gift_ctx* ctx, gift_csr* csr, const float** d_w32) {
+  GIFT_API_BEGIN
+  require(ctx && csr && d_w32, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  *d_w32 = gift::weights32(ctx, csr);
+  GIFT_API_END
+}
+
+int gift_csr_from_arrays(gift_ctx* ctx, int64_t n_rows, int64_t nnz, const int64_t* d_indptr,
+                         const int32_t* d_indices, const double* d_values, gift_csr** out) {
+  GIFT_API_BEGIN
+  require(ctx && out && d_indptr, GIFT_ERR_VALUE, "null argument");
+  require(n_rows >= 0 && nnz >= 0, GIFT_ERR_VALUE, "negative size");
+  DeviceGuard g(ctx->device);
+  *out = static_cast<gift_csr*>(gift::csr_from_arrays(ctx, n_rows, nnz, d_indptr, d_indices, d_values));
+  GIFT_API_END
+}
+
+int gift_hop_fp32(gift_ctx* ctx, gift_csr* csr, const gift_hop_desc* desc) {
+  GIFT_API_BEGIN
+  require(ctx && csr && desc, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  gift::hop_fp32(ctx, csr, desc);
+  GIFT_API_END
+}
+
+int gift_pack_fp32(gift_ctx* ctx, int64_t n, int wcols, int nch, const float* const* h_s, int in_dtype,
+                   const void* d_g, int64_t ld, int64_t c0, int F, float* d_z) {
+  GIFT_API_BEGIN
+  require(ctx && h_s, GIFT_ERR_VALUE, "null argument");
+  require(nch >= 1 && nch <= 4 && wcols * nch <= F, GIFT_ERR_VALUE, "bad packing");
+  DeviceGuard g(ctx->device);
+  gift::pack_fp32(ctx, n, wcols, nch, h_s, in_dtype, d_g, ld, c0, F, d_z);
+  GIFT_API_END
+}
+
+int gift_gather_rows_f32(gift_ctx* ctx, int64_t n_idx, int F, const int64_t* d_idx, const float* d_src,
+                         float* d_dst) {
+  GIFT_API_BEGIN
+  require(ctx, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  gift::gather_rows_f32(ctx, n_idx, F, d_idx, d_src, d_dst);
   GIFT_API_END
 }
 

@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -272,7 +273,10 @@ struct HopArgs {
   const int64_t* rowptr;
   const int32_t* col;
   const float* w;
-  int64_t n;
+  int64_t n;          // one past the last row processed
+  int64_t row_begin;  // first row processed
+  const float* part_in;  // [rows, FIN] partial sums added before the epilogue (split hop), or null
+  float* part_out;       // write the raw row sums here and skip the epilogue (split hop), or null
   const float* zin;  // [n, FIN]
   float* zout;       // [n, FOUT]
   int wcols;         // signal columns per chain
@@ -317,18 +321,6 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
-// streamed once per hop: skip L1, evict first from L2
-__device__ __forceinline__ int32_t ld_stream_s32(const int32_t* p, uint64_t pol) {
-  int32_t r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ float ld_stream_f32(const float* p, uint64_t pol) {
-  float r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
-  return r;
-}
-
 // gathered signal rows: L1-allocating, keep in L2
 template <int F>
 __device__ __forceinline__ VecF<F> ld_z(const float* p, uint64_t pol);
@@ -355,12 +347,30 @@ __device__ __forceinline__ VecF<4> ld_z<4>(const float* p, uint64_t pol) {
   return r;
 }
 
-// One hop for every chain packed in zin. G lanes per row reduce with a fixed
-// xor-butterfly (deterministic order); lane 0 runs the row epilogue.
-template <int FIN, int FOUT, int G>
+__device__ __forceinline__ int4 ld_stream_v4s32(const int32_t* p, uint64_t pol) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float4 ld_stream_v4f32(const float* p, uint64_t pol) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+// One hop for every chain packed in zin.  G lanes own a row; each lane
+// streams 4 consecutive (col, w) per 16-byte vector load (aligned down to a
+// multiple of 4, out-of-row slots masked), U such chunks in flight, so a lane
+// has 2U streaming loads then 4U gathers outstanding.  Lane partials reduce
+// with a fixed xor-butterfly (deterministic order); lane 0 runs the epilogue.
+template <int FIN, int FOUT, int G, int U>
 __global__ void __launch_bounds__(kBlock) k_hop(HopArgs a) {
   const int lane = threadIdx.x & (G - 1);
-  const int64_t row = (blockIdx.x * (int64_t)kBlock + threadIdx.x) / G;
+  const int64_t row = a.row_begin + (blockIdx.x * (int64_t)kBlock + threadIdx.x) / G;
   if (row >= a.n) return;  // uniform within a row group
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
   const uint64_t pol_s = policy_evict_first();
@@ -369,12 +379,45 @@ __global__ void __launch_bounds__(kBlock) k_hop(HopArgs a) {
   float acc[FIN];
 #pragma unroll
   for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
-  for (int64_t k = beg + lane; k < end; k += G) {
-    const int32_t c = ld_stream_s32(a.col + k, pol_s);
-    const float wk = ld_stream_f32(a.w + k, pol_s);
-    const VecF<FIN> z = ld_z<FIN>(a.zin + (int64_t)c * FIN, pol_z);
+  const int64_t base = beg & ~(int64_t)3;
+  for (int64_t k0 = base + 4 * lane; k0 < end; k0 += 4 * G * U) {
+    int4 cv[U];
+    float4 wv[U];
 #pragma unroll
-    for (int f = 0; f < FIN; ++f) acc[f] = fmaf(wk, z.v[f], acc[f]);
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = k0 + (int64_t)(4 * G) * u;
+      if (k < end) {
+        cv[u] = ld_stream_v4s32(a.col + k, pol_s);
+        wv[u] = ld_stream_v4f32(a.w + k, pol_s);
+      } else {
+        cv[u] = make_int4(0, 0, 0, 0);
+        wv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    VecF<FIN> zv[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = k0 + (int64_t)(4 * G) * u;
+      const int cc[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (k + j >= beg && k + j < end) {
+          zv[u][j] = ld_z<FIN>(a.zin + (int64_t)cc[j] * FIN, pol_z);
+        } else {
+#pragma unroll
+          for (int f = 0; f < FIN; ++f) zv[u][j].v[f] = 0.f;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float ww[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int f = 0; f < FIN; ++f) acc[f] = fmaf(ww[j], zv[u][j].v[f], acc[f]);
+      }
+    }
   }
 #pragma unroll
   for (int off = G / 2; off > 0; off >>= 1) {
@@ -382,6 +425,15 @@ __global__ void __launch_bounds__(kBlock) k_hop(HopArgs a) {
     for (int f = 0; f < FIN; ++f) acc[f] += __shfl_xor_sync(gmask, acc[f], off, G);
   }
   if (lane != 0) return;
+  if (a.part_out) {
+#pragma unroll
+    for (int f = 0; f < FIN; ++f) a.part_out[row * FIN + f] = acc[f];
+    return;
+  }
+  if (a.part_in) {
+#pragma unroll
+    for (int f = 0; f < FIN; ++f) acc[f] = a.part_in[row * FIN + f] + acc[f];
+  }
   const VecF<FIN> zi = ld_z<FIN>(a.zin + row * FIN, pol_z);
   float o[4] = {0.f, 0.f, 0.f, 0.f};
   if (a.any_term && a.acc_read)
@@ -441,22 +493,46 @@ __global__ void k_prep(int64_t n, int wcols, int nch, const float* s0, const flo
   }
 }
 
+__global__ void k_gather_rows(int64_t n_idx, int F, const int64_t* __restrict__ idx, const float* __restrict__ src,
+                              float* __restrict__ dst) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_idx * F; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / F;
+    dst[t] = src[idx[r] * F + (t - r * F)];
+  }
+}
+
 int pow2_ceil(int v) {
   int p = 1;
   while (p < v) p <<= 1;
   return p;
 }
 
+// lanes per row and chunks in flight; GIFT_HOP_G / GIFT_HOP_U override (tuning sweeps)
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 template <int FIN, int FOUT>
 void launch_hop_g(Ctx* ctx, const HopArgs& a, int G) {
-  const int64_t threads = a.n * (int64_t)G;
+  if (a.n <= a.row_begin) return;
+  G = env_int("GIFT_HOP_G", G);
+  const int U = env_int("GIFT_HOP_U", 1);
+  const int64_t threads = (a.n - a.row_begin) * (int64_t)G;
   const unsigned grid = (unsigned)((threads + kBlock - 1) / kBlock);
   cudaStream_t st = ctx->stream;
-  switch (G) {
-    case 4: k_hop<FIN, FOUT, 4><<<grid, kBlock, 0, st>>>(a); break;
-    case 8: k_hop<FIN, FOUT, 8><<<grid, kBlock, 0, st>>>(a); break;
-    case 16: k_hop<FIN, FOUT, 16><<<grid, kBlock, 0, st>>>(a); break;
-    default: k_hop<FIN, FOUT, 32><<<grid, kBlock, 0, st>>>(a); break;
+  if (U >= 2) {
+    switch (G) {
+      case 8: k_hop<FIN, FOUT, 8, 2><<<grid, kBlock, 0, st>>>(a); break;
+      case 16: k_hop<FIN, FOUT, 16, 2><<<grid, kBlock, 0, st>>>(a); break;
+      default: k_hop<FIN, FOUT, 32, 2><<<grid, kBlock, 0, st>>>(a); break;
+    }
+  } else {
+    switch (G) {
+      case 8: k_hop<FIN, FOUT, 8, 1><<<grid, kBlock, 0, st>>>(a); break;
+      case 16: k_hop<FIN, FOUT, 16, 1><<<grid, kBlock, 0, st>>>(a); break;
+      default: k_hop<FIN, FOUT, 32, 1><<<grid, kBlock, 0, st>>>(a); break;
+    }
   }
   GIFT_LAUNCH_CHECK(ctx);
 }
@@ -657,11 +733,11 @@ static void bank_fp64_exact(Ctx* ctx, Csr* c, const std::vector<TermGroup>& grou
   GIFT_LAUNCH_CHECK(ctx);
 }
 
+// measured on B200 (profiles/r01_sweep_hop.txt): 8 lanes per row at mean
+// row length ~64 (c1), 16 at ~400 (c2/c3); one 4-nnz chunk in flight per lane
 static int pick_group_lanes(double mean_row) {
-  if (mean_row < 12) return 4;
-  if (mean_row < 40) return 8;
-  if (mean_row < 100) return 16;
-  return 32;
+  if (mean_row < 160) return 8;
+  return 16;
 }
 
 // GIFT_PREC_FP32: fused pre-scaled bank.
@@ -760,6 +836,97 @@ static void bank_fp32(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, in
       }
     }
   }
+}
+
+static int pick_group_lanes(double mean_row);
+
+// ---- stepped building blocks for host-driven (sharded) banks ----------------
+void scale_vectors(Ctx* ctx, Csr* c, double sigma, const double** s64, const float** s32) {
+  const double* s = csr_scale(ctx, c, sigma);
+  if (s64) *s64 = s;
+  if (s32) *s32 = c->s32[sigma];
+}
+
+const float* weights32(Ctx* ctx, Csr* c) { return csr_w32(ctx, c); }
+
+void hop_fp32(Ctx* ctx, Csr* c, const gift_hop_desc* d) {
+  if (d->fin != 1 && d->fin != 2 && d->fin != 4) throw_error(GIFT_ERR_VALUE, "fin must be 1, 2 or 4");
+  if (d->fout != 0 && d->fout != 1 && d->fout != 2 && d->fout != 4) throw_error(GIFT_ERR_VALUE, "bad fout");
+  if (d->nch < 1 || d->nch > 4 || d->wcols < 1 || d->wcols * d->nch > d->fin)
+    throw_error(GIFT_ERR_VALUE, "bad chain packing");
+  if (d->row_begin < 0 || d->row_end > c->n || d->row_begin > d->row_end) throw_error(GIFT_ERR_VALUE, "bad row range");
+  HopArgs a{};
+  a.rowptr = c->indptr;
+  a.col = c->indices;
+  a.w = csr_w32(ctx, c);
+  a.n = d->row_end;
+  a.row_begin = d->row_begin;
+  a.part_in = d->part_in;
+  a.part_out = d->part_out;
+  a.zin = d->zin;
+  a.zout = d->zout;
+  a.wcols = d->wcols;
+  a.nch = d->nch;
+  for (int j = 0; j < d->nch; ++j) {
+    a.ch[j].s = d->chain[j].s;
+    a.ch[j].sigma = (float)d->chain[j].sigma;
+    a.ch[j].cont = d->chain[j].cont;
+    a.ch[j].has_term = d->chain[j].has_term;
+    a.ch[j].alpha = (float)d->chain[j].alpha;
+    a.any_term |= d->chain[j].has_term;
+  }
+  a.acc = d->acc;
+  a.acc_read = d->acc_read;
+  a.is_final = d->is_final;
+  a.out_dtype = d->out_dtype;
+  a.out = d->out;
+  a.out_ld = d->out_ld;
+  a.out_c0 = d->out_c0;
+  a.fixed_mask = d->fixed_mask;
+  a.fixed_pos = d->fixed_pos;
+  memcpy(a.reg.v, d->region, sizeof(a.reg.v));
+  launch_hop(ctx, a, d->fin, d->fout, pick_group_lanes(c->mean_row));
+}
+
+void pack_fp32(Ctx* ctx, int64_t n, int wcols, int nch, const float* const* s, int in_dtype, const void* g,
+               int64_t ld, int64_t c0, int F, float* z) {
+  if (n <= 0) return;
+  ProfScope prof(ctx, 0, nch);
+  const float* sp[4] = {nullptr, nullptr, nullptr, nullptr};
+  for (int j = 0; j < nch && j < 4; ++j) sp[j] = s[j];
+  const unsigned grid = grid_for(n, kBlock, 1LL << 30);
+  switch (F) {
+    case 1: k_prep<1><<<grid, kBlock, 0, ctx->stream>>>(n, wcols, nch, sp[0], sp[1], sp[2], sp[3], in_dtype, g, ld, c0, z); break;
+    case 2: k_prep<2><<<grid, kBlock, 0, ctx->stream>>>(n, wcols, nch, sp[0], sp[1], sp[2], sp[3], in_dtype, g, ld, c0, z); break;
+    case 4: k_prep<4><<<grid, kBlock, 0, ctx->stream>>>(n, wcols, nch, sp[0], sp[1], sp[2], sp[3], in_dtype, g, ld, c0, z); break;
+    default: throw_error(GIFT_ERR_VALUE, "F must be 1, 2 or 4");
+  }
+  GIFT_LAUNCH_CHECK(ctx);
+}
+
+void gather_rows_f32(Ctx* ctx, int64_t n_idx, int F, const int64_t* idx, const float* src, float* dst) {
+  if (n_idx <= 0) return;
+  k_gather_rows<<<grid_for(n_idx * F, kBlock), kBlock, 0, ctx->stream>>>(n_idx, F, idx, src, dst);
+  GIFT_LAUNCH_CHECK(ctx);
+}
+
+Csr* csr_from_arrays(Ctx* ctx, int64_t n_rows, int64_t nnz, const int64_t* d_indptr, const int32_t* d_indices,
+                     const double* d_values) {
+  Csr* c = new gift_csr();
+  c->device = ctx->device;
+  c->n = n_rows;
+  c->nnz = nnz;
+  c->indptr = static_cast<int64_t*>(csr_alloc(ctx, c, (n_rows + 1) * sizeof(int64_t)));
+  c->indices = static_cast<int32_t*>(csr_alloc(ctx, c, (nnz > 0 ? nnz : 1) * sizeof(int32_t)));
+  c->values = static_cast<double*>(csr_alloc(ctx, c, (nnz > 0 ? nnz : 1) * sizeof(double)));
+  c->mean_row = n_rows > 0 ? (double)nnz / n_rows : 0.0;
+  c->has_diagonal = true;
+  GIFT_CUDA(cudaMemcpyAsync(c->indptr, d_indptr, (n_rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (nnz > 0) {
+    GIFT_CUDA(cudaMemcpyAsync(c->indices, d_indices, nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    GIFT_CUDA(cudaMemcpyAsync(c->values, d_values, nnz * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  return c;
 }
 
 void filter(Ctx* ctx, Csr* c, int n_terms, const double* sigma, const int64_t* k, const double* alpha, int64_t ncols,

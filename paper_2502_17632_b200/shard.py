@@ -1,0 +1,500 @@
+"""Row-sharded GiFt filter bank over several GPUs (one process per GPU).
+
+SURVEY.md §8(e): rows are independent given the signal, so the CSR is cut
+into contiguous, nnz-balanced row blocks; the only exchange is, per hop, the
+signal rows a block's columns reference outside the block ("ghosts").  For
+netlists with index locality (every net inside a +-W window) the ghosts are a
+2W-row halo on each side plus the fixed objects (pads/macros) referenced from
+everywhere.
+
+Per hop, each rank
+  1. packs the rows other ranks asked for (gift_gather_rows_f32),
+  2. starts an all-to-all of those rows (NCCL over NVLink; async),
+  3. runs the LOCAL part of the hop (columns it owns) -> partial row sums,
+  4. waits for the exchange (stream-ordered; the host never blocks),
+  5. runs the GHOST part (columns owned elsewhere) plus the epilogue.
+Steps 2 and 3 overlap.  The bank schedule (chain packing, term accumulation,
+fused re-pin/clamp) is `plan_bank`, the host mirror of bank_fp32 in
+csrc/filter.cu; the numeric kernels are the same k_hop instances.
+
+Degrees and s_sigma come from the FULL rows each rank owns, so they are the
+single-GPU values bit for bit; only fp32 summation order differs (split
+local/ghost partial sums), well inside the 1e-5 tolerance.
+
+Everything except the kernel calls is backend-neutral: `CudaBackend` calls the
+C ABI; tests drive the same schedule and exchange over gloo with a numpy
+backend (tests/test_shard.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# ------------------------------------------------------------------ bank plan
+
+
+@dataclass
+class ChainStep:
+    group: int        # index into the sigma groups
+    cont: int         # slot in zout, -1 if the chain ends here
+    has_term: int
+    alpha: float
+
+
+@dataclass
+class PackStep:
+    c0: int
+    wcols: int
+    groups: list[int]
+    F: int
+
+
+@dataclass
+class HopStep:
+    c0: int
+    wcols: int
+    chains: list[ChainStep]
+    fin: int
+    fout: int
+    acc_read: int
+    is_final: int
+    any_term: int
+
+
+@dataclass
+class BankPlan:
+    sigmas: list[float]
+    steps: list = field(default_factory=list)
+
+    @property
+    def hops(self) -> int:
+        return sum(len(s.chains) for s in self.steps if isinstance(s, HopStep))
+
+
+def _pow2(v: int) -> int:
+    p = 1
+    while p < v:
+        p <<= 1
+    return p
+
+
+def plan_bank(terms, ncols: int) -> BankPlan:
+    """Chain packing of gift.py:83-94: sigma groups in first-appearance order,
+    each group's terms stable-sorted by k; groups packed 4 // wcols per pass."""
+    groups: list[list] = []
+    sigmas: list[float] = []
+    for t in terms:
+        sigma, k, alpha = (t.sigma, t.k, t.alpha) if hasattr(t, "sigma") else t
+        if sigma < 0:
+            raise ValueError(f"sigma must be >= 0, got {sigma}")
+        if k < 1:
+            raise ValueError(f"power k must be >= 1, got {k}")
+        if sigma not in sigmas:
+            sigmas.append(sigma)
+            groups.append([])
+        groups[sigmas.index(sigma)].append((int(k), float(alpha)))
+    if not groups:
+        raise ValueError("filter needs at least one term")
+    for g in groups:
+        g.sort(key=lambda x: x[0])  # list.sort is stable
+    plan = BankPlan(sigmas=sigmas)
+    for c0 in range(0, ncols, 4):
+        wcols = min(4, ncols - c0)
+        per = max(1, 4 // wcols)
+        acc_written = False
+        for g0 in range(0, len(groups), per):
+            pack = list(range(g0, min(g0 + per, len(groups))))
+            last_pack = pack[-1] == len(groups) - 1
+            maxk = max(groups[j][-1][0] for j in pack)
+            plan.steps.append(PackStep(c0, wcols, pack, _pow2(wcols * len(pack))))
+            active = list(pack)
+            for h in range(1, maxk + 1):
+                nxt, chains, any_term = [], [], 0
+                for j in active:
+                    al = sum(a for k, a in groups[j] if k == h)
+                    has = int(any(k == h for k, _ in groups[j]))
+                    any_term |= has
+                    if groups[j][-1][0] > h:
+                        cont = len(nxt)
+                        nxt.append(j)
+                    else:
+                        cont = -1
+                    chains.append(ChainStep(j, cont, has, al))
+                plan.steps.append(HopStep(
+                    c0, wcols, chains, _pow2(wcols * len(active)), _pow2(wcols * len(nxt)) if nxt else 0,
+                    int(acc_written), int(last_pack and h == maxk), any_term))
+                if any_term:
+                    acc_written = True
+                active = nxt
+    return plan
+
+
+# ------------------------------------------------------------------ partition
+
+
+def nnz_balanced_bounds(indptr: np.ndarray, world: int) -> np.ndarray:
+    """Row boundaries r_0 = 0 < ... < r_P = n splitting nnz (+1 per row) evenly."""
+    indptr = np.asarray(indptr, dtype=np.int64)
+    n = len(indptr) - 1
+    work = indptr + np.arange(n + 1)  # count each row once so empty rows still spread
+    targets = (np.arange(1, world) * work[-1]) // world
+    cuts = np.searchsorted(work, targets, side="left")
+    b = np.concatenate([[0], np.clip(cuts, 0, n), [n]]).astype(np.int64)
+    return np.maximum.accumulate(b)
+
+
+@dataclass
+class ShardPlan:
+    """Rank-local view: local/ghost CSR blocks (remapped columns) and the
+    exchange lists.  Column ids index z_ext = [owned rows | ghost rows]."""
+
+    world: int
+    rank: int
+    bounds: np.ndarray          # [world+1]
+    r0: int
+    r1: int
+    ghosts: np.ndarray          # sorted global ids this rank reads but does not own
+    recv_counts: list[int]      # ghosts owned by each rank (grouped, ascending)
+    send_counts: list[int]      # rows each rank asked this rank for
+    send_rows: np.ndarray       # local row ids to pack, grouped by destination rank
+    local_indptr: np.ndarray    # entries with owned columns
+    local_indices: np.ndarray
+    local_pos: np.ndarray       # positions of those entries in the global value array
+    ghost_indptr: np.ndarray    # entries with ghost columns
+    ghost_indices: np.ndarray
+    ghost_pos: np.ndarray
+
+    @property
+    def n_local(self) -> int:
+        return self.r1 - self.r0
+
+    @property
+    def n_ghost(self) -> int:
+        return len(self.ghosts)
+
+
+def _split_block(indptr, indices, r0, r1):
+    lo, hi = int(indptr[r0]), int(indptr[r1])
+    cols = np.asarray(indices[lo:hi], dtype=np.int64)
+    rowlen = np.diff(np.asarray(indptr[r0:r1 + 1], dtype=np.int64))
+    row_of = np.repeat(np.arange(r1 - r0), rowlen)
+    owned = (cols >= r0) & (cols < r1)
+    pos = np.arange(lo, hi, dtype=np.int64)
+    ghosts = np.unique(cols[~owned])
+
+    def block(mask, remap):
+        cnt = np.bincount(row_of[mask], minlength=r1 - r0)
+        ptr = np.zeros(r1 - r0 + 1, dtype=np.int64)
+        np.cumsum(cnt, out=ptr[1:])
+        return ptr, remap.astype(np.int32), pos[mask]
+
+    l_ptr, l_idx, l_pos = block(owned, cols[owned] - r0)
+    g_ptr, g_idx, g_pos = block(~owned, (r1 - r0) + np.searchsorted(ghosts, cols[~owned]))
+    return ghosts, (l_ptr, l_idx, l_pos), (g_ptr, g_idx, g_pos)
+
+
+def make_shard_plan(indptr, indices, world: int, rank: int, exchange_ids) -> ShardPlan:
+    """Build this rank's plan.  `exchange_ids(send_lists) -> recv_lists` is an
+    all-to-all of int64 id lists (setup only): rank p tells each owner which
+    of its rows it needs."""
+    bounds = nnz_balanced_bounds(indptr, world)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    ghosts, loc, gh = _split_block(indptr, indices, r0, r1)
+    owner = np.searchsorted(bounds, ghosts, side="right") - 1
+    requests = [ghosts[owner == q] for q in range(world)]
+    recv_counts = [len(x) for x in requests]
+    asked = exchange_ids(requests)  # asked[q] = my rows rank q needs (global ids)
+    send_counts = [len(x) for x in asked]
+    send_rows = (np.concatenate(asked) - r0).astype(np.int64) if asked else np.zeros(0, np.int64)
+    return ShardPlan(world, rank, bounds, r0, r1, ghosts, recv_counts, send_counts, send_rows,
+                     loc[0], loc[1], loc[2], gh[0], gh[1], gh[2])
+
+
+# ------------------------------------------------------------------ exchange
+
+
+class TorchExchange:
+    """Per-hop ghost exchange with torch.distributed all_to_all_single
+    (NCCL over NVLink for CUDA tensors; gloo for CPU tensors in tests)."""
+
+    def __init__(self, plan: ShardPlan | None = None, group=None, device="cpu"):
+        self.plan = plan
+        self.group = group
+        self.device = device
+
+    def ids(self, requests):
+        import torch
+        import torch.distributed as dist
+
+        counts = torch.tensor([len(r) for r in requests], dtype=torch.int64, device=self.device)
+        recv = torch.empty_like(counts)
+        dist.all_to_all_single(recv, counts, group=self.group)
+        flat = np.concatenate(requests).astype(np.int64) if requests else np.zeros(0, np.int64)
+        send = torch.from_numpy(flat).to(self.device)
+        rc = recv.cpu().numpy()
+        out = torch.empty(int(rc.sum()), dtype=torch.int64, device=self.device)
+        dist.all_to_all_single(out, send, output_split_sizes=rc.tolist(), input_split_sizes=counts.cpu().tolist(),
+                               group=self.group)
+        parts = np.split(out.cpu().numpy(), np.cumsum(rc)[:-1])
+        return [np.asarray(p, dtype=np.int64) for p in parts]
+
+    def start(self, sendbuf, recvbuf, F: int):
+        """Async all-to-all of packed rows (F floats each) into the ghost rows."""
+        import torch.distributed as dist
+
+        p = self.plan
+        if p.world == 1:
+            return None
+        return dist.all_to_all_single(recvbuf, sendbuf, output_split_sizes=[c * F for c in p.recv_counts],
+                                      input_split_sizes=[c * F for c in p.send_counts], group=self.group,
+                                      async_op=True)
+
+
+class ThreadExchange:
+    """In-process stand-in for the collective: P virtual ranks as Python
+    threads sharing one device and one stream.  Each hop, every rank deposits
+    its packed rows, a host barrier orders them, and receivers copy their
+    ghost rows out -- stream-ordered device copies, no kernel ever waits on
+    another.  Used to run the exact sharded code path on a single GPU."""
+
+    def __init__(self, world: int):
+        import threading
+
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.box: dict = {}
+        self.plans: dict = {}
+
+    def for_rank(self, rank: int):
+        return _ThreadRankExchange(self, rank)
+
+
+class _ThreadRankExchange:
+    def __init__(self, hub: ThreadExchange, rank: int):
+        self.hub, self.rank, self.plan = hub, rank, None
+
+    def ids(self, requests):
+        self.hub.box[("ids", self.rank)] = requests
+        self.hub.barrier.wait()
+        got = [self.hub.box[("ids", q)][self.rank] for q in range(self.hub.world)]
+        self.hub.barrier.wait()
+        return got
+
+    def start(self, sendbuf, recvbuf, F: int):
+        p = self.plan
+        offs = np.concatenate([[0], np.cumsum(p.send_counts)]) * F
+        self.hub.box[("rows", self.rank)] = [sendbuf[offs[q]:offs[q + 1]] for q in range(p.world)]
+        self.hub.barrier.wait()
+        roff = np.concatenate([[0], np.cumsum(p.recv_counts)]) * F
+        for q in range(p.world):
+            src = self.hub.box[("rows", q)][self.rank]
+            if src.numel():
+                recvbuf[roff[q]:roff[q + 1]].copy_(src)
+        self.hub.barrier.wait()
+        return None
+
+
+# ------------------------------------------------------------------ backends
+
+
+class CudaBackend:
+    """Kernel calls through libgiftb200.so on this rank's GPU."""
+
+    def __init__(self, device: int):
+        from . import _lib
+
+        self._lib = _lib
+        self.lib = _lib.load_library()
+        self.device = device
+        self.torch = _lib.torch_cuda()
+
+    def ctx(self):
+        return self._lib.context(self.device)
+
+    def empty(self, rows: int, cols: int, dtype="f32"):
+        t = self.torch
+        return t.zeros((max(rows, 1), cols), dtype=t.float32 if dtype == "f32" else t.float64,
+                       device=f"cuda:{self.device}")
+
+    def upload(self, arr):
+        return self.torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{self.device}")
+
+    def block(self, indptr, indices, values):
+        """Local row block -> gift_csr handle (values fp64; fp32 copy made lazily)."""
+        d_ptr = self.upload(np.asarray(indptr, np.int64))
+        d_idx = self.upload(np.asarray(indices, np.int32))
+        d_val = self.upload(np.asarray(values, np.float64))
+        h = ctypes.c_void_p()
+        self._lib.check(self.lib.gift_csr_from_arrays(self.ctx(), len(indptr) - 1, len(indices),
+                                                      self._lib.dptr(d_ptr), self._lib.dptr(d_idx),
+                                                      self._lib.dptr(d_val), ctypes.byref(h)))
+        return _Handle(self.lib, h.value)
+
+    def pack(self, n, wcols, groups_s, g, ld, c0, F, z):
+        arr = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(p) for p in groups_s] + [None] * (4 - len(groups_s)))
+        in_dtype = self._lib.GIFT_DTYPE_F32 if g.dtype == self.torch.float32 else self._lib.GIFT_DTYPE_F64
+        self._lib.check(self.lib.gift_pack_fp32(self.ctx(), n, wcols, len(groups_s),
+                                                ctypes.cast(arr, ctypes.c_void_p), in_dtype, self._lib.dptr(g),
+                                                ld, c0, F, self._lib.dptr(z)))
+
+    def gather(self, idx, F, src, dst):
+        self._lib.check(self.lib.gift_gather_rows_f32(self.ctx(), idx.numel(), F, self._lib.dptr(idx),
+                                                      self._lib.dptr(src), self._lib.dptr(dst)))
+
+    def hop(self, block, desc: dict):
+        d = _hop_desc(desc)
+        self._lib.check(self.lib.gift_hop_fp32(self.ctx(), block.h, ctypes.byref(d)))
+
+
+class _Handle:
+    def __init__(self, lib, h):
+        self.lib, self.h = lib, h
+
+    def __del__(self):
+        if self.h:
+            self.lib.gift_csr_destroy(self.h)
+            self.h = None
+
+
+class _Chain(ctypes.Structure):
+    _fields_ = [("s", ctypes.c_void_p), ("sigma", ctypes.c_double), ("cont", ctypes.c_int),
+                ("has_term", ctypes.c_int), ("alpha", ctypes.c_double)]
+
+
+class _HopDesc(ctypes.Structure):
+    _fields_ = [("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64), ("fin", ctypes.c_int),
+                ("fout", ctypes.c_int), ("wcols", ctypes.c_int), ("nch", ctypes.c_int),
+                ("zin", ctypes.c_void_p), ("zout", ctypes.c_void_p), ("part_in", ctypes.c_void_p),
+                ("part_out", ctypes.c_void_p), ("chain", _Chain * 4), ("acc", ctypes.c_void_p),
+                ("acc_read", ctypes.c_int), ("is_final", ctypes.c_int), ("out_dtype", ctypes.c_int),
+                ("out", ctypes.c_void_p), ("out_ld", ctypes.c_int64), ("out_c0", ctypes.c_int64),
+                ("fixed_mask", ctypes.c_void_p), ("fixed_pos", ctypes.c_void_p),
+                ("region", ctypes.c_double * 4)]
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _hop_desc(d: dict) -> _HopDesc:
+    h = _HopDesc()
+    h.row_begin, h.row_end = d["row_begin"], d["row_end"]
+    h.fin, h.fout, h.wcols, h.nch = d["fin"], d["fout"], d["wcols"], len(d["chains"])
+    h.zin, h.zout = _ptr(d["zin"]), _ptr(d.get("zout"))
+    h.part_in, h.part_out = _ptr(d.get("part_in")), _ptr(d.get("part_out"))
+    for j, ch in enumerate(d["chains"]):
+        h.chain[j] = _Chain(ch["s"], ch["sigma"], ch["cont"], ch["has_term"], ch["alpha"])
+    h.acc = _ptr(d["acc"])
+    h.acc_read, h.is_final = d["acc_read"], d["is_final"]
+    h.out_dtype, h.out = d.get("out_dtype", 1), _ptr(d.get("out"))
+    h.out_ld, h.out_c0 = d.get("out_ld", 0), d.get("out_c0", 0)
+    h.fixed_mask, h.fixed_pos = _ptr(d.get("fixed_mask")), _ptr(d.get("fixed_pos"))
+    reg = d.get("region")
+    if reg is not None:
+        for i in range(4):
+            h.region[i] = float(reg[i])
+    return h
+
+
+# ------------------------------------------------------------------ driver
+
+
+class ShardedFilter:
+    """Runs the bank on this rank's row block with per-hop ghost exchange.
+
+    plan      : ShardPlan
+    values    : global fp64 CSR values (host) -- only this block's are used
+    s_by_sigma: {sigma: handle-to-local s32} backend-specific (device pointers
+                for CudaBackend, numpy arrays for tests)
+    """
+
+    def __init__(self, plan: ShardPlan, values: np.ndarray, backend, exchange, s_of):
+        self.plan = plan
+        self.be = backend
+        self.ex = exchange
+        self.ex.plan = plan
+        self.s_of = s_of  # sigma -> this block's s32 (backend handle)
+        self.local = backend.block(plan.local_indptr, plan.local_indices, values[plan.local_pos])
+        self.ghost = backend.block(plan.ghost_indptr, plan.ghost_indices, values[plan.ghost_pos])
+        n, ng = plan.n_local, plan.n_ghost
+        self.zA = backend.empty(n + ng, 4)
+        self.zB = backend.empty(n + ng, 4)
+        self.acc = backend.empty(n, 4)
+        self.part = backend.empty(n, 4)
+        self.sendbuf = backend.empty(len(plan.send_rows), 4)
+        self.send_idx = backend.upload(plan.send_rows)
+
+    def _exchange(self, z, F):
+        p = self.plan
+        n, ng = p.n_local, p.n_ghost
+        flat = z.view(-1)
+        send = self.sendbuf.view(-1)[: len(p.send_rows) * F]
+        if len(p.send_rows):
+            self.be.gather(self.send_idx, F, flat, send)
+        recv = flat[n * F: (n + ng) * F]
+        if p.world == 1:
+            return None
+        return self.ex.start(send, recv, F)
+
+    def run(self, g, terms, out, fixed_mask=None, fixed_pos=None, region=None):
+        """g: [n_local, ncols] (f32/f64) on the backend; out: [n_local, ncols] f64."""
+        p = self.plan
+        n = p.n_local
+        ncols = g.shape[1]
+        bank = plan_bank(terms, ncols)
+        zin, zout = self.zA, self.zB
+        for st in bank.steps:
+            if isinstance(st, PackStep):
+                F = st.F
+                self.be.pack(n, st.wcols, [self.s_of(bank.sigmas[j]) for j in st.groups], g, ncols, st.c0, F,
+                             self.zA.view(-1))
+                zin, zout = self.zA, self.zB
+                continue
+            F = st.fin
+            zin_f = zin.view(-1)
+            zout_f = zout.view(-1)
+            work = self._exchange(zin, F)
+            chains = [dict(s=self.s_of(bank.sigmas[c.group]), sigma=bank.sigmas[c.group], cont=c.cont,
+                           has_term=c.has_term, alpha=c.alpha) for c in st.chains]
+            common = dict(row_begin=0, row_end=n, fin=F, fout=st.fout, wcols=st.wcols, chains=chains,
+                          zin=zin_f, acc=self.acc, acc_read=st.acc_read, is_final=st.is_final)
+            # local columns overlap the exchange
+            self.be.hop(self.local, dict(common, part_out=self.part.view(-1), zout=None))
+            if work is not None:
+                work.wait()
+            self.be.hop(self.ghost, dict(common, part_in=self.part.view(-1), zout=zout_f if st.fout else None,
+                                         out=out, out_ld=ncols, out_c0=st.c0, out_dtype=1,
+                                         fixed_mask=fixed_mask, fixed_pos=fixed_pos, region=region))
+            zin, zout = zout, zin
+        return out
+
+
+# ------------------------------------------------------------------ CUDA entry
+
+
+def cuda_sharded_filter(adj, world: int, rank: int, device: int, exchange=None, group=None) -> ShardedFilter:
+    """Set up this rank's share of `adj` (a full SparseSymMatrix resident on
+    `device`, built replicated on every rank).  s_sigma comes from the full
+    graph's degrees, sliced to the block, so it is the single-GPU vector."""
+    from . import _lib
+
+    be = CudaBackend(device)
+    ex = exchange or TorchExchange(group=group, device=f"cuda:{device}")
+    indptr = np.asarray(adj.indptr, dtype=np.int64)
+    plan = make_shard_plan(indptr, adj.indices, world, rank, ex.ids)
+    lib = _lib.load_library()
+    cache: dict = {}
+
+    def s_of(sigma):
+        if sigma not in cache:
+            s64 = ctypes.c_void_p()
+            s32 = ctypes.c_void_p()
+            _lib.check(lib.gift_csr_scale(_lib.context(device), adj.handle, float(sigma), ctypes.byref(s64),
+                                          ctypes.byref(s32)))
+            cache[sigma] = (s32.value or 0) + 4 * plan.r0
+        return cache[sigma]
+
+    return ShardedFilter(plan, np.asarray(adj.values), be, ex, s_of)

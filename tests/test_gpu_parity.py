@@ -339,3 +339,60 @@ def _flat(nets):
     np.cumsum(counts, out=ns[1:])
     pc = np.array([c for p in nets for c in p], dtype=np.int64)
     return ns, pc
+
+
+# ---------------------------------------------------------- sharded path --
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, world):
+    """The multi-GPU code path (partition, ghost pack, split local/ghost hops,
+    fused epilogue) with `world` virtual ranks as threads on one device; the
+    all-to-all is replaced by stream-ordered device copies (ThreadExchange),
+    so no kernel ever waits on another."""
+    import threading
+
+    import torch
+
+    from paper_2502_17632_b200 import shard, synth
+
+    fd = synth.generate("c2", seed=4, scale=0.02, window=600)
+    adj = gb.build_clique_graph(fd, max_clique_pins=200)
+    g32 = synth.signal_fp32(fd, seed=2)
+    hub = shard.ThreadExchange(world)
+    blocks = [None] * world
+    errors = []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            sf = shard.cuda_sharded_filter(adj, world, rank, 0, exchange=hub.for_rank(rank))
+            r0, r1 = sf.plan.r0, sf.plan.r1
+            g = torch.from_numpy(np.ascontiguousarray(g32[r0:r1])).cuda()
+            out = torch.zeros((r1 - r0, 2), dtype=torch.float64, device="cuda")
+            mask = torch.from_numpy(fd.fixed_mask()[r0:r1].astype(np.uint8)).cuda()
+            pos = torch.from_numpy(np.nan_to_num(fd.fixed_positions()[r0:r1], nan=0.0)).cuda()
+            sf.run(g, gb.DEFAULT_TERMS, out, fixed_mask=mask, fixed_pos=pos, region=fd.region.bounds())
+            torch.cuda.synchronize()
+            blocks[rank] = (r0, out.cpu().numpy(), sf.plan.n_ghost)
+        except Exception as e:  # surfaced below
+            errors.append(repr(e))
+            hub.barrier.abort()
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errors, errors
+    full = np.zeros((fd.num_cells, 2))
+    for r0, blk, _ in blocks:
+        full[r0:r0 + len(blk)] = blk
+    assert all(b[2] > 0 for b in blocks)
+    single, _ = gb.gift_place(fd, adj, gb.GiftConfig(seed=0, jitter_scale=10.0))
+    ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, 200)
+    want = orc.place_epilogue(orc.gift_filter(ref, g32.astype(np.float64), DEFAULT), fd.fixed_mask(),
+                              fd.fixed_positions(), fd.region.bounds())
+    assert rel_l2(full, want) <= FP32_TOL
+    mask = fd.fixed_mask()
+    assert np.array_equal(full[mask], fd.fixed_positions()[mask])
+    assert rel_l2(full, single) <= FP32_TOL
