@@ -346,7 +346,7 @@ class CudaBackend:
 
     def hop(self, block, desc: dict):
         d = _hop_desc(desc)
-        self._lib.check(self.lib.gift_hop_fp32(self.ctx(), block.h, ctypes.byref(d)))
+        self._lib.check(self.lib.gift_hop_fp32(self.ctx(), block.h, ctypes.addressof(d)))
 
 
 class _Handle:
