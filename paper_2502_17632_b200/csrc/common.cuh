@@ -133,6 +133,13 @@ struct Csr {
   double mean_row = 0.0;
   std::map<double, double*> s64;  // sigma -> 1/sqrt(d+sigma)   (fp64, exact)
   std::map<double, float*> s32;   // sigma -> fp32 rounding of s64
+  bool sorted_rows = true;        // columns ascending within every row (canonical CSR)
+  struct Tiles {
+    int maxb = 0;
+    int32_t* nblk = nullptr;
+    int32_t* blk = nullptr;
+  };
+  std::map<int, Tiles> tiles;     // column-block lists of the tiled hop, per block width
   std::vector<void*> owned;       // everything above, freed on destroy
 };
 

@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -362,6 +363,55 @@ __device__ __forceinline__ float4 ld_stream_v4f32(const float* p, uint64_t pol) 
   return r;
 }
 
+// Row epilogue shared by every hop kernel: y = s o (A z + sigma z) per packed
+// chain; next-hop signal z' = s o y; completed terms accumulate alpha * y;
+// the final hop re-pins fixed rows and clamps movable rows (gift.py:112-118).
+template <int FIN, int FOUT>
+__device__ __forceinline__ void row_epilogue(const HopArgs& a, int64_t row, float (&acc)[FIN], uint64_t pol_z) {
+  if (a.part_out) {
+#pragma unroll
+    for (int f = 0; f < FIN; ++f) a.part_out[row * FIN + f] = acc[f];
+    return;
+  }
+  if (a.part_in) {
+#pragma unroll
+    for (int f = 0; f < FIN; ++f) acc[f] = a.part_in[row * FIN + f] + acc[f];
+  }
+  const VecF<FIN> zi = ld_z<FIN>(a.zin + row * FIN, pol_z);
+  float o[4] = {0.f, 0.f, 0.f, 0.f};
+  if (a.any_term && a.acc_read)
+    for (int cc = 0; cc < a.wcols; ++cc) o[cc] = a.acc[row * a.wcols + cc];
+  float zo[FOUT > 0 ? FOUT : 1];
+#pragma unroll
+  for (int f = 0; f < (FOUT > 0 ? FOUT : 1); ++f) zo[f] = 0.f;
+#pragma unroll
+  for (int f = 0; f < FIN; ++f) {
+    const int chn = f / a.wcols;
+    if (chn >= a.nch) break;
+    const int cc = f - chn * a.wcols;
+    const ChainArgs& ch = a.ch[chn];
+    const float si = ch.s[row];
+    const float y = si * (acc[f] + ch.sigma * zi.v[f]);
+    if (FOUT > 0 && ch.cont >= 0) zo[(ch.cont * a.wcols + cc) % (FOUT > 0 ? FOUT : 1)] = si * y;
+    if (ch.has_term) o[cc] = fmaf(ch.alpha, y, o[cc]);
+  }
+  if constexpr (FOUT == 4) *reinterpret_cast<float4*>(a.zout + row * 4) = make_float4(zo[0], zo[1], zo[2], zo[3]);
+  else if constexpr (FOUT == 2) *reinterpret_cast<float2*>(a.zout + row * 2) = make_float2(zo[0], zo[1]);
+  else if constexpr (FOUT == 1) a.zout[row] = zo[0];
+  if (!a.any_term) return;
+  if (!a.is_final) {
+    for (int cc = 0; cc < a.wcols; ++cc) a.acc[row * a.wcols + cc] = o[cc];
+    return;
+  }
+  for (int cc = 0; cc < a.wcols; ++cc) {
+    double v = (double)o[cc];
+    if (a.fixed_mask) v = a.fixed_mask[row] ? a.fixed_pos[row * 2 + cc] : np_clip(v, a.reg.v[cc], a.reg.v[cc + 2]);
+    const int64_t oi = row * a.out_ld + a.out_c0 + cc;
+    if (a.out_dtype == GIFT_DTYPE_F64) static_cast<double*>(a.out)[oi] = v;
+    else static_cast<float*>(a.out)[oi] = __double2float_rn(v);
+  }
+}
+
 // One hop for every chain packed in zin.  G lanes own a row; each lane
 // streams 4 consecutive (col, w) per 16-byte vector load (aligned down to a
 // multiple of 4, out-of-row slots masked), U such chunks in flight, so a lane
@@ -425,48 +475,169 @@ __global__ void __launch_bounds__(kBlock) k_hop(HopArgs a) {
     for (int f = 0; f < FIN; ++f) acc[f] += __shfl_xor_sync(gmask, acc[f], off, G);
   }
   if (lane != 0) return;
-  if (a.part_out) {
+  row_epilogue<FIN, FOUT>(a, row, acc, pol_z);
+}
+
+
+// ---- column-tiled hop: signal blocks staged in shared memory -----------------
+// A CTA owns a tile of kTileRows consecutive rows and walks the column blocks
+// (kTileFloats / FIN signal rows each) its entries touch, in ascending order.
+// Dense blocks are staged into shared memory once per tile and gathered from
+// there (bank-conflicted LDS instead of one L1 sector per gathered row);
+// sparse blocks (few entries, e.g. pad columns) are gathered from L2 directly.
+// Every row keeps a cursor and an fp32 accumulator in shared memory across
+// blocks; a G-lane group handles one row's segment of the current block,
+// detecting the segment end on the fly (first column >= block end).
+// Summation order: per block ascending, lane partials + fixed butterfly ->
+// deterministic.  The staged bytes per tile are (tile rows + the tile's
+// column window) * FIN * 4, a few % of the tile's (col, w) stream.
+constexpr int kTileRows = 2048;
+constexpr int kTileFloats = 16384;  // signal floats per staged block (64 KB)
+constexpr int kTileThreads = 512;
+
+struct TileArgs {
+  int C;          // signal rows per column block
+  int maxb;       // stride of blk per tile
+  int64_t ncols;  // signal rows addressable (columns of the CSR)
+  const int32_t* nblk;
+  const int32_t* blk;  // >= 0: staged block id, < 0: -(id+1) direct block
+};
+
+__global__ void k_tile_blocks(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, int C,
+                              int nblocks, int maxb, int thr, int32_t* __restrict__ nblk, int32_t* __restrict__ blk) {
+  extern __shared__ int hist[];
+  const int64_t tile = blockIdx.x;
+  const int64_t r0 = tile * kTileRows, r1 = min(n, r0 + kTileRows);
+  for (int i = threadIdx.x; i < nblocks; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (int64_t k = rowptr[r0] + threadIdx.x; k < rowptr[r1]; k += blockDim.x) atomicAdd(&hist[col[k] / C], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int cnt = 0;
+    for (int b = 0; b < nblocks; ++b)
+      if (hist[b] > 0) blk[tile * maxb + cnt++] = hist[b] >= thr ? b : -(b + 1);
+    nblk[tile] = cnt;
+  }
+}
+
+template <int FIN, int FOUT, int G>
+__global__ void __launch_bounds__(kTileThreads, 2) k_hop_tiled(HopArgs a, TileArgs t) {
+  extern __shared__ float4 smem_f4[];
+  float* zs = reinterpret_cast<float*>(smem_f4);
+  float* accs = zs + kTileFloats;
+  int* curs = reinterpret_cast<int*>(accs + kTileRows * FIN);
+  const int64_t r0 = (int64_t)blockIdx.x * kTileRows;
+  const int nrows = (int)min((int64_t)kTileRows, a.n - r0);
+  const int tid = threadIdx.x;
+  const int lane = tid & (G - 1);
+  const int rg = tid / G;
+  constexpr int NRG = kTileThreads / G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((tid & 31) & ~(G - 1)));
+  const uint64_t pol_s = policy_evict_first();
+  const uint64_t pol_z = policy_evict_last();
+  for (int i = tid; i < nrows * FIN; i += kTileThreads) accs[i] = 0.f;
+  for (int i = tid; i < nrows; i += kTileThreads) curs[i] = 0;
+  const int nb = t.nblk[blockIdx.x];
+  for (int bi = 0; bi < nb; ++bi) {
+    const int code = t.blk[(int64_t)blockIdx.x * t.maxb + bi];
+    const bool staged = code >= 0;
+    const int64_t cbase = (int64_t)(staged ? code : -code - 1) * t.C;
+    const int64_t cend = min(cbase + t.C, t.ncols);
+    __syncthreads();  // previous block done with zs; cursors visible
+    if (staged) {
+      const float4* src = reinterpret_cast<const float4*>(a.zin + cbase * FIN);
+      float4* dst = reinterpret_cast<float4*>(zs);
+      const int nv = (int)(((cend - cbase) * FIN + 3) / 4);
+      for (int i = tid; i < nv; i += kTileThreads) dst[i] = src[i];
+      __syncthreads();
+    }
+    for (int rr = rg; rr < nrows; rr += NRG) {
+      const int64_t rs = a.rowptr[r0 + rr];
+      const int64_t end = a.rowptr[r0 + rr + 1];
+      const int64_t beg = rs + curs[rr];
+      if (beg >= end) continue;  // uniform in the group
+      float acc[FIN];
 #pragma unroll
-    for (int f = 0; f < FIN; ++f) a.part_out[row * FIN + f] = acc[f];
-    return;
-  }
-  if (a.part_in) {
+      for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
+      int stop = INT_MAX;  // relative to rs
+      for (int64_t k0 = (beg & ~(int64_t)3) + 4 * lane;; k0 += 4 * G) {
+        int4 cv = make_int4(0, 0, 0, 0);
+        float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k0 < end) {
+          cv = ld_stream_v4s32(a.col + k0, pol_s);
+          wv = ld_stream_v4f32(a.w + k0, pol_s);
+        }
+        const int cc[4] = {cv.x, cv.y, cv.z, cv.w};
+        const float ww[4] = {wv.x, wv.y, wv.z, wv.w};
+        int my_stop = INT_MAX;
+        VecF<FIN> zv[4];
 #pragma unroll
-    for (int f = 0; f < FIN; ++f) acc[f] = a.part_in[row * FIN + f] + acc[f];
-  }
-  const VecF<FIN> zi = ld_z<FIN>(a.zin + row * FIN, pol_z);
-  float o[4] = {0.f, 0.f, 0.f, 0.f};
-  if (a.any_term && a.acc_read)
-    for (int cc = 0; cc < a.wcols; ++cc) o[cc] = a.acc[row * a.wcols + cc];
-  float zo[FOUT > 0 ? FOUT : 1];
+        for (int j = 0; j < 4; ++j) {
+          const int64_t idx = k0 + j;
+          bool in = idx >= beg && idx < end;
+          if (in && cc[j] >= cend) {
+            my_stop = min(my_stop, (int)(idx - rs));
+            in = false;
+          }
+          if (in) {
+            if (staged) {
+              const float* zp = zs + (int64_t)(cc[j] - cbase) * FIN;
+              if constexpr (FIN == 4) {
+                const float4 q = *reinterpret_cast<const float4*>(zp);
+                zv[j].v[0] = q.x; zv[j].v[1] = q.y; zv[j].v[2] = q.z; zv[j].v[3] = q.w;
+              } else if constexpr (FIN == 2) {
+                const float2 q = *reinterpret_cast<const float2*>(zp);
+                zv[j].v[0] = q.x; zv[j].v[1] = q.y;
+              } else {
+                zv[j].v[0] = zp[0];
+              }
+            } else {
+              zv[j] = ld_z<FIN>(a.zin + (int64_t)cc[j] * FIN, pol_z);
+            }
+          } else {
 #pragma unroll
-  for (int f = 0; f < (FOUT > 0 ? FOUT : 1); ++f) zo[f] = 0.f;
+            for (int f = 0; f < FIN; ++f) zv[j].v[f] = 0.f;
+          }
+        }
 #pragma unroll
-  for (int f = 0; f < FIN; ++f) {
-    const int chn = f / a.wcols;
-    if (chn >= a.nch) break;
-    const int cc = f - chn * a.wcols;
-    const ChainArgs& ch = a.ch[chn];
-    const float si = ch.s[row];
-    const float y = si * (acc[f] + ch.sigma * zi.v[f]);
-    if (FOUT > 0 && ch.cont >= 0) zo[(ch.cont * a.wcols + cc) % (FOUT > 0 ? FOUT : 1)] = si * y;
-    if (ch.has_term) o[cc] = fmaf(ch.alpha, y, o[cc]);
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int f = 0; f < FIN; ++f) acc[f] = fmaf(ww[j], zv[j].v[f], acc[f]);
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) my_stop = min(my_stop, __shfl_xor_sync(gmask, my_stop, off, G));
+        if (my_stop != INT_MAX) {
+          stop = my_stop;
+          break;
+        }
+        const int64_t next = (beg & ~(int64_t)3) + 4 * G * ((k0 - (beg & ~(int64_t)3)) / (4 * G) + 1);
+        if (next >= end) {
+          stop = (int)(end - rs);
+          break;
+        }
+      }
+#pragma unroll
+      for (int off = G / 2; off > 0; off >>= 1) {
+#pragma unroll
+        for (int f = 0; f < FIN; ++f) acc[f] += __shfl_xor_sync(gmask, acc[f], off, G);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int f = 0; f < FIN; ++f) accs[rr * FIN + f] += acc[f];
+        curs[rr] = stop;
+      }
+    }
   }
-  if constexpr (FOUT == 4) *reinterpret_cast<float4*>(a.zout + row * 4) = make_float4(zo[0], zo[1], zo[2], zo[3]);
-  else if constexpr (FOUT == 2) *reinterpret_cast<float2*>(a.zout + row * 2) = make_float2(zo[0], zo[1]);
-  else if constexpr (FOUT == 1) a.zout[row] = zo[0];
-  if (!a.any_term) return;
-  if (!a.is_final) {
-    for (int cc = 0; cc < a.wcols; ++cc) a.acc[row * a.wcols + cc] = o[cc];
-    return;
+  __syncthreads();
+  for (int rr = tid; rr < nrows; rr += kTileThreads) {
+    float acc[FIN];
+#pragma unroll
+    for (int f = 0; f < FIN; ++f) acc[f] = accs[rr * FIN + f];
+    row_epilogue<FIN, FOUT>(a, r0 + rr, acc, pol_z);
   }
-  for (int cc = 0; cc < a.wcols; ++cc) {
-    double v = (double)o[cc];
-    if (a.fixed_mask) v = a.fixed_mask[row] ? a.fixed_pos[row * 2 + cc] : np_clip(v, a.reg.v[cc], a.reg.v[cc + 2]);
-    const int64_t oi = row * a.out_ld + a.out_c0 + cc;
-    if (a.out_dtype == GIFT_DTYPE_F64) static_cast<double*>(a.out)[oi] = v;
-    else static_cast<float*>(a.out)[oi] = __double2float_rn(v);
-  }
+}
+
+size_t tiled_smem_bytes(int fin) {
+  return (size_t)kTileFloats * 4 + (size_t)kTileRows * fin * 4 + (size_t)kTileRows * 4;
 }
 
 // z0[i, chn*wcols + cc] = s_chn[i] * g[i, c0 + cc]
@@ -537,8 +708,35 @@ void launch_hop_g(Ctx* ctx, const HopArgs& a, int G) {
   GIFT_LAUNCH_CHECK(ctx);
 }
 
+template <int FIN, int FOUT>
+void launch_hop_tiled_g(Ctx* ctx, const HopArgs& a, const TileArgs& t, int G, int64_t ntiles) {
+  const size_t smem = tiled_smem_bytes(FIN);
+  cudaStream_t st = ctx->stream;
+  G = env_int("GIFT_TILE_G", G);
+  auto run = [&](auto kern) {
+    static bool configured = false;  // one per template instance
+    if (!configured) {
+      GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      configured = true;
+    }
+    kern<<<(unsigned)ntiles, kTileThreads, smem, st>>>(a, t);
+  };
+  if (G <= 8) run(k_hop_tiled<FIN, FOUT, 8>);
+  else run(k_hop_tiled<FIN, FOUT, 16>);
+  GIFT_LAUNCH_CHECK(ctx);
+}
+
 template <int FIN>
-void launch_hop_out(Ctx* ctx, const HopArgs& a, int fout, int G) {
+void launch_hop_out(Ctx* ctx, const HopArgs& a, int fout, int G, const TileArgs* t, int64_t ntiles) {
+  if (t) {
+    switch (fout) {
+      case 0: launch_hop_tiled_g<FIN, 0>(ctx, a, *t, G, ntiles); break;
+      case 1: launch_hop_tiled_g<FIN, 1>(ctx, a, *t, G, ntiles); break;
+      case 2: launch_hop_tiled_g<FIN, 2>(ctx, a, *t, G, ntiles); break;
+      default: launch_hop_tiled_g<FIN, 4>(ctx, a, *t, G, ntiles); break;
+    }
+    return;
+  }
   switch (fout) {
     case 0: launch_hop_g<FIN, 0>(ctx, a, G); break;
     case 1: launch_hop_g<FIN, 1>(ctx, a, G); break;
@@ -547,12 +745,13 @@ void launch_hop_out(Ctx* ctx, const HopArgs& a, int fout, int G) {
   }
 }
 
-void launch_hop(Ctx* ctx, const HopArgs& a, int fin, int fout, int G) {
+void launch_hop(Ctx* ctx, const HopArgs& a, int fin, int fout, int G, const TileArgs* t = nullptr,
+                int64_t ntiles = 0) {
   ProfScope prof(ctx, fin, a.nch);
   switch (fin) {
-    case 1: launch_hop_out<1>(ctx, a, fout, G); break;
-    case 2: launch_hop_out<2>(ctx, a, fout, G); break;
-    default: launch_hop_out<4>(ctx, a, fout, G); break;
+    case 1: launch_hop_out<1>(ctx, a, fout, G, t, ntiles); break;
+    case 2: launch_hop_out<2>(ctx, a, fout, G, t, ntiles); break;
+    default: launch_hop_out<4>(ctx, a, fout, G, t, ntiles); break;
   }
 }
 
@@ -735,6 +934,36 @@ static void bank_fp64_exact(Ctx* ctx, Csr* c, const std::vector<TermGroup>& grou
 
 // measured on B200 (profiles/r01_sweep_hop.txt): 8 lanes per row at mean
 // row length ~64 (c1), 16 at ~400 (c2/c3); one 4-nnz chunk in flight per lane
+// column-block list per row tile for signal width fin (cached on the csr)
+static bool tile_meta(Ctx* ctx, Csr* c, int fin, TileArgs* out, int64_t* ntiles) {
+  if (env_int("GIFT_HOP_TILED", 1) == 0 || c->n < kTileRows || !c->sorted_rows) return false;
+  const int C = kTileFloats / fin;
+  const int64_t nt = (c->n + kTileRows - 1) / kTileRows;
+  const int nblocks = (int)((c->n + C - 1) / C);
+  if ((size_t)nblocks * 4 > 200 * 1024) return false;  // histogram must fit in shared memory
+  auto it = c->tiles.find(C);
+  if (it == c->tiles.end()) {
+    Csr::Tiles tl;
+    tl.maxb = nblocks;
+    tl.nblk = static_cast<int32_t*>(csr_alloc(ctx, c, nt * sizeof(int32_t)));
+    tl.blk = static_cast<int32_t*>(csr_alloc(ctx, c, (size_t)nt * nblocks * sizeof(int32_t)));
+    const size_t smem = (size_t)nblocks * sizeof(int);
+    if (smem > 48 * 1024)
+      GIFT_CUDA(cudaFuncSetAttribute(k_tile_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_tile_blocks<<<(unsigned)nt, 512, smem, ctx->stream>>>(c->n, c->indptr, c->indices, C, nblocks, nblocks,
+                                                            kTileFloats / 8, tl.nblk, tl.blk);
+    GIFT_LAUNCH_CHECK(ctx);
+    it = c->tiles.emplace(C, tl).first;
+  }
+  out->C = C;
+  out->maxb = it->second.maxb;
+  out->ncols = c->n;
+  out->nblk = it->second.nblk;
+  out->blk = it->second.blk;
+  *ntiles = nt;
+  return true;
+}
+
 static int pick_group_lanes(double mean_row) {
   if (mean_row < 160) return 8;
   return 16;
@@ -829,7 +1058,10 @@ static void bank_fp32(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, in
         a.fixed_mask = fixed_mask;
         a.fixed_pos = fixed_pos;
         a.reg = reg;
-        launch_hop(ctx, a, fin, fout, G);
+        TileArgs tl;
+        int64_t ntiles = 0;
+        if (tile_meta(ctx, c, fin, &tl, &ntiles)) launch_hop(ctx, a, fin, fout, G, &tl, ntiles);
+        else launch_hop(ctx, a, fin, fout, G);
         if (a.any_term) acc_written = true;
         active.swap(next);
         std::swap(zin, zout);
@@ -921,6 +1153,7 @@ Csr* csr_from_arrays(Ctx* ctx, int64_t n_rows, int64_t nnz, const int64_t* d_ind
   c->values = static_cast<double*>(csr_alloc(ctx, c, (nnz > 0 ? nnz : 1) * sizeof(double)));
   c->mean_row = n_rows > 0 ? (double)nnz / n_rows : 0.0;
   c->has_diagonal = true;
+  c->sorted_rows = false;  // remapped shard blocks: owned columns first, ghosts after
   GIFT_CUDA(cudaMemcpyAsync(c->indptr, d_indptr, (n_rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream));
   if (nnz > 0) {
     GIFT_CUDA(cudaMemcpyAsync(c->indices, d_indices, nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
