@@ -21,6 +21,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <mutex>
+#include <set>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -570,7 +572,6 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_hop_tiled(HopArgs a, TileAr
         const int cc[4] = {cv.x, cv.y, cv.z, cv.w};
         const float ww[4] = {wv.x, wv.y, wv.z, wv.w};
         int my_stop = INT_MAX;
-        VecF<FIN> zv[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int64_t idx = k0 + j;
@@ -579,30 +580,30 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_hop_tiled(HopArgs a, TileAr
             my_stop = min(my_stop, (int)(idx - rs));
             in = false;
           }
+          float zq[FIN];
+#pragma unroll
+          for (int f = 0; f < FIN; ++f) zq[f] = 0.f;
           if (in) {
             if (staged) {
-              const float* zp = zs + (int64_t)(cc[j] - cbase) * FIN;
+              const float* zp = zs + (cc[j] - (int)cbase) * FIN;
               if constexpr (FIN == 4) {
                 const float4 q = *reinterpret_cast<const float4*>(zp);
-                zv[j].v[0] = q.x; zv[j].v[1] = q.y; zv[j].v[2] = q.z; zv[j].v[3] = q.w;
+                zq[0] = q.x; zq[1] = q.y; zq[2] = q.z; zq[3] = q.w;
               } else if constexpr (FIN == 2) {
                 const float2 q = *reinterpret_cast<const float2*>(zp);
-                zv[j].v[0] = q.x; zv[j].v[1] = q.y;
+                zq[0] = q.x; zq[1] = q.y;
               } else {
-                zv[j].v[0] = zp[0];
+                zq[0] = zp[0];
               }
             } else {
-              zv[j] = ld_z<FIN>(a.zin + (int64_t)cc[j] * FIN, pol_z);
+              const VecF<FIN> q = ld_z<FIN>(a.zin + (int64_t)cc[j] * FIN, pol_z);
+#pragma unroll
+              for (int f = 0; f < FIN; ++f) zq[f] = q.v[f];
             }
-          } else {
-#pragma unroll
-            for (int f = 0; f < FIN; ++f) zv[j].v[f] = 0.f;
           }
+#pragma unroll
+          for (int f = 0; f < FIN; ++f) acc[f] = fmaf(ww[j], zq[f], acc[f]);
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int f = 0; f < FIN; ++f) acc[f] = fmaf(ww[j], zv[j].v[f], acc[f]);
 #pragma unroll
         for (int off = G / 2; off > 0; off >>= 1) my_stop = min(my_stop, __shfl_xor_sync(gmask, my_stop, off, G));
         if (my_stop != INT_MAX) {
@@ -713,11 +714,13 @@ void launch_hop_tiled_g(Ctx* ctx, const HopArgs& a, const TileArgs& t, int G, in
   const size_t smem = tiled_smem_bytes(FIN);
   cudaStream_t st = ctx->stream;
   G = env_int("GIFT_TILE_G", G);
-  auto run = [&](auto kern) {
-    static bool configured = false;  // one per template instance
-    if (!configured) {
-      GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      configured = true;
+  auto run = [&](void (*kern)(HopArgs, TileArgs)) {
+    static std::mutex mu;
+    static std::set<const void*> configured;  // dynamic smem opt-in, once per instance
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (configured.insert((const void*)kern).second)
+        GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
     kern<<<(unsigned)ntiles, kTileThreads, smem, st>>>(a, t);
   };
