@@ -134,12 +134,13 @@ struct Csr {
   std::map<double, double*> s64;  // sigma -> 1/sqrt(d+sigma)   (fp64, exact)
   std::map<double, float*> s32;   // sigma -> fp32 rounding of s64
   bool sorted_rows = true;        // columns ascending within every row (canonical CSR)
-  struct Tiles {
-    int maxb = 0;
-    int32_t* nblk = nullptr;
-    int32_t* blk = nullptr;
-  };
-  std::map<int, Tiles> tiles;     // column-block lists of the tiled hop, per block width
+  // tiled-hop metadata (filter.cu tile_meta): per row tile, the column blocks it
+  // touches and each row's segment offset per block
+  bool tile_ready = false, tile_ok = false;
+  int32_t* tile_nblk = nullptr;
+  int64_t* tile_base = nullptr;
+  int32_t* tile_blk = nullptr;
+  uint16_t* tile_offs = nullptr;
   std::vector<void*> owned;       // everything above, freed on destroy
 };
 

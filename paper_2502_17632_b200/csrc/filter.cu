@@ -482,52 +482,94 @@ __global__ void __launch_bounds__(kBlock) k_hop(HopArgs a) {
 
 
 // ---- column-tiled hop: signal blocks staged in shared memory -----------------
-// A CTA owns a tile of kTileRows consecutive rows and walks the column blocks
-// (kTileFloats / FIN signal rows each) its entries touch, in ascending order.
+// A CTA owns a tile of kTileRows consecutive rows and walks, in ascending
+// order, the column blocks (kTileCols signal rows each) its entries touch.
 // Dense blocks are staged into shared memory once per tile and gathered from
-// there (bank-conflicted LDS instead of one L1 sector per gathered row);
-// sparse blocks (few entries, e.g. pad columns) are gathered from L2 directly.
-// Every row keeps a cursor and an fp32 accumulator in shared memory across
-// blocks; a G-lane group handles one row's segment of the current block,
-// detecting the segment end on the fly (first column >= block end).
-// Summation order: per block ascending, lane partials + fixed butterfly ->
-// deterministic.  The staged bytes per tile are (tile rows + the tile's
-// column window) * FIN * 4, a few % of the tile's (col, w) stream.
+// there (LDS instead of one L1 sector per gathered signal row); sparse blocks
+// (few entries: pad / macro columns) are gathered from L2 directly.  The
+// per-row split of each row into its block segments is precomputed once per
+// graph (u16 offsets, `tile_meta`), so a G-lane group streams exactly one
+// row's segment per (row, block) and skips empty ones without touching DRAM.
+// Rows keep an fp32 accumulator in shared memory across blocks.  Summation
+// order: blocks ascending, lane partials + fixed butterfly -> deterministic.
+// Staged bytes per tile = (tile rows + column window) * FIN * 4, a few % of
+// the tile's (col, w) stream.
 constexpr int kTileRows = 2048;
-constexpr int kTileFloats = 16384;  // signal floats per staged block (64 KB)
+constexpr int kTileCols = 4096;     // signal rows per column block (64 KB at FIN = 4)
 constexpr int kTileThreads = 512;
+constexpr int kStageMin = 2048;     // entries of a (tile, block) worth staging
 
 struct TileArgs {
-  int C;          // signal rows per column block
-  int maxb;       // stride of blk per tile
-  int64_t ncols;  // signal rows addressable (columns of the CSR)
-  const int32_t* nblk;
-  const int32_t* blk;  // >= 0: staged block id, < 0: -(id+1) direct block
+  int64_t ncols;             // signal rows addressable (columns of the CSR)
+  const int32_t* nblk;       // [tiles] blocks touched
+  const int64_t* blk_base;   // [tiles] first slot of the tile in blk / offs
+  const int32_t* blk;        // [slots] >= 0: staged block id, < 0: -(id+1) direct block
+  const uint16_t* offs;      // [slots * kTileRows] row segment start (relative to the row) per block
 };
 
-__global__ void k_tile_blocks(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, int C,
-                              int nblocks, int maxb, int thr, int32_t* __restrict__ nblk, int32_t* __restrict__ blk) {
+// pass 1: which blocks a tile touches (and whether to stage them)
+__global__ void k_tile_count(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                             int nblocks, int32_t* __restrict__ hist_out, int32_t* __restrict__ nblk,
+                             int32_t* __restrict__ maxlen) {
   extern __shared__ int hist[];
   const int64_t tile = blockIdx.x;
   const int64_t r0 = tile * kTileRows, r1 = min(n, r0 + kTileRows);
   for (int i = threadIdx.x; i < nblocks; i += blockDim.x) hist[i] = 0;
   __syncthreads();
-  for (int64_t k = rowptr[r0] + threadIdx.x; k < rowptr[r1]; k += blockDim.x) atomicAdd(&hist[col[k] / C], 1);
+  for (int64_t k = rowptr[r0] + threadIdx.x; k < rowptr[r1]; k += blockDim.x) atomicAdd(&hist[col[k] / kTileCols], 1);
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    const int64_t L = rowptr[r + 1] - rowptr[r];
+    atomicMax(maxlen, L > INT_MAX ? INT_MAX : (int)L);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     int cnt = 0;
-    for (int b = 0; b < nblocks; ++b)
-      if (hist[b] > 0) blk[tile * maxb + cnt++] = hist[b] >= thr ? b : -(b + 1);
+    for (int b = 0; b < nblocks; ++b) cnt += hist[b] > 0;
     nblk[tile] = cnt;
+  }
+  for (int i = threadIdx.x; i < nblocks; i += blockDim.x) hist_out[tile * nblocks + i] = hist[i];
+}
+
+// pass 2: block list + per-row segment offsets (thread per row, one sweep of its columns)
+__global__ void k_tile_offsets(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                               int nblocks, const int32_t* __restrict__ hist, const int64_t* __restrict__ blk_base,
+                               int32_t* __restrict__ blk, uint16_t* __restrict__ offs) {
+  __shared__ int list[4096];
+  __shared__ int nb;
+  const int64_t tile = blockIdx.x;
+  const int64_t r0 = tile * kTileRows, r1 = min(n, r0 + kTileRows);
+  const int64_t base = blk_base[tile];
+  if (threadIdx.x == 0) {
+    int cnt = 0;
+    for (int b = 0; b < nblocks; ++b) {
+      const int h = hist[tile * nblocks + b];
+      if (h > 0) {
+        blk[base + cnt] = h >= kStageMin ? b : -(b + 1);
+        if (cnt < 4096) list[cnt] = b;
+        ++cnt;
+      }
+    }
+    nb = cnt;
+  }
+  __syncthreads();
+  const int cnt = nb;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    const int64_t rs = rowptr[r], L = rowptr[r + 1] - rs;
+    int64_t j = 0;
+    for (int bi = 0; bi < cnt; ++bi) {
+      const int64_t lo = (int64_t)(bi < 4096 ? list[bi] : -1) * kTileCols;
+      while (j < L && col[rs + j] < lo) ++j;
+      offs[(base + bi) * kTileRows + (r - r0)] = (uint16_t)j;
+    }
   }
 }
 
 template <int FIN, int FOUT, int G>
 __global__ void __launch_bounds__(kTileThreads, 2) k_hop_tiled(HopArgs a, TileArgs t) {
   extern __shared__ float4 smem_f4[];
-  float* zs = reinterpret_cast<float*>(smem_f4);
-  float* accs = zs + kTileFloats;
-  int* curs = reinterpret_cast<int*>(accs + kTileRows * FIN);
+  float* zs = reinterpret_cast<float*>(smem_f4);              // [kTileCols * FIN]
+  float* accs = zs + kTileCols * FIN;                          // [kTileRows * FIN]
+  int* rstart = reinterpret_cast<int*>(accs + kTileRows * FIN);  // [kTileRows + 1], relative to the tile
   const int64_t r0 = (int64_t)blockIdx.x * kTileRows;
   const int nrows = (int)min((int64_t)kTileRows, a.n - r0);
   const int tid = threadIdx.x;
@@ -537,49 +579,43 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_hop_tiled(HopArgs a, TileAr
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((tid & 31) & ~(G - 1)));
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_z = policy_evict_last();
+  const int64_t tile_lo = a.rowptr[r0];
   for (int i = tid; i < nrows * FIN; i += kTileThreads) accs[i] = 0.f;
-  for (int i = tid; i < nrows; i += kTileThreads) curs[i] = 0;
+  for (int i = tid; i <= nrows; i += kTileThreads) rstart[i] = (int)(a.rowptr[r0 + i] - tile_lo);
   const int nb = t.nblk[blockIdx.x];
+  const int64_t sbase = t.blk_base[blockIdx.x];
   for (int bi = 0; bi < nb; ++bi) {
-    const int code = t.blk[(int64_t)blockIdx.x * t.maxb + bi];
+    const int code = t.blk[sbase + bi];
     const bool staged = code >= 0;
-    const int64_t cbase = (int64_t)(staged ? code : -code - 1) * t.C;
-    const int64_t cend = min(cbase + t.C, t.ncols);
-    __syncthreads();  // previous block done with zs; cursors visible
+    const int64_t cbase = (int64_t)(staged ? code : -code - 1) * kTileCols;
+    __syncthreads();  // previous block done with zs (and rstart / accs initialised)
     if (staged) {
+      const int64_t cend = min(cbase + kTileCols, t.ncols);
       const float4* src = reinterpret_cast<const float4*>(a.zin + cbase * FIN);
       float4* dst = reinterpret_cast<float4*>(zs);
       const int nv = (int)(((cend - cbase) * FIN + 3) / 4);
+#pragma unroll 4
       for (int i = tid; i < nv; i += kTileThreads) dst[i] = src[i];
       __syncthreads();
     }
+    const uint16_t* o0 = t.offs + (sbase + bi) * kTileRows;
+    const uint16_t* o1 = (bi + 1 < nb) ? o0 + kTileRows : nullptr;
     for (int rr = rg; rr < nrows; rr += NRG) {
-      const int64_t rs = a.rowptr[r0 + rr];
-      const int64_t end = a.rowptr[r0 + rr + 1];
-      const int64_t beg = rs + curs[rr];
+      const int rs = rstart[rr];
+      const int64_t beg = tile_lo + rs + o0[rr];
+      const int64_t end = tile_lo + (o1 ? rs + o1[rr] : rstart[rr + 1]);
       if (beg >= end) continue;  // uniform in the group
       float acc[FIN];
 #pragma unroll
       for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
-      int stop = INT_MAX;  // relative to rs
-      for (int64_t k0 = (beg & ~(int64_t)3) + 4 * lane;; k0 += 4 * G) {
-        int4 cv = make_int4(0, 0, 0, 0);
-        float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (k0 < end) {
-          cv = ld_stream_v4s32(a.col + k0, pol_s);
-          wv = ld_stream_v4f32(a.w + k0, pol_s);
-        }
+      for (int64_t k0 = (beg & ~(int64_t)3) + 4 * lane; k0 < end; k0 += 4 * G) {
+        const int4 cv = ld_stream_v4s32(a.col + k0, pol_s);
+        const float4 wv = ld_stream_v4f32(a.w + k0, pol_s);
         const int cc[4] = {cv.x, cv.y, cv.z, cv.w};
         const float ww[4] = {wv.x, wv.y, wv.z, wv.w};
-        int my_stop = INT_MAX;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int64_t idx = k0 + j;
-          bool in = idx >= beg && idx < end;
-          if (in && cc[j] >= cend) {
-            my_stop = min(my_stop, (int)(idx - rs));
-            in = false;
-          }
+          const bool in = (k0 + j >= beg) && (k0 + j < end);
           float zq[FIN];
 #pragma unroll
           for (int f = 0; f < FIN; ++f) zq[f] = 0.f;
@@ -604,17 +640,6 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_hop_tiled(HopArgs a, TileAr
 #pragma unroll
           for (int f = 0; f < FIN; ++f) acc[f] = fmaf(ww[j], zq[f], acc[f]);
         }
-#pragma unroll
-        for (int off = G / 2; off > 0; off >>= 1) my_stop = min(my_stop, __shfl_xor_sync(gmask, my_stop, off, G));
-        if (my_stop != INT_MAX) {
-          stop = my_stop;
-          break;
-        }
-        const int64_t next = (beg & ~(int64_t)3) + 4 * G * ((k0 - (beg & ~(int64_t)3)) / (4 * G) + 1);
-        if (next >= end) {
-          stop = (int)(end - rs);
-          break;
-        }
       }
 #pragma unroll
       for (int off = G / 2; off > 0; off >>= 1) {
@@ -624,7 +649,6 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_hop_tiled(HopArgs a, TileAr
       if (lane == 0) {
 #pragma unroll
         for (int f = 0; f < FIN; ++f) accs[rr * FIN + f] += acc[f];
-        curs[rr] = stop;
       }
     }
   }
@@ -638,7 +662,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_hop_tiled(HopArgs a, TileAr
 }
 
 size_t tiled_smem_bytes(int fin) {
-  return (size_t)kTileFloats * 4 + (size_t)kTileRows * fin * 4 + (size_t)kTileRows * 4;
+  return (size_t)kTileCols * fin * 4 + (size_t)kTileRows * fin * 4 + (size_t)(kTileRows + 1) * 4;
 }
 
 // z0[i, chn*wcols + cc] = s_chn[i] * g[i, c0 + cc]
@@ -937,32 +961,53 @@ static void bank_fp64_exact(Ctx* ctx, Csr* c, const std::vector<TermGroup>& grou
 
 // measured on B200 (profiles/r01_sweep_hop.txt): 8 lanes per row at mean
 // row length ~64 (c1), 16 at ~400 (c2/c3); one 4-nnz chunk in flight per lane
-// column-block list per row tile for signal width fin (cached on the csr)
+// column-block lists + per-row block offsets of the tiled hop (cached on the csr)
 static bool tile_meta(Ctx* ctx, Csr* c, int fin, TileArgs* out, int64_t* ntiles) {
-  if (env_int("GIFT_HOP_TILED", 1) == 0 || c->n < kTileRows || !c->sorted_rows) return false;
-  const int C = kTileFloats / fin;
+  (void)fin;
+  if (env_int("GIFT_HOP_TILED", 1) == 0 || !c->sorted_rows) return false;
+  if (c->n < env_int("GIFT_TILE_MIN_ROWS", 262144) || c->mean_row < env_int("GIFT_TILE_MIN_MEAN", 100)) return false;
   const int64_t nt = (c->n + kTileRows - 1) / kTileRows;
-  const int nblocks = (int)((c->n + C - 1) / C);
+  const int nblocks = (int)((c->n + kTileCols - 1) / kTileCols);
   if ((size_t)nblocks * 4 > 200 * 1024) return false;  // histogram must fit in shared memory
-  auto it = c->tiles.find(C);
-  if (it == c->tiles.end()) {
-    Csr::Tiles tl;
-    tl.maxb = nblocks;
-    tl.nblk = static_cast<int32_t*>(csr_alloc(ctx, c, nt * sizeof(int32_t)));
-    tl.blk = static_cast<int32_t*>(csr_alloc(ctx, c, (size_t)nt * nblocks * sizeof(int32_t)));
+  if (!c->tile_ready) {
+    c->tile_ready = true;
+    c->tile_ok = false;
+    cudaStream_t st = ctx->stream;
+    DevBuf<int32_t> hist(ctx, (size_t)nt * nblocks), maxlen(ctx, 1);
+    c->tile_nblk = static_cast<int32_t*>(csr_alloc(ctx, c, nt * sizeof(int32_t)));
+    c->tile_base = static_cast<int64_t*>(csr_alloc(ctx, c, (nt + 1) * sizeof(int64_t)));
+    GIFT_CUDA(cudaMemsetAsync(maxlen.p, 0, sizeof(int32_t), st));
     const size_t smem = (size_t)nblocks * sizeof(int);
     if (smem > 48 * 1024)
-      GIFT_CUDA(cudaFuncSetAttribute(k_tile_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_tile_blocks<<<(unsigned)nt, 512, smem, ctx->stream>>>(c->n, c->indptr, c->indices, C, nblocks, nblocks,
-                                                            kTileFloats / 8, tl.nblk, tl.blk);
+      GIFT_CUDA(cudaFuncSetAttribute(k_tile_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_tile_count<<<(unsigned)nt, 512, smem, st>>>(c->n, c->indptr, c->indices, nblocks, hist.p, c->tile_nblk, maxlen.p);
     GIFT_LAUNCH_CHECK(ctx);
-    it = c->tiles.emplace(C, tl).first;
+    size_t bytes = 0;
+    GIFT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->tile_nblk, c->tile_base, nt, st));
+    DevBuf<char> tmp(ctx, bytes);
+    GIFT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, c->tile_nblk, c->tile_base, nt, st));
+    ctx->launches += 2;
+    int32_t last = 0, mx = 0;
+    int64_t lastb = 0;
+    GIFT_CUDA(cudaMemcpyAsync(&last, c->tile_nblk + nt - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    GIFT_CUDA(cudaMemcpyAsync(&lastb, c->tile_base + nt - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GIFT_CUDA(cudaMemcpyAsync(&mx, maxlen.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    GIFT_CUDA(cudaStreamSynchronize(st));
+    const int64_t slots = lastb + last;
+    if (mx >= 65536) return false;  // u16 row offsets
+    c->tile_blk = static_cast<int32_t*>(csr_alloc(ctx, c, (slots > 0 ? slots : 1) * sizeof(int32_t)));
+    c->tile_offs = static_cast<uint16_t*>(csr_alloc(ctx, c, (slots > 0 ? slots : 1) * kTileRows * sizeof(uint16_t)));
+    k_tile_offsets<<<(unsigned)nt, 256, 0, st>>>(c->n, c->indptr, c->indices, nblocks, hist.p, c->tile_base,
+                                                c->tile_blk, c->tile_offs);
+    GIFT_LAUNCH_CHECK(ctx);
+    c->tile_ok = true;
   }
-  out->C = C;
-  out->maxb = it->second.maxb;
+  if (!c->tile_ok) return false;
   out->ncols = c->n;
-  out->nblk = it->second.nblk;
-  out->blk = it->second.blk;
+  out->nblk = c->tile_nblk;
+  out->blk_base = c->tile_base;
+  out->blk = c->tile_blk;
+  out->offs = c->tile_offs;
   *ntiles = nt;
   return true;
 }
