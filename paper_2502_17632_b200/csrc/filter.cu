@@ -964,7 +964,7 @@ static void bank_fp64_exact(Ctx* ctx, Csr* c, const std::vector<TermGroup>& grou
 // column-block lists + per-row block offsets of the tiled hop (cached on the csr)
 static bool tile_meta(Ctx* ctx, Csr* c, int fin, TileArgs* out, int64_t* ntiles) {
   (void)fin;
-  if (env_int("GIFT_HOP_TILED", 1) == 0 || !c->sorted_rows) return false;
+  if (env_int("GIFT_HOP_TILED", 0) == 0 || !c->sorted_rows) return false;  // opt-in: slower than k_hop (profiles/r01_tiled_v2_c2.txt)
   if (c->n < env_int("GIFT_TILE_MIN_ROWS", 262144) || c->mean_row < env_int("GIFT_TILE_MIN_MEAN", 100)) return false;
   const int64_t nt = (c->n + kTileRows - 1) / kTileRows;
   const int nblocks = (int)((c->n + kTileCols - 1) / kTileCols);
