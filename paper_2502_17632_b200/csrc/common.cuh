@@ -134,13 +134,17 @@ struct Csr {
   std::map<double, double*> s64;  // sigma -> 1/sqrt(d+sigma)   (fp64, exact)
   std::map<double, float*> s32;   // sigma -> fp32 rounding of s64
   bool sorted_rows = true;        // columns ascending within every row (canonical CSR)
-  // tiled-hop metadata (filter.cu tile_meta): per row tile, the column blocks it
-  // touches and each row's segment offset per block
-  bool tile_ready = false, tile_ok = false;
-  int32_t* tile_nblk = nullptr;
-  int64_t* tile_base = nullptr;
-  int32_t* tile_blk = nullptr;
-  uint16_t* tile_offs = nullptr;
+  // block-major tiled copy of the matrix for the fp32 hop (bmt.cu), lazy
+  struct Bmt {
+    bool ready = false, ok = false;
+    int64_t ntiles = 0, nseg = 0, nunits = 0;
+    int64_t* tile_seg = nullptr;   // [ntiles + 1]
+    int32_t* seg_code = nullptr;   // [nseg]: staged block id, or -(id + 1) for direct gathers
+    int64_t* seg_unit = nullptr;   // [nseg + 1]
+    int64_t* unit_start = nullptr; // [nunits + 1]
+    uint32_t* idx = nullptr;       // [nnz] (row in tile << 12) | (column in block)
+    float* w = nullptr;            // [nnz]
+  } bmt;
   std::vector<void*> owned;       // everything above, freed on destroy
 };
 

@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "hop.cuh"
 
 namespace gift {
 
@@ -236,16 +237,6 @@ __global__ void k_load_f64(int64_t m, int in_dtype, const void* __restrict__ g, 
                                       : (double)static_cast<const float*>(g)[i];
 }
 
-// np.clip for floats: MIN(MAX(x, lo), hi), NaN passes, PyArray_MAX(a,b) = a > b ? a : b
-__device__ __forceinline__ double np_clip(double x, double lo, double hi) {
-  double t = isnan(x) ? x : (x > lo ? x : lo);
-  return isnan(t) ? t : (t < hi ? t : hi);
-}
-
-struct Region4 {
-  double v[4];
-};
-
 // gift.py:112-118 on an fp64 [n, 2] result, written in out_dtype
 __global__ void k_epilogue_f64(int64_t n, int64_t ncols, const double* __restrict__ res,
                                const uint8_t* __restrict__ fixed_mask, const double* __restrict__ fixed_pos,
@@ -260,157 +251,6 @@ __global__ void k_epilogue_f64(int64_t n, int64_t ncols, const double* __restric
     }
     if (out_dtype == GIFT_DTYPE_F64) static_cast<double*>(out)[i] = v;
     else static_cast<float*>(out)[i] = __double2float_rn(v);
-  }
-}
-
-// ---- fp32 fused hop ---------------------------------------------------------
-struct ChainArgs {
-  const float* s;  // fp32 s_sigma
-  float sigma;
-  int cont;        // slot of this chain in zout, -1 if the chain ends here
-  int has_term;    // a term of this chain completes at this hop
-  float alpha;     // its weight (sum if several terms share k)
-};
-
-struct HopArgs {
-  const int64_t* rowptr;
-  const int32_t* col;
-  const float* w;
-  int64_t n;          // one past the last row processed
-  int64_t row_begin;  // first row processed
-  const float* part_in;  // [rows, FIN] partial sums added before the epilogue (split hop), or null
-  float* part_out;       // write the raw row sums here and skip the epilogue (split hop), or null
-  const float* zin;  // [n, FIN]
-  float* zout;       // [n, FOUT]
-  int wcols;         // signal columns per chain
-  int nch;           // chains packed in zin
-  ChainArgs ch[4];
-  float* acc;        // [n, wcols] fp32 bank accumulator
-  int acc_read;      // 0: first write (out = zeros + ...)
-  int is_final;
-  int out_dtype;
-  void* out;
-  int64_t out_ld;
-  int64_t out_c0;
-  const uint8_t* fixed_mask;
-  const double* fixed_pos;
-  Region4 reg;
-  int any_term;
-};
-
-template <int F>
-struct VecF;
-template <>
-struct VecF<1> {
-  float v[1];
-};
-template <>
-struct VecF<2> {
-  float v[2];
-};
-template <>
-struct VecF<4> {
-  float v[4];
-};
-
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-
-// gathered signal rows: L1-allocating, keep in L2
-template <int F>
-__device__ __forceinline__ VecF<F> ld_z(const float* p, uint64_t pol);
-template <>
-__device__ __forceinline__ VecF<1> ld_z<1>(const float* p, uint64_t pol) {
-  VecF<1> r;
-  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r.v[0]) : "l"(p), "l"(pol));
-  return r;
-}
-template <>
-__device__ __forceinline__ VecF<2> ld_z<2>(const float* p, uint64_t pol) {
-  VecF<2> r;
-  asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
-               : "=f"(r.v[0]), "=f"(r.v[1])
-               : "l"(p), "l"(pol));
-  return r;
-}
-template <>
-__device__ __forceinline__ VecF<4> ld_z<4>(const float* p, uint64_t pol) {
-  VecF<4> r;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
-               : "l"(p), "l"(pol));
-  return r;
-}
-
-__device__ __forceinline__ int4 ld_stream_v4s32(const int32_t* p, uint64_t pol) {
-  int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ float4 ld_stream_v4f32(const float* p, uint64_t pol) {
-  float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-               : "l"(p), "l"(pol));
-  return r;
-}
-
-// Row epilogue shared by every hop kernel: y = s o (A z + sigma z) per packed
-// chain; next-hop signal z' = s o y; completed terms accumulate alpha * y;
-// the final hop re-pins fixed rows and clamps movable rows (gift.py:112-118).
-template <int FIN, int FOUT>
-__device__ __forceinline__ void row_epilogue(const HopArgs& a, int64_t row, float (&acc)[FIN], uint64_t pol_z) {
-  if (a.part_out) {
-#pragma unroll
-    for (int f = 0; f < FIN; ++f) a.part_out[row * FIN + f] = acc[f];
-    return;
-  }
-  if (a.part_in) {
-#pragma unroll
-    for (int f = 0; f < FIN; ++f) acc[f] = a.part_in[row * FIN + f] + acc[f];
-  }
-  const VecF<FIN> zi = ld_z<FIN>(a.zin + row * FIN, pol_z);
-  float o[4] = {0.f, 0.f, 0.f, 0.f};
-  if (a.any_term && a.acc_read)
-    for (int cc = 0; cc < a.wcols; ++cc) o[cc] = a.acc[row * a.wcols + cc];
-  float zo[FOUT > 0 ? FOUT : 1];
-#pragma unroll
-  for (int f = 0; f < (FOUT > 0 ? FOUT : 1); ++f) zo[f] = 0.f;
-#pragma unroll
-  for (int f = 0; f < FIN; ++f) {
-    const int chn = f / a.wcols;
-    if (chn >= a.nch) break;
-    const int cc = f - chn * a.wcols;
-    const ChainArgs& ch = a.ch[chn];
-    const float si = ch.s[row];
-    const float y = si * (acc[f] + ch.sigma * zi.v[f]);
-    if (FOUT > 0 && ch.cont >= 0) zo[(ch.cont * a.wcols + cc) % (FOUT > 0 ? FOUT : 1)] = si * y;
-    if (ch.has_term) o[cc] = fmaf(ch.alpha, y, o[cc]);
-  }
-  if constexpr (FOUT == 4) *reinterpret_cast<float4*>(a.zout + row * 4) = make_float4(zo[0], zo[1], zo[2], zo[3]);
-  else if constexpr (FOUT == 2) *reinterpret_cast<float2*>(a.zout + row * 2) = make_float2(zo[0], zo[1]);
-  else if constexpr (FOUT == 1) a.zout[row] = zo[0];
-  if (!a.any_term) return;
-  if (!a.is_final) {
-    for (int cc = 0; cc < a.wcols; ++cc) a.acc[row * a.wcols + cc] = o[cc];
-    return;
-  }
-  for (int cc = 0; cc < a.wcols; ++cc) {
-    double v = (double)o[cc];
-    if (a.fixed_mask) v = a.fixed_mask[row] ? a.fixed_pos[row * 2 + cc] : np_clip(v, a.reg.v[cc], a.reg.v[cc + 2]);
-    const int64_t oi = row * a.out_ld + a.out_c0 + cc;
-    if (a.out_dtype == GIFT_DTYPE_F64) static_cast<double*>(a.out)[oi] = v;
-    else static_cast<float*>(a.out)[oi] = __double2float_rn(v);
   }
 }
 
@@ -481,190 +321,6 @@ __global__ void __launch_bounds__(kBlock) k_hop(HopArgs a) {
 }
 
 
-// ---- column-tiled hop: signal blocks staged in shared memory -----------------
-// A CTA owns a tile of kTileRows consecutive rows and walks, in ascending
-// order, the column blocks (kTileCols signal rows each) its entries touch.
-// Dense blocks are staged into shared memory once per tile and gathered from
-// there (LDS instead of one L1 sector per gathered signal row); sparse blocks
-// (few entries: pad / macro columns) are gathered from L2 directly.  The
-// per-row split of each row into its block segments is precomputed once per
-// graph (u16 offsets, `tile_meta`), so a G-lane group streams exactly one
-// row's segment per (row, block) and skips empty ones without touching DRAM.
-// Rows keep an fp32 accumulator in shared memory across blocks.  Summation
-// order: blocks ascending, lane partials + fixed butterfly -> deterministic.
-// Staged bytes per tile = (tile rows + column window) * FIN * 4, a few % of
-// the tile's (col, w) stream.
-constexpr int kTileRows = 2048;
-constexpr int kTileCols = 4096;     // signal rows per column block (64 KB at FIN = 4)
-constexpr int kTileThreads = 512;
-constexpr int kStageMin = 2048;     // entries of a (tile, block) worth staging
-
-struct TileArgs {
-  int64_t ncols;             // signal rows addressable (columns of the CSR)
-  const int32_t* nblk;       // [tiles] blocks touched
-  const int64_t* blk_base;   // [tiles] first slot of the tile in blk / offs
-  const int32_t* blk;        // [slots] >= 0: staged block id, < 0: -(id+1) direct block
-  const uint16_t* offs;      // [slots * kTileRows] row segment start (relative to the row) per block
-};
-
-// pass 1: which blocks a tile touches (and whether to stage them)
-__global__ void k_tile_count(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                             int nblocks, int32_t* __restrict__ hist_out, int32_t* __restrict__ nblk,
-                             int32_t* __restrict__ maxlen) {
-  extern __shared__ int hist[];
-  const int64_t tile = blockIdx.x;
-  const int64_t r0 = tile * kTileRows, r1 = min(n, r0 + kTileRows);
-  for (int i = threadIdx.x; i < nblocks; i += blockDim.x) hist[i] = 0;
-  __syncthreads();
-  for (int64_t k = rowptr[r0] + threadIdx.x; k < rowptr[r1]; k += blockDim.x) atomicAdd(&hist[col[k] / kTileCols], 1);
-  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-    const int64_t L = rowptr[r + 1] - rowptr[r];
-    atomicMax(maxlen, L > INT_MAX ? INT_MAX : (int)L);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int cnt = 0;
-    for (int b = 0; b < nblocks; ++b) cnt += hist[b] > 0;
-    nblk[tile] = cnt;
-  }
-  for (int i = threadIdx.x; i < nblocks; i += blockDim.x) hist_out[tile * nblocks + i] = hist[i];
-}
-
-// pass 2: block list + per-row segment offsets (thread per row, one sweep of its columns)
-__global__ void k_tile_offsets(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                               int nblocks, const int32_t* __restrict__ hist, const int64_t* __restrict__ blk_base,
-                               int32_t* __restrict__ blk, uint16_t* __restrict__ offs) {
-  __shared__ int list[4096];
-  __shared__ int nb;
-  const int64_t tile = blockIdx.x;
-  const int64_t r0 = tile * kTileRows, r1 = min(n, r0 + kTileRows);
-  const int64_t base = blk_base[tile];
-  if (threadIdx.x == 0) {
-    int cnt = 0;
-    for (int b = 0; b < nblocks; ++b) {
-      const int h = hist[tile * nblocks + b];
-      if (h > 0) {
-        blk[base + cnt] = h >= kStageMin ? b : -(b + 1);
-        if (cnt < 4096) list[cnt] = b;
-        ++cnt;
-      }
-    }
-    nb = cnt;
-  }
-  __syncthreads();
-  const int cnt = nb;
-  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-    const int64_t rs = rowptr[r], L = rowptr[r + 1] - rs;
-    int64_t j = 0;
-    for (int bi = 0; bi < cnt; ++bi) {
-      const int64_t lo = (int64_t)(bi < 4096 ? list[bi] : -1) * kTileCols;
-      while (j < L && col[rs + j] < lo) ++j;
-      offs[(base + bi) * kTileRows + (r - r0)] = (uint16_t)j;
-    }
-  }
-}
-
-template <int FIN, int FOUT, int G>
-__global__ void __launch_bounds__(kTileThreads, 2) k_hop_tiled(HopArgs a, TileArgs t) {
-  extern __shared__ float4 smem_f4[];
-  float* zs = reinterpret_cast<float*>(smem_f4);              // [kTileCols * FIN]
-  float* accs = zs + kTileCols * FIN;                          // [kTileRows * FIN]
-  int* rstart = reinterpret_cast<int*>(accs + kTileRows * FIN);  // [kTileRows + 1], relative to the tile
-  const int64_t r0 = (int64_t)blockIdx.x * kTileRows;
-  const int nrows = (int)min((int64_t)kTileRows, a.n - r0);
-  const int tid = threadIdx.x;
-  const int lane = tid & (G - 1);
-  const int rg = tid / G;
-  constexpr int NRG = kTileThreads / G;
-  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((tid & 31) & ~(G - 1)));
-  const uint64_t pol_s = policy_evict_first();
-  const uint64_t pol_z = policy_evict_last();
-  const int64_t tile_lo = a.rowptr[r0];
-  for (int i = tid; i < nrows * FIN; i += kTileThreads) accs[i] = 0.f;
-  for (int i = tid; i <= nrows; i += kTileThreads) rstart[i] = (int)(a.rowptr[r0 + i] - tile_lo);
-  const int nb = t.nblk[blockIdx.x];
-  const int64_t sbase = t.blk_base[blockIdx.x];
-  for (int bi = 0; bi < nb; ++bi) {
-    const int code = t.blk[sbase + bi];
-    const bool staged = code >= 0;
-    const int64_t cbase = (int64_t)(staged ? code : -code - 1) * kTileCols;
-    __syncthreads();  // previous block done with zs (and rstart / accs initialised)
-    if (staged) {
-      const int64_t cend = min(cbase + kTileCols, t.ncols);
-      const float4* src = reinterpret_cast<const float4*>(a.zin + cbase * FIN);
-      float4* dst = reinterpret_cast<float4*>(zs);
-      const int nv = (int)(((cend - cbase) * FIN + 3) / 4);
-#pragma unroll 4
-      for (int i = tid; i < nv; i += kTileThreads) dst[i] = src[i];
-      __syncthreads();
-    }
-    const uint16_t* o0 = t.offs + (sbase + bi) * kTileRows;
-    const uint16_t* o1 = (bi + 1 < nb) ? o0 + kTileRows : nullptr;
-    for (int rr = rg; rr < nrows; rr += NRG) {
-      const int rs = rstart[rr];
-      const int64_t beg = tile_lo + rs + o0[rr];
-      const int64_t end = tile_lo + (o1 ? rs + o1[rr] : rstart[rr + 1]);
-      if (beg >= end) continue;  // uniform in the group
-      float acc[FIN];
-#pragma unroll
-      for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
-      for (int64_t k0 = (beg & ~(int64_t)3) + 4 * lane; k0 < end; k0 += 4 * G) {
-        const int4 cv = ld_stream_v4s32(a.col + k0, pol_s);
-        const float4 wv = ld_stream_v4f32(a.w + k0, pol_s);
-        const int cc[4] = {cv.x, cv.y, cv.z, cv.w};
-        const float ww[4] = {wv.x, wv.y, wv.z, wv.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const bool in = (k0 + j >= beg) && (k0 + j < end);
-          float zq[FIN];
-#pragma unroll
-          for (int f = 0; f < FIN; ++f) zq[f] = 0.f;
-          if (in) {
-            if (staged) {
-              const float* zp = zs + (cc[j] - (int)cbase) * FIN;
-              if constexpr (FIN == 4) {
-                const float4 q = *reinterpret_cast<const float4*>(zp);
-                zq[0] = q.x; zq[1] = q.y; zq[2] = q.z; zq[3] = q.w;
-              } else if constexpr (FIN == 2) {
-                const float2 q = *reinterpret_cast<const float2*>(zp);
-                zq[0] = q.x; zq[1] = q.y;
-              } else {
-                zq[0] = zp[0];
-              }
-            } else {
-              const VecF<FIN> q = ld_z<FIN>(a.zin + (int64_t)cc[j] * FIN, pol_z);
-#pragma unroll
-              for (int f = 0; f < FIN; ++f) zq[f] = q.v[f];
-            }
-          }
-#pragma unroll
-          for (int f = 0; f < FIN; ++f) acc[f] = fmaf(ww[j], zq[f], acc[f]);
-        }
-      }
-#pragma unroll
-      for (int off = G / 2; off > 0; off >>= 1) {
-#pragma unroll
-        for (int f = 0; f < FIN; ++f) acc[f] += __shfl_xor_sync(gmask, acc[f], off, G);
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int f = 0; f < FIN; ++f) accs[rr * FIN + f] += acc[f];
-      }
-    }
-  }
-  __syncthreads();
-  for (int rr = tid; rr < nrows; rr += kTileThreads) {
-    float acc[FIN];
-#pragma unroll
-    for (int f = 0; f < FIN; ++f) acc[f] = accs[rr * FIN + f];
-    row_epilogue<FIN, FOUT>(a, r0 + rr, acc, pol_z);
-  }
-}
-
-size_t tiled_smem_bytes(int fin) {
-  return (size_t)kTileCols * fin * 4 + (size_t)kTileRows * fin * 4 + (size_t)(kTileRows + 1) * 4;
-}
-
 // z0[i, chn*wcols + cc] = s_chn[i] * g[i, c0 + cc]
 template <int F>
 __global__ void k_prep(int64_t n, int wcols, int nch, const float* s0, const float* s1, const float* s2,
@@ -703,12 +359,6 @@ int pow2_ceil(int v) {
   return p;
 }
 
-// lanes per row and chunks in flight; GIFT_HOP_G / GIFT_HOP_U override (tuning sweeps)
-static int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
-
 template <int FIN, int FOUT>
 void launch_hop_g(Ctx* ctx, const HopArgs& a, int G) {
   if (a.n <= a.row_begin) return;
@@ -733,37 +383,8 @@ void launch_hop_g(Ctx* ctx, const HopArgs& a, int G) {
   GIFT_LAUNCH_CHECK(ctx);
 }
 
-template <int FIN, int FOUT>
-void launch_hop_tiled_g(Ctx* ctx, const HopArgs& a, const TileArgs& t, int G, int64_t ntiles) {
-  const size_t smem = tiled_smem_bytes(FIN);
-  cudaStream_t st = ctx->stream;
-  G = env_int("GIFT_TILE_G", G);
-  auto run = [&](void (*kern)(HopArgs, TileArgs)) {
-    static std::mutex mu;
-    static std::set<const void*> configured;  // dynamic smem opt-in, once per instance
-    {
-      std::lock_guard<std::mutex> lk(mu);
-      if (configured.insert((const void*)kern).second)
-        GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    }
-    kern<<<(unsigned)ntiles, kTileThreads, smem, st>>>(a, t);
-  };
-  if (G <= 8) run(k_hop_tiled<FIN, FOUT, 8>);
-  else run(k_hop_tiled<FIN, FOUT, 16>);
-  GIFT_LAUNCH_CHECK(ctx);
-}
-
 template <int FIN>
-void launch_hop_out(Ctx* ctx, const HopArgs& a, int fout, int G, const TileArgs* t, int64_t ntiles) {
-  if (t) {
-    switch (fout) {
-      case 0: launch_hop_tiled_g<FIN, 0>(ctx, a, *t, G, ntiles); break;
-      case 1: launch_hop_tiled_g<FIN, 1>(ctx, a, *t, G, ntiles); break;
-      case 2: launch_hop_tiled_g<FIN, 2>(ctx, a, *t, G, ntiles); break;
-      default: launch_hop_tiled_g<FIN, 4>(ctx, a, *t, G, ntiles); break;
-    }
-    return;
-  }
+void launch_hop_out(Ctx* ctx, const HopArgs& a, int fout, int G) {
   switch (fout) {
     case 0: launch_hop_g<FIN, 0>(ctx, a, G); break;
     case 1: launch_hop_g<FIN, 1>(ctx, a, G); break;
@@ -772,13 +393,13 @@ void launch_hop_out(Ctx* ctx, const HopArgs& a, int fout, int G, const TileArgs*
   }
 }
 
-void launch_hop(Ctx* ctx, const HopArgs& a, int fin, int fout, int G, const TileArgs* t = nullptr,
-                int64_t ntiles = 0) {
+void launch_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout, int G, bool allow_bmt) {
   ProfScope prof(ctx, fin, a.nch);
+  if (allow_bmt && bmt_hop(ctx, c, a, fin, fout)) return;
   switch (fin) {
-    case 1: launch_hop_out<1>(ctx, a, fout, G, t, ntiles); break;
-    case 2: launch_hop_out<2>(ctx, a, fout, G, t, ntiles); break;
-    default: launch_hop_out<4>(ctx, a, fout, G, t, ntiles); break;
+    case 1: launch_hop_out<1>(ctx, a, fout, G); break;
+    case 2: launch_hop_out<2>(ctx, a, fout, G); break;
+    default: launch_hop_out<4>(ctx, a, fout, G); break;
   }
 }
 
@@ -807,6 +428,8 @@ static const float* csr_w32(Ctx* ctx, Csr* c) {
   }
   return c->w32;
 }
+
+const float* csr_w32_public(Ctx* ctx, Csr* c) { return csr_w32(ctx, c); }
 
 // sigma validation + isolated-node check (graph.py:174-180); returns s64
 static const double* csr_scale(Ctx* ctx, Csr* c, double sigma) {
@@ -961,57 +584,6 @@ static void bank_fp64_exact(Ctx* ctx, Csr* c, const std::vector<TermGroup>& grou
 
 // measured on B200 (profiles/r01_sweep_hop.txt): 8 lanes per row at mean
 // row length ~64 (c1), 16 at ~400 (c2/c3); one 4-nnz chunk in flight per lane
-// column-block lists + per-row block offsets of the tiled hop (cached on the csr)
-static bool tile_meta(Ctx* ctx, Csr* c, int fin, TileArgs* out, int64_t* ntiles) {
-  (void)fin;
-  if (env_int("GIFT_HOP_TILED", 0) == 0 || !c->sorted_rows) return false;  // opt-in: slower than k_hop (profiles/r01_tiled_v2_c2.txt)
-  if (c->n < env_int("GIFT_TILE_MIN_ROWS", 262144) || c->mean_row < env_int("GIFT_TILE_MIN_MEAN", 100)) return false;
-  const int64_t nt = (c->n + kTileRows - 1) / kTileRows;
-  const int nblocks = (int)((c->n + kTileCols - 1) / kTileCols);
-  if ((size_t)nblocks * 4 > 200 * 1024) return false;  // histogram must fit in shared memory
-  if (!c->tile_ready) {
-    c->tile_ready = true;
-    c->tile_ok = false;
-    cudaStream_t st = ctx->stream;
-    DevBuf<int32_t> hist(ctx, (size_t)nt * nblocks), maxlen(ctx, 1);
-    c->tile_nblk = static_cast<int32_t*>(csr_alloc(ctx, c, nt * sizeof(int32_t)));
-    c->tile_base = static_cast<int64_t*>(csr_alloc(ctx, c, (nt + 1) * sizeof(int64_t)));
-    GIFT_CUDA(cudaMemsetAsync(maxlen.p, 0, sizeof(int32_t), st));
-    const size_t smem = (size_t)nblocks * sizeof(int);
-    if (smem > 48 * 1024)
-      GIFT_CUDA(cudaFuncSetAttribute(k_tile_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_tile_count<<<(unsigned)nt, 512, smem, st>>>(c->n, c->indptr, c->indices, nblocks, hist.p, c->tile_nblk, maxlen.p);
-    GIFT_LAUNCH_CHECK(ctx);
-    size_t bytes = 0;
-    GIFT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->tile_nblk, c->tile_base, nt, st));
-    DevBuf<char> tmp(ctx, bytes);
-    GIFT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, c->tile_nblk, c->tile_base, nt, st));
-    ctx->launches += 2;
-    int32_t last = 0, mx = 0;
-    int64_t lastb = 0;
-    GIFT_CUDA(cudaMemcpyAsync(&last, c->tile_nblk + nt - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    GIFT_CUDA(cudaMemcpyAsync(&lastb, c->tile_base + nt - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    GIFT_CUDA(cudaMemcpyAsync(&mx, maxlen.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    GIFT_CUDA(cudaStreamSynchronize(st));
-    const int64_t slots = lastb + last;
-    if (mx >= 65536) return false;  // u16 row offsets
-    c->tile_blk = static_cast<int32_t*>(csr_alloc(ctx, c, (slots > 0 ? slots : 1) * sizeof(int32_t)));
-    c->tile_offs = static_cast<uint16_t*>(csr_alloc(ctx, c, (slots > 0 ? slots : 1) * kTileRows * sizeof(uint16_t)));
-    k_tile_offsets<<<(unsigned)nt, 256, 0, st>>>(c->n, c->indptr, c->indices, nblocks, hist.p, c->tile_base,
-                                                c->tile_blk, c->tile_offs);
-    GIFT_LAUNCH_CHECK(ctx);
-    c->tile_ok = true;
-  }
-  if (!c->tile_ok) return false;
-  out->ncols = c->n;
-  out->nblk = c->tile_nblk;
-  out->blk_base = c->tile_base;
-  out->blk = c->tile_blk;
-  out->offs = c->tile_offs;
-  *ntiles = nt;
-  return true;
-}
-
 static int pick_group_lanes(double mean_row) {
   if (mean_row < 160) return 8;
   return 16;
@@ -1106,10 +678,7 @@ static void bank_fp32(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, in
         a.fixed_mask = fixed_mask;
         a.fixed_pos = fixed_pos;
         a.reg = reg;
-        TileArgs tl;
-        int64_t ntiles = 0;
-        if (tile_meta(ctx, c, fin, &tl, &ntiles)) launch_hop(ctx, a, fin, fout, G, &tl, ntiles);
-        else launch_hop(ctx, a, fin, fout, G);
+        launch_hop(ctx, c, a, fin, fout, G, true);
         if (a.any_term) acc_written = true;
         active.swap(next);
         std::swap(zin, zout);
@@ -1165,7 +734,7 @@ void hop_fp32(Ctx* ctx, Csr* c, const gift_hop_desc* d) {
   a.fixed_mask = d->fixed_mask;
   a.fixed_pos = d->fixed_pos;
   memcpy(a.reg.v, d->region, sizeof(a.reg.v));
-  launch_hop(ctx, a, d->fin, d->fout, pick_group_lanes(c->mean_row));
+  launch_hop(ctx, c, a, d->fin, d->fout, pick_group_lanes(c->mean_row), false);
 }
 
 void pack_fp32(Ctx* ctx, int64_t n, int wcols, int nch, const float* const* s, int in_dtype, const void* g,

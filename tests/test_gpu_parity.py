@@ -398,9 +398,10 @@ def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, world):
     assert rel_l2(full, single) <= FP32_TOL
 
 
-@pytest.mark.parametrize("config,scale,cap", [("c2", 0.05, 200), ("c3", 0.03, 200), ("c1", 0.2, None)])
-def test_tiled_hop_matches_oracle_and_row_kernel(gb, orc, monkeypatch, config, scale, cap):
-    """Force the shared-memory column-tiled hop on small graphs (it is normally
+@pytest.mark.parametrize("config,scale,cap", [("c2", 0.05, 200), ("c3", 0.03, 200), ("c1", 0.2, None),
+                                              ("c0", 1.0, None), ("c2", 0.01, None)])
+def test_bmt_hop_matches_oracle_and_row_kernel(gb, orc, monkeypatch, config, scale, cap):
+    """Force the block-major tiled hop (bmt.cu) on small graphs (it is normally
     reserved for >= 256k rows) and check it against the oracle and the
     row-parallel kernel."""
     from paper_2502_17632_b200 import synth
@@ -409,11 +410,11 @@ def test_tiled_hop_matches_oracle_and_row_kernel(gb, orc, monkeypatch, config, s
     ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, cap)
     g32 = synth.signal_fp32(fd, seed=3)
     want = orc.gift_filter(ref, g32.astype(np.float64), DEFAULT)
-    monkeypatch.setenv("GIFT_HOP_TILED", "0")
+    monkeypatch.setenv("GIFT_BMT", "0")
     row_kernel = gb.gift_filter(gb.build_clique_graph(fd, max_clique_pins=cap), g32)
-    monkeypatch.setenv("GIFT_HOP_TILED", "1")
-    monkeypatch.setenv("GIFT_TILE_MIN_ROWS", "1")
-    monkeypatch.setenv("GIFT_TILE_MIN_MEAN", "1")
+    monkeypatch.setenv("GIFT_BMT", "1")
+    monkeypatch.setenv("GIFT_BMT_MIN_ROWS", "1")
+    monkeypatch.setenv("GIFT_BMT_MIN_MEAN", "1")
     adj = gb.build_clique_graph(fd, max_clique_pins=cap)
     tiled = gb.gift_filter(adj, g32)
     assert rel_l2(tiled, want) <= FP32_TOL
