@@ -1,29 +1,34 @@
-// bmt.cu -- block-major tiled (BMT) fp32 hop: the signal is gathered from
-// shared memory instead of through L1.
+// bmt.cu -- sliced block-major tiled (BMT) fp32 hop: signal gathers from
+// shared memory, 6-byte matrix entries, no cross-lane reductions.
 //
-// Why: the row kernel (filter.cu k_hop) streams (col, w) at full coalescing
-// but every stored entry gathers one signal row z_j (8-16 B) from L1/L2; on
-// c2/c3 those scattered gathers keep the L1TEX pipe ~90% busy and the kernel
-// at ~50-60% of HBM bandwidth (profiles/r01_v2_k_hop_c3.txt).  Netlist
-// graphs are banded (nets live in +-W index windows), so a tile of rows only
-// touches a few column blocks.  BMT reorders a copy of the matrix so that
-// each (row tile, column block) pair is one contiguous SEGMENT:
+// Why: the row kernel (filter.cu k_hop) streams (col, w) fully coalesced but
+// each stored entry gathers a signal row z_j (8-16 B) through L1; on c2/c3
+// those scattered gathers keep the L1TEX pipe ~90% busy and cap the kernel at
+// ~50-60% of HBM bandwidth (profiles/r01_v2_k_hop_c3.txt).  Netlist graphs
+// are banded (nets live in +-W index windows): a tile of rows touches only a
+// few column blocks.  BMT stores a reordered copy of the matrix:
 //
-//   tiles of kR = 2048 rows, blocks of kC = 4096 columns;
-//   segments ordered tile-major, block ascending; inside a segment entries
-//   keep CSR order (row, then column) -- a stable sort by (tile, block);
-//   entry = u32 (row in tile << 12 | column in block) + f32 weight: 8 B, the
-//   same stream bytes as (int32 col, f32 w).
+//   row tiles of kR = 2048 rows x column blocks of kC = 4096 columns;
+//   a SEGMENT = the entries of one (tile, block) pair; segments tile-major,
+//   blocks ascending;
+//   inside a segment, every row's run of entries goes to one lane of a
+//   SLICE of 32 runs (runs sorted by length, longest first, so slices are
+//   nearly rectangular); a slice stores its runs lane-interleaved in groups
+//   of 4: slot(k, lane) = base + (k/4)*128 + lane*4 + k%4 -- each lane reads
+//   4 consecutive entries with one 8-byte (columns) + one 16-byte (weights)
+//   load, the warp reads 768 contiguous bytes;
+//   entry = u16 column-in-block + f32 weight = 6 B (vs 8 B for int32 col);
+//   padding = column kC, which addresses a zero row of the staged block.
 //
-// A CTA owns a tile.  For each segment it stages the 64 KB signal block in
-// shared memory (dense segments; sparse ones -- pad / macro columns -- gather
-// from L2 directly) and its warps stream the segment: warp-level units are
-// row-aligned runs of ~256 entries, so every row of a segment is summed by
-// one warp: lane-local segmented scan over 8 entries, a 5-step segmented
-// Hillis-Steele scan across lanes, a register carry across chunks.  Row sums
-// land in a per-tile shared accumulator (blocks ascending), then the shared
-// row epilogue of hop.cuh runs per row.  Fixed reduction tree everywhere ->
-// deterministic.
+// Kernel: a CTA owns a tile.  Per segment it stages the block's signal rows
+// in shared memory (dense segments; sparse ones -- pad / macro columns -- are
+// gathered from L2 directly), then warps take slices: each lane sums its
+// row's run sequentially in ascending column order and adds it to the row's
+// shared fp32 accumulator (each row has one run per segment, so no two lanes
+// touch a row in one segment).  After the last segment the shared row
+// epilogue (hop.cuh) runs per row.  Summation order is fixed -> deterministic.
+// (A first BMT version summed segment runs with warp segmented scans; it was
+// instruction-bound at ~4 instructions per entry -- profiles/r01_bmt_scan_c2.txt.)
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -38,13 +43,11 @@ namespace gift {
 
 namespace {
 
-constexpr int kR = 2048;        // rows per tile (11 bits)
+constexpr int kR = 2048;          // rows per tile (11 bits)
 constexpr int kCbits = 12;
-constexpr int kC = 1 << kCbits;  // columns per block
+constexpr int kC = 1 << kCbits;   // columns per block; column kC = zero padding row
 constexpr int kThreads = 512;
-template <int FIN>
-__host__ __device__ constexpr int kVof() { return FIN >= 4 ? 4 : 8; }  // entries per lane per chunk (register budget: 64 at 2 CTAs/SM)
-constexpr int kStage = 1024;    // a segment with >= kStage entries stages its block
+constexpr int kStage = 1024;      // a segment with >= kStage entries stages its block
 constexpr int kBlock = 256;
 
 __global__ void k_mark_rows(int64_t n, const int64_t* __restrict__ indptr, int32_t* __restrict__ mark) {
@@ -56,6 +59,11 @@ struct MaxI32 {
   __device__ __forceinline__ int32_t operator()(int32_t a, int32_t b) const { return a > b ? a : b; }
 };
 
+__global__ void k_iota64(int64_t n, int64_t* __restrict__ p) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = i;
+}
+
+// sort key (tile, block) and payload (weight bits, row in tile, column in block)
 __global__ void k_bmt_keys(int64_t nnz, const int32_t* __restrict__ row_of, const int32_t* __restrict__ col,
                            const float* __restrict__ w, int bb, uint32_t* __restrict__ key,
                            uint64_t* __restrict__ payload) {
@@ -67,54 +75,110 @@ __global__ void k_bmt_keys(int64_t nnz, const int32_t* __restrict__ row_of, cons
   }
 }
 
-// segment heads (key change) and unit boundaries (segment heads, plus row
-// heads whose row group of D consecutive rows differs from the previous row's)
-__global__ void k_bmt_flags(int64_t nnz, const uint32_t* __restrict__ key, const uint64_t* __restrict__ payload,
-                            int D, uint8_t* __restrict__ seg_head, uint8_t* __restrict__ unit_head,
-                            unsigned long long* __restrict__ row_heads) {
-  unsigned long long cnt = 0;
+// segment heads (new (tile, block)) and run heads (new (segment, row)), counted
+__global__ void k_bmt_heads(int64_t nnz, const uint32_t* __restrict__ key, const uint64_t* __restrict__ pay,
+                            uint8_t* __restrict__ seg_head, uint8_t* __restrict__ run_head,
+                            unsigned long long* __restrict__ counts) {
+  unsigned long long ns = 0, nr = 0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
     const bool sh = k == 0 || key[k] != key[k - 1];
-    const uint32_t r = (uint32_t)payload[k] >> kCbits;
-    const uint32_t rp = k == 0 ? 0xffffffffu : (uint32_t)payload[k - 1] >> kCbits;
-    const bool rh = sh || r != rp;
+    const bool rh = sh || ((uint32_t)pay[k] >> kCbits) != ((uint32_t)pay[k - 1] >> kCbits);
     seg_head[k] = sh;
-    unit_head[k] = sh || (rh && (r / D) != (rp / D));
-    cnt += rh;
+    run_head[k] = rh;
+    ns += sh;
+    nr += rh;
   }
-  if (row_heads) atomicAdd(row_heads, cnt);
+  for (int off = 16; off > 0; off >>= 1) {
+    ns += __shfl_xor_sync(0xffffffffu, ns, off);
+    nr += __shfl_xor_sync(0xffffffffu, nr, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(counts, ns);
+    atomicAdd(counts + 1, nr);
+  }
 }
 
-__global__ void k_bmt_split(int64_t nnz, const uint64_t* __restrict__ payload, uint32_t* __restrict__ idx,
-                            float* __restrict__ w) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t p = payload[k];
-    idx[k] = (uint32_t)p;
-    w[k] = __uint_as_float((uint32_t)(p >> 32));
-  }
-}
-
-__global__ void k_bmt_segs(int64_t nseg, const int64_t* __restrict__ seg_start, const uint32_t* __restrict__ key_s,
-                           int64_t nnz, int bb, const int64_t* __restrict__ unit_start, int64_t nunits,
-                           int32_t* __restrict__ seg_code, int64_t* __restrict__ seg_unit,
-                           uint32_t* __restrict__ seg_tile) {
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s <= nseg; s += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a = s < nseg ? seg_start[s] : nnz;
-    // first unit starting at or after a (segment starts are unit starts)
-    int64_t lo = 0, hi = nunits;
-    while (lo < hi) {
+// per run: sort key (segment, longest first); the stable sort keeps row order among equals
+__global__ void k_run_keys(int64_t nruns, const int64_t* __restrict__ run_start, int64_t nnz,
+                           const int64_t* __restrict__ seg_start, int64_t nseg, uint64_t* __restrict__ rkey) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nruns; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = run_start[i], b = i + 1 < nruns ? run_start[i + 1] : nnz;
+    int64_t lo = 0, hi = nseg;  // segment = last seg_start <= a
+    while (hi - lo > 1) {
       const int64_t mid = (lo + hi) >> 1;
-      if (unit_start[mid] < a) lo = mid + 1;
+      if (seg_start[mid] <= a) lo = mid;
       else hi = mid;
     }
-    seg_unit[s] = lo;
-    if (s < nseg) {
-      const int64_t b = s + 1 < nseg ? seg_start[s + 1] : nnz;
-      const uint32_t k = key_s[a];
-      const int blk = (int)(k & ((1u << bb) - 1));
-      seg_code[s] = (b - a) >= kStage ? blk : -(blk + 1);
-      seg_tile[s] = k >> bb;
+    const uint64_t len = (uint64_t)(b - a);  // <= kC distinct columns in a block
+    rkey[i] = ((uint64_t)lo << 13) | ((uint64_t)kC - len);
+  }
+}
+
+// first sorted run of every segment
+__global__ void k_seg_runs(int64_t nruns, const uint64_t* __restrict__ rkey_s, int64_t nseg,
+                           int64_t* __restrict__ seg_run) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= nruns; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = i < nruns ? (int64_t)(rkey_s[i] >> 13) : nseg;
+    const int64_t sp = i > 0 ? (int64_t)(rkey_s[i - 1] >> 13) : -1;
+    for (int64_t t = sp + 1; t <= s; ++t) seg_run[t] = i;
+  }
+}
+
+__global__ void k_seg_slices(int64_t nseg, const int64_t* __restrict__ seg_run, int64_t* __restrict__ nsl) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x)
+    nsl[s] = (seg_run[s + 1] - seg_run[s] + 31) / 32;
+}
+
+// slot count of each slice: its longest (first) run rounded up to 4, x 32 lanes
+__global__ void k_slice_len(int64_t nseg, const int64_t* __restrict__ seg_run, const int64_t* __restrict__ seg_slice,
+                            const uint64_t* __restrict__ rkey_s, int64_t* __restrict__ slice_slots) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r0 = seg_run[s], r1 = seg_run[s + 1];
+    for (int64_t j = 0; r0 + 32 * j < r1; ++j) {
+      const int64_t len = kC - (int64_t)(rkey_s[r0 + 32 * j] & 0x1fff);
+      slice_slots[seg_slice[s] + j] = ((len + 3) / 4) * 4 * 32;
     }
+  }
+}
+
+// scatter every run's entries into its slice lane (CTA per segment, thread per run)
+__global__ void k_scatter_runs(int64_t nseg, const int64_t* __restrict__ seg_run, const int64_t* __restrict__ seg_slice,
+                               const int64_t* __restrict__ run_perm, const int64_t* __restrict__ run_start,
+                               int64_t nruns, int64_t nnz, const uint64_t* __restrict__ pay,
+                               const int64_t* __restrict__ slice_off, uint16_t* __restrict__ slice_rows,
+                               uint16_t* __restrict__ col, float* __restrict__ w) {
+  for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
+    const int64_t r0 = seg_run[s], r1 = seg_run[s + 1];
+    for (int64_t q = r0 + threadIdx.x; q < r1; q += blockDim.x) {
+      const int64_t pos = q - r0;
+      const int64_t slice = seg_slice[s] + pos / 32;
+      const int lane = (int)(pos % 32);
+      const int64_t run = run_perm[q];
+      const int64_t a = run_start[run], b = run + 1 < nruns ? run_start[run + 1] : nnz;
+      const int64_t base = slice_off[slice] + 4 * lane;
+      slice_rows[slice * 32 + lane] = (uint16_t)((uint32_t)pay[a] >> kCbits);
+      for (int64_t k = 0; k < b - a; ++k) {
+        const uint64_t p = pay[a + k];
+        const int64_t slot = base + (k / 4) * 128 + (k % 4);
+        col[slot] = (uint16_t)(p & (kC - 1));
+        w[slot] = __uint_as_float((uint32_t)(p >> 32));
+      }
+    }
+  }
+}
+
+__global__ void k_fill_u16(int64_t m, uint16_t v, uint16_t* __restrict__ p) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+__global__ void k_seg_meta(int64_t nseg, const int64_t* __restrict__ seg_start, const uint32_t* __restrict__ key_s,
+                           int64_t nnz, int bb, int32_t* __restrict__ seg_code, uint32_t* __restrict__ seg_tile) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = seg_start[s], b = s + 1 < nseg ? seg_start[s + 1] : nnz;
+    const uint32_t k = key_s[a];
+    const int blk = (int)(k & ((1u << bb) - 1));
+    seg_code[s] = (b - a) >= kStage ? blk : -(blk + 1);
+    seg_tile[s] = k >> bb;
   }
 }
 
@@ -131,28 +195,83 @@ struct BmtArgs {
   int64_t ncols;
   const int64_t* tile_seg;
   const int32_t* seg_code;
-  const int64_t* seg_unit;
-  const int64_t* unit_start;
-  const uint32_t* idx;
+  const int64_t* seg_slice;
+  const int64_t* slice_off;
+  const uint16_t* slice_rows;
+  const uint16_t* col;
   const float* w;
 };
 
-template <int F>
-__device__ __forceinline__ void add_to(float (&d)[F], const float (&s)[F]) {
+__device__ __forceinline__ uint2 ld_stream_v2u32(const void* p, uint64_t pol) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+template <int FIN, bool STAGED>
+__device__ __forceinline__ void gather_fma(float (&acc)[FIN], float w, int c, const float* zs, const float* zg,
+                                           uint64_t pol_z) {
+  if constexpr (STAGED) {
+    const float* zp = zs + c * FIN;  // c == kC hits the zero row
+    if constexpr (FIN == 4) {
+      const float4 q = *reinterpret_cast<const float4*>(zp);
+      acc[0] = fmaf(w, q.x, acc[0]); acc[1] = fmaf(w, q.y, acc[1]);
+      acc[2] = fmaf(w, q.z, acc[2]); acc[3] = fmaf(w, q.w, acc[3]);
+    } else if constexpr (FIN == 2) {
+      const float2 q = *reinterpret_cast<const float2*>(zp);
+      acc[0] = fmaf(w, q.x, acc[0]); acc[1] = fmaf(w, q.y, acc[1]);
+    } else {
+      acc[0] = fmaf(w, zp[0], acc[0]);
+    }
+  } else {
+    if (c < kC) {  // padding slots skip the gather
+      const VecF<FIN> q = ld_z<FIN>(zg + (int64_t)c * FIN, pol_z);
 #pragma unroll
-  for (int f = 0; f < F; ++f) d[f] += s[f];
+      for (int f = 0; f < FIN; ++f) acc[f] = fmaf(w, q.v[f], acc[f]);
+    }
+  }
+}
+
+template <int FIN, bool STAGED>
+__device__ __forceinline__ void run_slices(const BmtArgs& b, int64_t s, const float* zs, const float* zg,
+                                           float* accs, int lane, int warp, uint64_t pol_s, uint64_t pol_z) {
+  constexpr int NW = kThreads / 32;
+  const int64_t sl_end = b.seg_slice[s + 1];
+  for (int64_t sl = b.seg_slice[s] + warp; sl < sl_end; sl += NW) {
+    const int64_t off = b.slice_off[sl];
+    const int64_t steps = (b.slice_off[sl + 1] - off) / 128;
+    const int row = b.slice_rows[sl * 32 + lane];
+    float acc[FIN];
+#pragma unroll
+    for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
+    const uint16_t* cp = b.col + off + 4 * lane;
+    const float* wp = b.w + off + 4 * lane;
+#pragma unroll 2
+    for (int64_t k = 0; k < steps; ++k) {
+      const uint2 cv = ld_stream_v2u32(cp + k * 128, pol_s);
+      const float4 wv = ld_stream_v4f32(wp + k * 128, pol_s);
+      gather_fma<FIN, STAGED>(acc, wv.x, (int)(cv.x & 0xffff), zs, zg, pol_z);
+      gather_fma<FIN, STAGED>(acc, wv.y, (int)(cv.x >> 16), zs, zg, pol_z);
+      gather_fma<FIN, STAGED>(acc, wv.z, (int)(cv.y & 0xffff), zs, zg, pol_z);
+      gather_fma<FIN, STAGED>(acc, wv.w, (int)(cv.y >> 16), zs, zg, pol_z);
+    }
+    if (row != 0xffff) {
+#pragma unroll
+      for (int f = 0; f < FIN; ++f) accs[row * FIN + f] += acc[f];
+    }
+  }
 }
 
 template <int FIN, int FOUT>
 __global__ void __launch_bounds__(kThreads, 2) k_hop_bmt(HopArgs a, BmtArgs b) {
-  constexpr int kV = kVof<FIN>();
   extern __shared__ float4 smem_f4[];
-  float* zs = reinterpret_cast<float*>(smem_f4);  // [kC * FIN]
-  float* accs = zs + kC * FIN;                      // [kR * FIN]
+  float* zs = reinterpret_cast<float*>(smem_f4);  // [(kC + 1) * FIN], row kC stays zero
+  float* accs = zs + (kC + 1) * FIN;                // [kR * FIN]
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  constexpr int NW = kThreads / 32;
   const int64_t tile = blockIdx.x;
   const int64_t r0 = tile * kR;
   const int nrows = (int)min((int64_t)kR, a.n - r0);
@@ -164,151 +283,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_hop_bmt(HopArgs a, BmtArgs b) {
     const int code = b.seg_code[s];
     const bool staged = code >= 0;
     const int64_t cbase = (int64_t)(staged ? code : -code - 1) * kC;
-    __syncthreads();  // previous segment's readers are done with zs
+    const float* zg = a.zin + cbase * FIN;
     if (staged) {
+      __syncthreads();  // previous segment's readers are done with zs
       const int64_t cend = min(cbase + kC, b.ncols);
-      const float4* src = reinterpret_cast<const float4*>(a.zin + cbase * FIN);
+      const int nf = (int)((cend - cbase) * FIN);
+      const int nv = nf / 4;
+      const float4* src = reinterpret_cast<const float4*>(zg);
       float4* dst = reinterpret_cast<float4*>(zs);
-      const int nv = (int)(((cend - cbase) * FIN + 3) / 4);
 #pragma unroll 4
       for (int i = tid; i < nv; i += kThreads) dst[i] = src[i];
-    }
-    __syncthreads();
-    const float* zg = a.zin + cbase * FIN;
-    const int64_t u_end = b.seg_unit[s + 1];
-    for (int64_t u = b.seg_unit[s] + warp; u < u_end; u += NW) {
-      const int64_t us = b.unit_start[u], ue = b.unit_start[u + 1];
-      int carry_row = -1;
-      float carry[FIN];
-#pragma unroll
-      for (int f = 0; f < FIN; ++f) carry[f] = 0.f;
-      for (int64_t cb = us & ~(int64_t)3; cb < ue; cb += 32 * kV) {
-        const int64_t e0 = cb + (int64_t)kV * lane;
-        int rowl[kV];
-        float p[kV][FIN];
-        {
-          uint32_t ix[kV];
-          float wv[kV];
-#pragma unroll
-          for (int h = 0; h < kV / 4; ++h) {
-            const int64_t e = e0 + 4 * h;
-            int4 iv = make_int4(0, 0, 0, 0);
-            float4 ww = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (e < ue) {
-              iv = ld_stream_v4s32(reinterpret_cast<const int32_t*>(b.idx) + e, pol_s);
-              ww = ld_stream_v4f32(b.w + e, pol_s);
-            }
-            ix[4 * h + 0] = (uint32_t)iv.x; ix[4 * h + 1] = (uint32_t)iv.y;
-            ix[4 * h + 2] = (uint32_t)iv.z; ix[4 * h + 3] = (uint32_t)iv.w;
-            wv[4 * h + 0] = ww.x; wv[4 * h + 1] = ww.y; wv[4 * h + 2] = ww.z; wv[4 * h + 3] = ww.w;
-          }
-#pragma unroll
-          for (int j = 0; j < kV; ++j) {
-            const int64_t e = e0 + j;
-            const bool valid = e >= us && e < ue;
-            rowl[j] = valid ? (int)(ix[j] >> kCbits) : -1;
-            const int cl = (int)(ix[j] & (kC - 1));
-            float zq[FIN];
-#pragma unroll
-            for (int f = 0; f < FIN; ++f) zq[f] = 0.f;
-            if (valid) {
-              if (staged) {
-                const float* zp = zs + cl * FIN;
-                if constexpr (FIN == 4) {
-                  const float4 q = *reinterpret_cast<const float4*>(zp);
-                  zq[0] = q.x; zq[1] = q.y; zq[2] = q.z; zq[3] = q.w;
-                } else if constexpr (FIN == 2) {
-                  const float2 q = *reinterpret_cast<const float2*>(zp);
-                  zq[0] = q.x; zq[1] = q.y;
-                } else {
-                  zq[0] = zp[0];
-                }
-              } else {
-                const VecF<FIN> q = ld_z<FIN>(zg + (int64_t)cl * FIN, pol_z);
-#pragma unroll
-                for (int f = 0; f < FIN; ++f) zq[f] = q.v[f];
-              }
-            }
-#pragma unroll
-            for (int f = 0; f < FIN; ++f) p[j][f] = wv[j] * zq[f];
-          }
-        }
-        // lane-local inclusive segmented scan (rows are sorted inside a unit)
-#pragma unroll
-        for (int j = 1; j < kV; ++j)
-          if (rowl[j] == rowl[j - 1]) add_to<FIN>(p[j], p[j - 1]);
-        const int head = rowl[0], tail = rowl[kV - 1];
-        // the chunk carry flows into lane 0's first run
-        const int c_row = __shfl_sync(0xffffffffu, carry_row, 0);
-        float cin[FIN];
-#pragma unroll
-        for (int f = 0; f < FIN; ++f) cin[f] = 0.f;
-        if (lane == 0 && c_row >= 0 && c_row == head) {
-#pragma unroll
-          for (int f = 0; f < FIN; ++f) cin[f] = carry[f];
-        }
-        if (lane == 0 && c_row >= 0 && c_row != head) {
-          // the carried row ended exactly at the previous chunk boundary
-#pragma unroll
-          for (int f = 0; f < FIN; ++f) accs[c_row * FIN + f] += carry[f];
-        }
-        // segmented scan of lane tails: S_l = tail_l + (continues ? S_{l-1} : 0)
-        const int prev_tail = __shfl_up_sync(0xffffffffu, tail, 1);
-        const bool single = head == tail;
-        int flag = (lane == 0) ? 1 : (single && prev_tail == head && head >= 0 ? 0 : 1);
-        float sv[FIN];
-#pragma unroll
-        for (int f = 0; f < FIN; ++f) sv[f] = p[kV - 1][f] + (single ? cin[f] : 0.f);
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int fu = __shfl_up_sync(0xffffffffu, flag, d);
-          float vu[FIN];
-#pragma unroll
-          for (int f = 0; f < FIN; ++f) vu[f] = __shfl_up_sync(0xffffffffu, sv[f], d);
-          if (lane >= d) {
-            if (!flag) add_to<FIN>(sv, vu);
-            flag |= fu;
-          }
-        }
-        // carry into this lane's first run from the lanes before it
-        float pin[FIN];
-#pragma unroll
-        for (int f = 0; f < FIN; ++f) {
-          const float up = __shfl_up_sync(0xffffffffu, sv[f], 1);
-          pin[f] = (lane > 0 && prev_tail == head && head >= 0) ? up : cin[f];
-        }
-        const int next_head = __shfl_down_sync(0xffffffffu, head, 1);
-        // run ends: write finished rows; lane 31's tail becomes the chunk carry
-#pragma unroll
-        for (int j = 0; j < kV; ++j) {
-          const int r = rowl[j];
-          if (r < 0) continue;
-          const bool last_in_lane = j == kV - 1;
-          const int nxt = last_in_lane ? (lane < 31 ? next_head : INT_MIN) : rowl[j + 1];
-          if (nxt == r) continue;       // the run goes on
-          if (nxt == INT_MIN) continue;  // chunk end: carried below
-          float v[FIN];
-#pragma unroll
-          for (int f = 0; f < FIN; ++f) v[f] = p[j][f] + (r == head ? pin[f] : 0.f);
-#pragma unroll
-          for (int f = 0; f < FIN; ++f) accs[r * FIN + f] += v[f];
-        }
-        // new carry: lane 31's tail run (including everything before it in this row)
-        const int t31 = __shfl_sync(0xffffffffu, tail, 31);
-        float tv[FIN];
-#pragma unroll
-        for (int f = 0; f < FIN; ++f) {
-          const float mine = p[kV - 1][f] + (tail == head ? pin[f] : 0.f);
-          tv[f] = __shfl_sync(0xffffffffu, mine, 31);
-        }
-        carry_row = t31;
-#pragma unroll
-        for (int f = 0; f < FIN; ++f) carry[f] = tv[f];
-      }
-      if (lane == 0 && carry_row >= 0) {
-#pragma unroll
-        for (int f = 0; f < FIN; ++f) accs[carry_row * FIN + f] += carry[f];
-      }
+      for (int i = nv * 4 + tid; i < nf; i += kThreads) zs[i] = zg[i];
+      for (int i = nf + tid; i < (kC + 1) * FIN; i += kThreads) zs[i] = 0.f;  // short last block + padding row
+      __syncthreads();
+      run_slices<FIN, true>(b, s, zs, zg, accs, lane, warp, pol_s, pol_z);
+    } else {
+      run_slices<FIN, false>(b, s, zs, zg, accs, lane, warp, pol_s, pol_z);
     }
   }
   __syncthreads();
@@ -320,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_hop_bmt(HopArgs a, BmtArgs b) {
   }
 }
 
-size_t bmt_smem(int fin) { return (size_t)kC * fin * 4 + (size_t)kR * fin * 4; }
+size_t bmt_smem(int fin) { return (size_t)(kC + 1) * fin * 4 + (size_t)kR * fin * 4; }
 
 template <int FIN, int FOUT>
 void launch_bmt(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles) {
@@ -353,7 +343,24 @@ T fetch(Ctx* ctx, const T* d) {
   return h;
 }
 
-// Build the block-major copy (once per graph; cached on the csr).
+void select_positions(Ctx* ctx, const uint8_t* flags, int64_t n, int64_t* out, int64_t* d_count) {
+  thrust::counting_iterator<int64_t> it(0);
+  size_t bytes = 0;
+  GIFT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, d_count, n, ctx->stream));
+  DevBuf<char> tmp(ctx, bytes);
+  GIFT_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, it, flags, out, d_count, n, ctx->stream));
+  ctx->launches += 2;
+}
+
+void exclusive_sum(Ctx* ctx, const int64_t* in, int64_t* out, int64_t n) {
+  size_t bytes = 0;
+  GIFT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, ctx->stream));
+  DevBuf<char> tmp(ctx, bytes);
+  GIFT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, n, ctx->stream));
+  ctx->launches += 2;
+}
+
+// Build the sliced block-major copy (once per graph; cached on the csr).
 bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   Csr::Bmt& B = c->bmt;
   cudaStream_t st = ctx->stream;
@@ -362,87 +369,118 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   const int64_t nblocks = (n + kC - 1) / kC;
   const int bb = bit_length((uint64_t)(nblocks > 1 ? nblocks - 1 : 1));
   const int key_bits = bb + bit_length((uint64_t)(ntiles > 1 ? ntiles - 1 : 1));
-  if (key_bits > 32 || nnz >= (1LL << 31) * 2) return false;
-  // row of every entry: scatter row ids at row starts, max-scan
-  DevBuf<int32_t> mark(ctx, nnz), row_of(ctx, nnz);
-  GIFT_CUDA(cudaMemsetAsync(mark.p, 0, nnz * sizeof(int32_t), st));
-  k_mark_rows<<<grid_for(n, kBlock), kBlock, 0, st>>>(n, c->indptr, mark.p);
-  GIFT_LAUNCH_CHECK(ctx);
-  size_t bytes = 0;
-  GIFT_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, mark.p, row_of.p, MaxI32(), nnz, st));
-  DevBuf<char> tmp(ctx, bytes);
-  GIFT_CUDA(cub::DeviceScan::InclusiveScan(tmp.p, bytes, mark.p, row_of.p, MaxI32(), nnz, st));
-  ctx->launches += 2;
-  mark.reset();
-  tmp.reset();
-  DevBuf<uint32_t> key(ctx, nnz), key_s(ctx, nnz);
-  DevBuf<uint64_t> pay(ctx, nnz), pay_s(ctx, nnz);
-  k_bmt_keys<<<grid_for(nnz, kBlock), kBlock, 0, st>>>(nnz, row_of.p, c->indices, w32, bb, key.p, pay.p);
-  GIFT_LAUNCH_CHECK(ctx);
-  row_of.reset();
-  GIFT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key_s.p, pay.p, pay_s.p, nnz, 0, key_bits, st));
-  tmp = DevBuf<char>(ctx, bytes);
-  GIFT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key_s.p, pay.p, pay_s.p, nnz, 0, key_bits, st));
-  ctx->launches += 4;
-  tmp.reset();
-  key.reset();
-  pay.reset();
-  // unit granularity: D consecutive rows ~ 256 entries
-  DevBuf<uint8_t> seg_head(ctx, nnz), unit_head(ctx, nnz);
-  DevBuf<unsigned long long> cnt(ctx, 1);
-  GIFT_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st));
-  k_bmt_flags<<<grid_for(nnz, kBlock), kBlock, 0, st>>>(nnz, key_s.p, pay_s.p, 1, seg_head.p, unit_head.p, cnt.p);
-  GIFT_LAUNCH_CHECK(ctx);
-  const unsigned long long row_runs = fetch(ctx, cnt.p);
-  const double per_run = row_runs ? (double)nnz / (double)row_runs : 1.0;
-  int D = (int)(256.0 / per_run + 0.5);
-  D = D < 1 ? 1 : (D > 64 ? 64 : D);
-  if (D > 1) {
-    k_bmt_flags<<<grid_for(nnz, kBlock), kBlock, 0, st>>>(nnz, key_s.p, pay_s.p, D, seg_head.p, unit_head.p,
-                                                          nullptr);
+  if (key_bits > 32 || nnz == 0) return false;
+  // 1. row of every entry (scatter row ids at row starts, max-scan)
+  DevBuf<int32_t> row_of(ctx, nnz);
+  {
+    DevBuf<int32_t> mark(ctx, nnz);
+    GIFT_CUDA(cudaMemsetAsync(mark.p, 0, nnz * sizeof(int32_t), st));
+    k_mark_rows<<<grid_for(n, kBlock), kBlock, 0, st>>>(n, c->indptr, mark.p);
     GIFT_LAUNCH_CHECK(ctx);
+    size_t bytes = 0;
+    GIFT_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, mark.p, row_of.p, MaxI32(), nnz, st));
+    DevBuf<char> tmp(ctx, bytes);
+    GIFT_CUDA(cub::DeviceScan::InclusiveScan(tmp.p, bytes, mark.p, row_of.p, MaxI32(), nnz, st));
+    ctx->launches += 2;
   }
-  // segment starts and unit starts (positions of the flags)
-  const int64_t max_seg = std::min<int64_t>(nnz, ntiles * nblocks) + 1;
-  DevBuf<int64_t> seg_start(ctx, max_seg), nsel(ctx, 2);
-  thrust::counting_iterator<int64_t> it(0);
-  GIFT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, seg_head.p, seg_start.p, nsel.p, nnz, st));
+  // 2. stable sort by (tile, block): segments, CSR (row, column) order inside
+  DevBuf<uint32_t> key_s(ctx, nnz);
+  DevBuf<uint64_t> pay_s(ctx, nnz);
   {
-    DevBuf<char> t2(ctx, bytes);
-    GIFT_CUDA(cub::DeviceSelect::Flagged(t2.p, bytes, it, seg_head.p, seg_start.p, nsel.p, nnz, st));
+    DevBuf<uint32_t> key(ctx, nnz);
+    DevBuf<uint64_t> pay(ctx, nnz);
+    k_bmt_keys<<<grid_for(nnz, kBlock), kBlock, 0, st>>>(nnz, row_of.p, c->indices, w32, bb, key.p, pay.p);
+    GIFT_LAUNCH_CHECK(ctx);
+    row_of.reset();
+    size_t bytes = 0;
+    GIFT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key_s.p, pay.p, pay_s.p, nnz, 0, key_bits, st));
+    DevBuf<char> tmp(ctx, bytes);
+    GIFT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key_s.p, pay.p, pay_s.p, nnz, 0, key_bits, st));
+    ctx->launches += 4;
   }
-  const int64_t nseg = fetch(ctx, nsel.p);
-  if (nseg > (int64_t)seg_start.n) throw_error(GIFT_ERR_INTERNAL, "bmt: segment buffer overflow");
-  // every unit starts at a row run head, so row_runs bounds the unit count
-  B.unit_start = static_cast<int64_t*>(csr_alloc(ctx, c, (row_runs + 2) * sizeof(int64_t)));
-  GIFT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, unit_head.p, B.unit_start, nsel.p + 1, nnz, st));
+  // 3. segment and run heads; segment index of every entry
+  DevBuf<unsigned long long> counts(ctx, 2);
+  DevBuf<int64_t> nsel(ctx, 2);
+  DevBuf<int64_t> seg_start, run_start;
+  int64_t nseg = 0, nruns = 0;
   {
-    DevBuf<char> t2(ctx, bytes);
-    GIFT_CUDA(cub::DeviceSelect::Flagged(t2.p, bytes, it, unit_head.p, B.unit_start, nsel.p + 1, nnz, st));
+    DevBuf<uint8_t> seg_head(ctx, nnz), run_head(ctx, nnz);
+    GIFT_CUDA(cudaMemsetAsync(counts.p, 0, 2 * sizeof(unsigned long long), st));
+    k_bmt_heads<<<grid_for(nnz, kBlock), kBlock, 0, st>>>(nnz, key_s.p, pay_s.p, seg_head.p, run_head.p, counts.p);
+    GIFT_LAUNCH_CHECK(ctx);
+    unsigned long long h[2];
+    GIFT_CUDA(cudaMemcpyAsync(h, counts.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    GIFT_CUDA(cudaStreamSynchronize(st));
+    nseg = (int64_t)h[0];
+    nruns = (int64_t)h[1];
+    seg_start = DevBuf<int64_t>(ctx, nseg + 1);
+    run_start = DevBuf<int64_t>(ctx, nruns + 1);
+    select_positions(ctx, seg_head.p, nnz, seg_start.p, nsel.p);
+    select_positions(ctx, run_head.p, nnz, run_start.p, nsel.p + 1);
   }
-  ctx->launches += 4;
-  const int64_t nunits = fetch(ctx, nsel.p + 1);
-  if (nunits > (int64_t)row_runs) throw_error(GIFT_ERR_INTERNAL, "bmt: unit buffer overflow");
-  GIFT_CUDA(cudaMemcpyAsync(B.unit_start + nunits, &nnz, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  seg_head.reset();
-  unit_head.reset();
+  if (nseg >= (1LL << 40)) return false;
+  // 4. sort runs inside segments: longest first (stable: row order among equal lengths)
+  DevBuf<uint64_t> rkey_s(ctx, nruns);
+  DevBuf<int64_t> run_perm(ctx, nruns);
+  {
+    DevBuf<uint64_t> rkey(ctx, nruns);
+    DevBuf<int64_t> iota(ctx, nruns);
+    k_run_keys<<<grid_for(nruns, kBlock), kBlock, 0, st>>>(nruns, run_start.p, nnz, seg_start.p, nseg, rkey.p);
+    GIFT_LAUNCH_CHECK(ctx);
+    k_iota64<<<grid_for(nruns, kBlock), kBlock, 0, st>>>(nruns, iota.p);
+    GIFT_LAUNCH_CHECK(ctx);
+    const int rbits = 13 + bit_length((uint64_t)nseg);
+    size_t bytes = 0;
+    GIFT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, rkey.p, rkey_s.p, iota.p, run_perm.p, nruns, 0, rbits,
+                                              st));
+    DevBuf<char> tmp(ctx, bytes);
+    GIFT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, rkey.p, rkey_s.p, iota.p, run_perm.p, nruns, 0, rbits,
+                                              st));
+    ctx->launches += 4;
+  }
+  // 5. slices: ceil(runs / 32) per segment; slots from each slice's longest run
+  DevBuf<int64_t> seg_run(ctx, nseg + 1), nsl(ctx, nseg + 1);
+  k_seg_runs<<<grid_for(nruns + 1, kBlock), kBlock, 0, st>>>(nruns, rkey_s.p, nseg, seg_run.p);
+  GIFT_LAUNCH_CHECK(ctx);
+  k_seg_slices<<<grid_for(nseg, kBlock), kBlock, 0, st>>>(nseg, seg_run.p, nsl.p);
+  GIFT_LAUNCH_CHECK(ctx);
+  GIFT_CUDA(cudaMemsetAsync(nsl.p + nseg, 0, sizeof(int64_t), st));
+  B.seg_slice = static_cast<int64_t*>(csr_alloc(ctx, c, (nseg + 1) * sizeof(int64_t)));
+  exclusive_sum(ctx, nsl.p, B.seg_slice, nseg + 1);
+  const int64_t nslices = fetch(ctx, B.seg_slice + nseg);
+  DevBuf<int64_t> slots(ctx, nslices + 1);
+  GIFT_CUDA(cudaMemsetAsync(slots.p + nslices, 0, sizeof(int64_t), st));
+  k_slice_len<<<grid_for(nseg, kBlock), kBlock, 0, st>>>(nseg, seg_run.p, B.seg_slice, rkey_s.p, slots.p);
+  GIFT_LAUNCH_CHECK(ctx);
+  B.slice_off = static_cast<int64_t*>(csr_alloc(ctx, c, (nslices + 1) * sizeof(int64_t)));
+  exclusive_sum(ctx, slots.p, B.slice_off, nslices + 1);
+  const int64_t total = fetch(ctx, B.slice_off + nslices);
+  // 6. scatter entries into slices; padding = column kC (zero signal row), weight 0
+  B.slice_rows = static_cast<uint16_t*>(csr_alloc(ctx, c, (nslices * 32 + 1) * sizeof(uint16_t)));
+  B.col = static_cast<uint16_t*>(csr_alloc(ctx, c, (total + 8) * sizeof(uint16_t)));
+  B.w = static_cast<float*>(csr_alloc(ctx, c, (total + 8) * sizeof(float)));
+  k_fill_u16<<<grid_for(nslices * 32, kBlock), kBlock, 0, st>>>(nslices * 32, 0xffff, B.slice_rows);
+  GIFT_LAUNCH_CHECK(ctx);
+  k_fill_u16<<<grid_for(total, kBlock), kBlock, 0, st>>>(total, (uint16_t)kC, B.col);
+  GIFT_LAUNCH_CHECK(ctx);
+  GIFT_CUDA(cudaMemsetAsync(B.w, 0, total * sizeof(float), st));
+  k_scatter_runs<<<(unsigned)std::min<int64_t>(nseg, 65535), 256, 0, st>>>(
+      nseg, seg_run.p, B.seg_slice, run_perm.p, run_start.p, nruns, nnz, pay_s.p, B.slice_off, B.slice_rows, B.col,
+      B.w);
+  GIFT_LAUNCH_CHECK(ctx);
+  // 7. segment codes and tile -> segment ranges
   B.seg_code = static_cast<int32_t*>(csr_alloc(ctx, c, (nseg + 1) * sizeof(int32_t)));
-  B.seg_unit = static_cast<int64_t*>(csr_alloc(ctx, c, (nseg + 1) * sizeof(int64_t)));
   B.tile_seg = static_cast<int64_t*>(csr_alloc(ctx, c, (ntiles + 1) * sizeof(int64_t)));
   DevBuf<uint32_t> seg_tile(ctx, nseg + 1);
-  k_bmt_segs<<<grid_for(nseg + 1, kBlock), kBlock, 0, st>>>(nseg, seg_start.p, key_s.p, nnz, bb, B.unit_start,
-                                                            nunits, B.seg_code, B.seg_unit, seg_tile.p);
+  k_seg_meta<<<grid_for(nseg, kBlock), kBlock, 0, st>>>(nseg, seg_start.p, key_s.p, nnz, bb, B.seg_code, seg_tile.p);
   GIFT_LAUNCH_CHECK(ctx);
   k_bmt_tile_ptr<<<grid_for(nseg + 1, kBlock), kBlock, 0, st>>>(nseg, seg_tile.p, ntiles, B.tile_seg);
-  GIFT_LAUNCH_CHECK(ctx);
-  B.idx = static_cast<uint32_t*>(csr_alloc(ctx, c, nnz * sizeof(uint32_t)));
-  B.w = static_cast<float*>(csr_alloc(ctx, c, nnz * sizeof(float)));
-  k_bmt_split<<<grid_for(nnz, kBlock), kBlock, 0, st>>>(nnz, pay_s.p, B.idx, B.w);
   GIFT_LAUNCH_CHECK(ctx);
   GIFT_CUDA(cudaStreamSynchronize(st));
   B.ntiles = ntiles;
   B.nseg = nseg;
-  B.nunits = nunits;
+  B.nslices = nslices;
+  B.slots = total;
   return true;
 }
 
@@ -460,7 +498,7 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
     B.ok = bmt_build(ctx, c, csr_w32_public(ctx, c));
   }
   if (!B.ok) return false;
-  BmtArgs b{c->n, B.tile_seg, B.seg_code, B.seg_unit, B.unit_start, B.idx, B.w};
+  BmtArgs b{c->n, B.tile_seg, B.seg_code, B.seg_slice, B.slice_off, B.slice_rows, B.col, B.w};
   switch (fin) {
     case 1: launch_bmt_out<1>(ctx, a, b, B.ntiles, fout); break;
     case 2: launch_bmt_out<2>(ctx, a, b, B.ntiles, fout); break;

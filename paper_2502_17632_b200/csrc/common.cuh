@@ -134,16 +134,17 @@ struct Csr {
   std::map<double, double*> s64;  // sigma -> 1/sqrt(d+sigma)   (fp64, exact)
   std::map<double, float*> s32;   // sigma -> fp32 rounding of s64
   bool sorted_rows = true;        // columns ascending within every row (canonical CSR)
-  // block-major tiled copy of the matrix for the fp32 hop (bmt.cu), lazy
+  // sliced block-major copy of the matrix for the fp32 hop (bmt.cu), lazy
   struct Bmt {
     bool ready = false, ok = false;
-    int64_t ntiles = 0, nseg = 0, nunits = 0;
-    int64_t* tile_seg = nullptr;   // [ntiles + 1]
-    int32_t* seg_code = nullptr;   // [nseg]: staged block id, or -(id + 1) for direct gathers
-    int64_t* seg_unit = nullptr;   // [nseg + 1]
-    int64_t* unit_start = nullptr; // [nunits + 1]
-    uint32_t* idx = nullptr;       // [nnz] (row in tile << 12) | (column in block)
-    float* w = nullptr;            // [nnz]
+    int64_t ntiles = 0, nseg = 0, nslices = 0, slots = 0;
+    int64_t* tile_seg = nullptr;    // [ntiles + 1] segment range of each row tile
+    int32_t* seg_code = nullptr;    // [nseg] staged column block, or -(block + 1): gather from L2
+    int64_t* seg_slice = nullptr;   // [nseg + 1] slice range of each segment
+    int64_t* slice_off = nullptr;   // [nslices + 1] first slot of each slice
+    uint16_t* slice_rows = nullptr; // [nslices * 32] row in tile per lane (0xffff: none)
+    uint16_t* col = nullptr;        // [slots] column in block (kC = padding)
+    float* w = nullptr;             // [slots]
   } bmt;
   std::vector<void*> owned;       // everything above, freed on destroy
 };
