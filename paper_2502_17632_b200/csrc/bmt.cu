@@ -284,8 +284,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_hop_bmt(HopArgs a, BmtArgs b) {
     const bool staged = code >= 0;
     const int64_t cbase = (int64_t)(staged ? code : -code - 1) * kC;
     const float* zg = a.zin + cbase * FIN;
+    // every row has one run per segment, but consecutive segments touch the
+    // same rows: finish the previous segment (accumulators and zs) first
+    __syncthreads();
     if (staged) {
-      __syncthreads();  // previous segment's readers are done with zs
       const int64_t cend = min(cbase + kC, b.ncols);
       const int nf = (int)((cend - cbase) * FIN);
       const int nv = nf / 4;
