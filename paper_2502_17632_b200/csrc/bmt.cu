@@ -49,6 +49,7 @@ constexpr int kC = 1 << kCbits;   // columns per block; column kC = zero padding
 constexpr int kThreads = 512;
 constexpr int kStage = 1024;      // a segment with >= kStage entries stages its block
 constexpr int kBlock = 256;
+constexpr int kWide = 8;          // rows touching more column blocks run on the row kernel
 
 __global__ void k_mark_rows(int64_t n, const int64_t* __restrict__ indptr, int32_t* __restrict__ mark) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
@@ -63,13 +64,35 @@ __global__ void k_iota64(int64_t n, int64_t* __restrict__ p) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = i;
 }
 
-// sort key (tile, block) and payload (weight bits, row in tile, column in block)
+// rows whose entries span more than kWide column blocks (pads / macros wired
+// all over the die): one CTA would walk every block for them, so they stay on
+// the row kernel
+__global__ void k_wide_rows(int64_t n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ col,
+                            uint8_t* __restrict__ wide, unsigned long long* __restrict__ n_wide,
+                            unsigned long long* __restrict__ wide_nnz) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    int nb = 0, prev = -1;
+    for (int64_t k = indptr[r]; k < indptr[r + 1] && nb <= kWide; ++k) {
+      const int b = col[k] >> kCbits;
+      nb += b != prev;
+      prev = b;
+    }
+    wide[r] = nb > kWide;
+    if (nb > kWide) {
+      atomicAdd(n_wide, 1ULL);
+      atomicAdd(wide_nnz, (unsigned long long)(indptr[r + 1] - indptr[r]));
+    }
+  }
+}
+
+// sort key (tile, block) and payload (weight bits, row in tile, column in block);
+// wide rows get the sentinel key and sort past the kept entries
 __global__ void k_bmt_keys(int64_t nnz, const int32_t* __restrict__ row_of, const int32_t* __restrict__ col,
-                           const float* __restrict__ w, int bb, uint32_t* __restrict__ key,
-                           uint64_t* __restrict__ payload) {
+                           const float* __restrict__ w, int bb, const uint8_t* __restrict__ wide, uint32_t sentinel,
+                           uint32_t* __restrict__ key, uint64_t* __restrict__ payload) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t r = (uint32_t)row_of[k], c = (uint32_t)col[k];
-    key[k] = ((r / kR) << bb) | (c >> kCbits);
+    key[k] = wide[r] ? sentinel : (((r / kR) << bb) | (c >> kCbits));
     const uint32_t packed = ((r % kR) << kCbits) | (c & (kC - 1));
     payload[k] = ((uint64_t)__float_as_uint(w[k]) << 32) | packed;
   }
@@ -193,6 +216,7 @@ __global__ void k_bmt_tile_ptr(int64_t nseg, const uint32_t* __restrict__ seg_ti
 
 struct BmtArgs {
   int64_t ncols;
+  const uint8_t* wide;  // rows finished by the row kernel instead
   const int64_t* tile_seg;
   const int32_t* seg_code;
   const int64_t* seg_slice;
@@ -305,6 +329,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_hop_bmt(HopArgs a, BmtArgs b) {
   }
   __syncthreads();
   for (int rr = tid; rr < nrows; rr += kThreads) {
+    if (b.wide[r0 + rr]) continue;
     float acc[FIN];
 #pragma unroll
     for (int f = 0; f < FIN; ++f) acc[f] = accs[rr * FIN + f];
@@ -366,40 +391,70 @@ void exclusive_sum(Ctx* ctx, const int64_t* in, int64_t* out, int64_t n) {
 bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   Csr::Bmt& B = c->bmt;
   cudaStream_t st = ctx->stream;
-  const int64_t n = c->n, nnz = c->nnz;
+  const int64_t n = c->n, nnz_all = c->nnz;
   const int64_t ntiles = (n + kR - 1) / kR;
   const int64_t nblocks = (n + kC - 1) / kC;
   const int bb = bit_length((uint64_t)(nblocks > 1 ? nblocks - 1 : 1));
-  const int key_bits = bb + bit_length((uint64_t)(ntiles > 1 ? ntiles - 1 : 1));
-  if (key_bits > 32 || nnz == 0) return false;
-  // 1. row of every entry (scatter row ids at row starts, max-scan)
-  DevBuf<int32_t> row_of(ctx, nnz);
+  const int key_bits = bb + bit_length((uint64_t)(ntiles > 1 ? ntiles - 1 : 1)) + 1;  // + sentinel bit
+  if (key_bits > 32 || c->nnz == 0) return false;
+  const uint32_t sentinel = 1u << (key_bits - 1);
+  // 0. wide rows -> row kernel
+  B.wide = static_cast<uint8_t*>(csr_alloc(ctx, c, n));
+  int64_t nwide = 0, nnz = c->nnz;
   {
-    DevBuf<int32_t> mark(ctx, nnz);
-    GIFT_CUDA(cudaMemsetAsync(mark.p, 0, nnz * sizeof(int32_t), st));
+    DevBuf<unsigned long long> wc(ctx, 2);
+    GIFT_CUDA(cudaMemsetAsync(wc.p, 0, 2 * sizeof(unsigned long long), st));
+    k_wide_rows<<<grid_for(n, kBlock), kBlock, 0, st>>>(n, c->indptr, c->indices, B.wide, wc.p, wc.p + 1);
+    GIFT_LAUNCH_CHECK(ctx);
+    unsigned long long h[2];
+    GIFT_CUDA(cudaMemcpyAsync(h, wc.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    GIFT_CUDA(cudaStreamSynchronize(st));
+    nwide = (int64_t)h[0];
+    nnz = c->nnz - (int64_t)h[1];  // entries kept in the tiled copy
+    B.wide_rows = static_cast<int32_t*>(csr_alloc(ctx, c, (nwide + 1) * sizeof(int32_t)));
+    if (nwide > 0) {
+      DevBuf<int64_t> nsel1(ctx, 1);
+      thrust::counting_iterator<int32_t> it(0);
+      size_t bytes = 0;
+      GIFT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, B.wide, B.wide_rows, nsel1.p, n, st));
+      DevBuf<char> tmp(ctx, bytes);
+      GIFT_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, it, B.wide, B.wide_rows, nsel1.p, n, st));
+      ctx->launches += 2;
+    }
+  }
+  if (nnz == 0) return false;
+  // 1. row of every entry (scatter row ids at row starts, max-scan)
+  DevBuf<int32_t> row_of(ctx, nnz_all);
+  {
+    DevBuf<int32_t> mark(ctx, nnz_all);
+    GIFT_CUDA(cudaMemsetAsync(mark.p, 0, nnz_all * sizeof(int32_t), st));
     k_mark_rows<<<grid_for(n, kBlock), kBlock, 0, st>>>(n, c->indptr, mark.p);
     GIFT_LAUNCH_CHECK(ctx);
     size_t bytes = 0;
-    GIFT_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, mark.p, row_of.p, MaxI32(), nnz, st));
+    GIFT_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, mark.p, row_of.p, MaxI32(), nnz_all, st));
     DevBuf<char> tmp(ctx, bytes);
-    GIFT_CUDA(cub::DeviceScan::InclusiveScan(tmp.p, bytes, mark.p, row_of.p, MaxI32(), nnz, st));
+    GIFT_CUDA(cub::DeviceScan::InclusiveScan(tmp.p, bytes, mark.p, row_of.p, MaxI32(), nnz_all, st));
     ctx->launches += 2;
   }
   // 2. stable sort by (tile, block): segments, CSR (row, column) order inside
-  DevBuf<uint32_t> key_s(ctx, nnz);
-  DevBuf<uint64_t> pay_s(ctx, nnz);
+  DevBuf<uint32_t> key_s(ctx, nnz_all);
+  DevBuf<uint64_t> pay_s(ctx, nnz_all);
   {
-    DevBuf<uint32_t> key(ctx, nnz);
-    DevBuf<uint64_t> pay(ctx, nnz);
-    k_bmt_keys<<<grid_for(nnz, kBlock), kBlock, 0, st>>>(nnz, row_of.p, c->indices, w32, bb, key.p, pay.p);
+    DevBuf<uint32_t> key(ctx, nnz_all);
+    DevBuf<uint64_t> pay(ctx, nnz_all);
+    k_bmt_keys<<<grid_for(nnz_all, kBlock), kBlock, 0, st>>>(nnz_all, row_of.p, c->indices, w32, bb, B.wide, sentinel,
+                                                             key.p, pay.p);
     GIFT_LAUNCH_CHECK(ctx);
     row_of.reset();
     size_t bytes = 0;
-    GIFT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key_s.p, pay.p, pay_s.p, nnz, 0, key_bits, st));
+    GIFT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key_s.p, pay.p, pay_s.p, nnz_all, 0, key_bits,
+                                              st));
     DevBuf<char> tmp(ctx, bytes);
-    GIFT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key_s.p, pay.p, pay_s.p, nnz, 0, key_bits, st));
+    GIFT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key_s.p, pay.p, pay_s.p, nnz_all, 0, key_bits,
+                                              st));
     ctx->launches += 4;
   }
+  // entries [0, nnz) are the kept ones; wide rows' entries sorted past them
   // 3. segment and run heads; segment index of every entry
   DevBuf<unsigned long long> counts(ctx, 2);
   DevBuf<int64_t> nsel(ctx, 2);
@@ -480,6 +535,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   GIFT_LAUNCH_CHECK(ctx);
   GIFT_CUDA(cudaStreamSynchronize(st));
   B.ntiles = ntiles;
+  B.nwide = nwide;
   B.nseg = nseg;
   B.nslices = nslices;
   B.slots = total;
@@ -489,6 +545,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
 }  // namespace
 
 const float* csr_w32_public(Ctx* ctx, Csr* c);
+void launch_row_list(Ctx* ctx, const HopArgs& base, const int32_t* rows, int64_t nrows, int fin, int fout, int G);
 
 bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
   if (env_int("GIFT_BMT", 1) == 0 || !c->sorted_rows) return false;
@@ -500,12 +557,13 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
     B.ok = bmt_build(ctx, c, csr_w32_public(ctx, c));
   }
   if (!B.ok) return false;
-  BmtArgs b{c->n, B.tile_seg, B.seg_code, B.seg_slice, B.slice_off, B.slice_rows, B.col, B.w};
+  BmtArgs b{c->n, B.wide, B.tile_seg, B.seg_code, B.seg_slice, B.slice_off, B.slice_rows, B.col, B.w};
   switch (fin) {
     case 1: launch_bmt_out<1>(ctx, a, b, B.ntiles, fout); break;
     case 2: launch_bmt_out<2>(ctx, a, b, B.ntiles, fout); break;
     default: launch_bmt_out<4>(ctx, a, b, B.ntiles, fout); break;
   }
+  if (B.nwide > 0) launch_row_list(ctx, a, B.wide_rows, B.nwide, fin, fout, 32);
   return true;
 }
 

@@ -262,8 +262,9 @@ __global__ void k_epilogue_f64(int64_t n, int64_t ncols, const double* __restric
 template <int FIN, int FOUT, int G, int U>
 __global__ void __launch_bounds__(kBlock) k_hop(HopArgs a) {
   const int lane = threadIdx.x & (G - 1);
-  const int64_t row = a.row_begin + (blockIdx.x * (int64_t)kBlock + threadIdx.x) / G;
-  if (row >= a.n) return;  // uniform within a row group
+  const int64_t gi = a.row_begin + (blockIdx.x * (int64_t)kBlock + threadIdx.x) / G;
+  if (gi >= a.n) return;  // uniform within a row group
+  const int64_t row = a.row_list ? (int64_t)a.row_list[gi] : gi;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_z = policy_evict_last();
@@ -392,6 +393,23 @@ void launch_hop_out(Ctx* ctx, const HopArgs& a, int fout, int G) {
     default: launch_hop_g<FIN, 4>(ctx, a, G); break;
   }
 }
+
+}  // namespace
+
+// row kernel over an explicit row list (bmt.cu: the wide rows it leaves out)
+void launch_row_list(Ctx* ctx, const HopArgs& base, const int32_t* rows, int64_t nrows, int fin, int fout, int G) {
+  HopArgs a = base;
+  a.row_list = rows;
+  a.row_begin = 0;
+  a.n = nrows;
+  switch (fin) {
+    case 1: launch_hop_out<1>(ctx, a, fout, G); break;
+    case 2: launch_hop_out<2>(ctx, a, fout, G); break;
+    default: launch_hop_out<4>(ctx, a, fout, G); break;
+  }
+}
+
+namespace {
 
 void launch_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout, int G, bool allow_bmt) {
   ProfScope prof(ctx, fin, a.nch);

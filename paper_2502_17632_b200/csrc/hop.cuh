@@ -43,6 +43,7 @@ struct HopArgs {
   const float* w;
   int64_t n;          // one past the last row processed
   int64_t row_begin;  // first row processed
+  const int32_t* row_list;  // when set: process rows row_list[row_begin .. n) instead of [row_begin, n)
   const float* part_in;  // [rows, FIN] partial sums added before the epilogue (split hop), or null
   float* part_out;       // write the raw row sums here and skip the epilogue (split hop), or null
   const float* zin;  // [n, FIN]
