@@ -58,6 +58,26 @@ def bytes_per_hop(nnz_op: int, n: int) -> int:
     return 8 * nnz_op + 24 * n + 8
 
 
+def ncu_traffic(config: str, fin: int):
+    """DRAM bytes per launch of the hop pass with fin floats per row, from the
+    committed ncu --set full capture of this bench (profiles/r01_traffic_<config>.json),
+    summed over the kernels the pass launches (BMT tile kernel + wide-row kernel)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_traffic_{config}.json")))
+    if not files:
+        return None
+    with open(files[-1]) as f:
+        k = json.load(f)["kernels"]
+    by_fout: dict[str, float] = {}
+    for name, v in k.items():
+        args = name[name.index("<") + 1:name.index(">")].split(",")
+        if int(args[0]) != fin:
+            continue
+        by_fout[args[1].strip()] = by_fout.get(args[1].strip(), 0.0) + v["dram_bytes_per_launch"]
+    return round(sum(by_fout.values()) / len(by_fout)) if by_fout else None
+
+
 def peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -302,7 +322,7 @@ def main() -> None:
         k = kernels[kind]
         ach = k["bytes"] / (k["mean_ms"] / 1e3) / 1e9
         return {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": round(ach / pk["hbm_gbs"], 4), "traffic": None,
+                "frac": round(ach / pk["hbm_gbs"], 4), "traffic": ncu_traffic(args.config, kind) if world == 1 else None,
                 "kernel": f"k_hop<FIN={kind}> ({k['units']} hop unit(s)/launch)",
                 "bytes_per_launch": k["bytes"], "mean_launch_ms": round(k["mean_ms"], 5),
                 "share_of_step": round(k["share"] / total_prof, 4), "peak_source": pk["source"]}
