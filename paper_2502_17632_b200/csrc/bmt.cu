@@ -190,6 +190,72 @@ __global__ void k_scatter_runs(int64_t nseg, const int64_t* __restrict__ seg_run
   }
 }
 
+// Bank-conflict-aware step order.  An LDS.128 of the F=4 hop serves a quarter
+// warp (8 lanes) per shared-memory wavefront when the 8 signal rows sit in
+// distinct 16-byte bank groups, i.e. distinct (column mod 8); random columns
+// average ~2.5 wavefronts per quarter warp.  Each lane may take its run's
+// entries in any FIXED order (the per-row fp32 sum stays deterministic), so
+// per (slice, 8-lane group) a greedy pass reorders the lanes' entries: at every
+// step each lane takes an entry whose residue no earlier lane of the group used
+// at that step, preferring its most plentiful residue.  Thread per group;
+// tmp holds the group's entries bucketed by residue.
+__global__ void k_slice_schedule(int64_t nslices, const int64_t* __restrict__ slice_off, uint16_t* __restrict__ col,
+                                 float* __restrict__ w, uint16_t* __restrict__ tcol, float* __restrict__ tw) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nslices * 4;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sl = g / 4;
+    const int lane0 = (int)(g % 4) * 8;
+    const int64_t off = slice_off[sl];
+    const int64_t L = (slice_off[sl + 1] - off) / 32;  // slots per lane
+    int cnt[8][8];
+    int64_t start[8][8];
+#pragma unroll
+    for (int l = 0; l < 8; ++l)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) cnt[l][r] = 0;
+    for (int l = 0; l < 8; ++l)
+      for (int64_t k = 0; k < L; ++k) {
+        const int64_t slot = off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4);
+        cnt[l][col[slot] & 7]++;
+      }
+    // bucket the lane's entries by residue into tmp (same slot range, lane-major)
+    for (int l = 0; l < 8; ++l) {
+      int64_t base = off + (int64_t)(lane0 + l) * L;
+      int64_t pos[8];
+      for (int r = 0; r < 8; ++r) {
+        start[l][r] = base;
+        pos[r] = base;
+        base += cnt[l][r];
+      }
+      for (int64_t k = 0; k < L; ++k) {
+        const int64_t slot = off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4);
+        const int r = col[slot] & 7;
+        tcol[pos[r]] = col[slot];
+        tw[pos[r]] = w[slot];
+        pos[r]++;
+      }
+    }
+    for (int64_t k = 0; k < L; ++k) {
+      unsigned used = 0;
+      for (int l = 0; l < 8; ++l) {
+        int best = -1, bestc = 0, any = -1, anyc = 0;
+        for (int r = 0; r < 8; ++r) {
+          const int c = cnt[l][r];
+          if (c > anyc) { anyc = c; any = r; }
+          if (!(used & (1u << r)) && c > bestc) { bestc = c; best = r; }
+        }
+        const int r = best >= 0 ? best : any;  // every lane has exactly L entries: any >= 0
+        used |= 1u << r;
+        const int64_t src = start[l][r]++;
+        cnt[l][r]--;
+        const int64_t slot = off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4);
+        col[slot] = tcol[src];
+        w[slot] = tw[src];
+      }
+    }
+  }
+}
+
 __global__ void k_fill_u16(int64_t m, uint16_t v, uint16_t* __restrict__ p) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
@@ -525,6 +591,13 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
       nseg, seg_run.p, B.seg_slice, run_perm.p, run_start.p, nruns, nnz, pay_s.p, B.slice_off, B.slice_rows, B.col,
       B.w);
   GIFT_LAUNCH_CHECK(ctx);
+  if (env_int("GIFT_BMT_SCHEDULE", 1)) {
+    DevBuf<uint16_t> tcol(ctx, total + 8);
+    DevBuf<float> tw(ctx, total + 8);
+    k_slice_schedule<<<grid_for(nslices * 4, 128, 1LL << 30), 128, 0, st>>>(nslices, B.slice_off, B.col, B.w, tcol.p,
+                                                                           tw.p);
+    GIFT_LAUNCH_CHECK(ctx);
+  }
   // 7. segment codes and tile -> segment ranges
   B.seg_code = static_cast<int32_t*>(csr_alloc(ctx, c, (nseg + 1) * sizeof(int32_t)));
   B.tile_seg = static_cast<int64_t*>(csr_alloc(ctx, c, (ntiles + 1) * sizeof(int64_t)));
