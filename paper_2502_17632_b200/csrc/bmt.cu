@@ -190,68 +190,112 @@ __global__ void k_scatter_runs(int64_t nseg, const int64_t* __restrict__ seg_run
   }
 }
 
-// Bank-conflict-aware step order.  An LDS.128 of the F=4 hop serves a quarter
-// warp (8 lanes) per shared-memory wavefront when the 8 signal rows sit in
-// distinct 16-byte bank groups, i.e. distinct (column mod 8); random columns
-// average ~2.5 wavefronts per quarter warp.  Each lane may take its run's
-// entries in any FIXED order (the per-row fp32 sum stays deterministic), so
-// per (slice, 8-lane group) a greedy pass reorders the lanes' entries: at every
-// step each lane takes an entry whose residue no earlier lane of the group used
-// at that step, preferring its most plentiful residue.  Thread per group;
-// tmp holds the group's entries bucketed by residue.
+// Bank-conflict-aware step order.  Shared-memory gathers conflict when lanes
+// of one wavefront hit the same bank group with different addresses:
+//   F = 4 (LDS.128): a wavefront serves 8 lanes  -> want distinct col mod 8
+//                    within each 8-lane quarter warp;
+//   F = 2 (LDS.64):  a wavefront serves 16 lanes -> want distinct col mod 16
+//                    within each 16-lane half warp.
+// Random columns average ~2.5 wavefronts per phase.  A lane may take its run's
+// entries in any FIXED order (the per-row fp32 sum stays deterministic), so per
+// (slice, 16-lane half) a greedy pass reorders the lanes' entries: at every
+// step each lane takes an entry whose residue mod 16 is unused in its half and
+// whose residue mod 8 is unused in its quarter, preferring its most plentiful
+// residue; failing that, one free mod 8 only; failing that, its most plentiful.
+// Thread per half warp; tmp holds the lanes' entries bucketed by residue.
 __global__ void k_slice_schedule(int64_t nslices, const int64_t* __restrict__ slice_off, uint16_t* __restrict__ col,
                                  float* __restrict__ w, uint16_t* __restrict__ tcol, float* __restrict__ tw) {
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nslices * 4;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nslices * 2;
        g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t sl = g / 4;
-    const int lane0 = (int)(g % 4) * 8;
+    const int64_t sl = g / 2;
+    const int lane0 = (int)(g % 2) * 16;
     const int64_t off = slice_off[sl];
     const int64_t L = (slice_off[sl + 1] - off) / 32;  // slots per lane
-    int cnt[8][8];
-    int64_t start[8][8];
-#pragma unroll
-    for (int l = 0; l < 8; ++l)
-#pragma unroll
-      for (int r = 0; r < 8; ++r) cnt[l][r] = 0;
-    for (int l = 0; l < 8; ++l)
-      for (int64_t k = 0; k < L; ++k) {
-        const int64_t slot = off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4);
-        cnt[l][col[slot] & 7]++;
-      }
-    // bucket the lane's entries by residue into tmp (same slot range, lane-major)
-    for (int l = 0; l < 8; ++l) {
+    int cnt[16][16];
+    int64_t next[16][16];
+    for (int l = 0; l < 16; ++l)
+      for (int r = 0; r < 16; ++r) cnt[l][r] = 0;
+    for (int l = 0; l < 16; ++l)
+      for (int64_t k = 0; k < L; ++k) cnt[l][col[off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4)] & 15]++;
+    for (int l = 0; l < 16; ++l) {
       int64_t base = off + (int64_t)(lane0 + l) * L;
-      int64_t pos[8];
-      for (int r = 0; r < 8; ++r) {
-        start[l][r] = base;
+      int64_t pos[16];
+      for (int r = 0; r < 16; ++r) {
+        next[l][r] = base;
         pos[r] = base;
         base += cnt[l][r];
       }
       for (int64_t k = 0; k < L; ++k) {
         const int64_t slot = off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4);
-        const int r = col[slot] & 7;
+        const int r = col[slot] & 15;
         tcol[pos[r]] = col[slot];
         tw[pos[r]] = w[slot];
         pos[r]++;
       }
     }
     for (int64_t k = 0; k < L; ++k) {
-      unsigned used = 0;
-      for (int l = 0; l < 8; ++l) {
-        int best = -1, bestc = 0, any = -1, anyc = 0;
-        for (int r = 0; r < 8; ++r) {
+      unsigned used16 = 0, used8[2] = {0, 0};
+      for (int l = 0; l < 16; ++l) {
+        const int q = l >> 3;
+        int best = -1, bestc = 0, ok8 = -1, ok8c = 0, any = -1, anyc = 0;
+        for (int r = 0; r < 16; ++r) {
           const int c = cnt[l][r];
+          if (c <= 0) continue;
           if (c > anyc) { anyc = c; any = r; }
-          if (!(used & (1u << r)) && c > bestc) { bestc = c; best = r; }
+          if (!(used8[q] & (1u << (r & 7)))) {
+            if (c > ok8c) { ok8c = c; ok8 = r; }
+            if (!(used16 & (1u << r)) && c > bestc) { bestc = c; best = r; }
+          }
         }
-        const int r = best >= 0 ? best : any;  // every lane has exactly L entries: any >= 0
-        used |= 1u << r;
-        const int64_t src = start[l][r]++;
+        const int r = best >= 0 ? best : (ok8 >= 0 ? ok8 : any);  // every lane has L entries: any >= 0
+        used16 |= 1u << r;
+        used8[q] |= 1u << (r & 7);
+        const int64_t src = next[l][r]++;
         cnt[l][r]--;
         const int64_t slot = off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4);
         col[slot] = tcol[src];
         w[slot] = tw[src];
       }
+    }
+  }
+}
+
+// entries of sparse segments (fewer than kStage entries: pad / macro columns)
+__global__ void k_flag_sparse(int64_t nseg, const int64_t* __restrict__ seg_start, int64_t nnz,
+                              uint8_t* __restrict__ sparse, uint8_t* __restrict__ dense) {
+  for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+    const int64_t a = seg_start[sg], b = sg + 1 < nseg ? seg_start[sg + 1] : nnz;
+    const uint8_t sp = (b - a) < kStage;
+    for (int64_t k = a + threadIdx.x; k < b; k += blockDim.x) {
+      sparse[k] = sp;
+      dense[k] = !sp;
+    }
+  }
+}
+
+// residual entry -> (global row key, payload with global column)
+__global__ void k_residual_keys(int64_t m, const uint32_t* __restrict__ key, const uint64_t* __restrict__ pay, int bb,
+                                uint32_t* __restrict__ rkey, uint64_t* __restrict__ rpay) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t kk = key[k];
+    const uint64_t p = pay[k];
+    const uint32_t tile = kk >> bb, blk = kk & ((1u << bb) - 1);
+    const uint32_t rowl = (uint32_t)p >> kCbits, coll = (uint32_t)p & (kC - 1);
+    rkey[k] = tile * kR + rowl;
+    rpay[k] = (p & 0xffffffff00000000ULL) | (uint64_t)(blk * (uint32_t)kC + coll);
+  }
+}
+
+__global__ void k_residual_split(int64_t m, const uint32_t* __restrict__ rkey, const uint64_t* __restrict__ rpay,
+                                 int64_t n, int64_t* __restrict__ rowptr, int32_t* __restrict__ col,
+                                 float* __restrict__ w) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= m; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = k < m ? (int64_t)rkey[k] : n;
+    const int64_t rp = k > 0 ? (int64_t)rkey[k - 1] : -1;
+    for (int64_t t = rp + 1; t <= r; ++t) rowptr[t] = k;
+    if (k < m) {
+      col[k] = (int32_t)(uint32_t)rpay[k];
+      w[k] = __uint_as_float((uint32_t)(rpay[k] >> 32));
     }
   }
 }
@@ -266,7 +310,8 @@ __global__ void k_seg_meta(int64_t nseg, const int64_t* __restrict__ seg_start, 
     const int64_t a = seg_start[s], b = s + 1 < nseg ? seg_start[s + 1] : nnz;
     const uint32_t k = key_s[a];
     const int blk = (int)(k & ((1u << bb) - 1));
-    seg_code[s] = (b - a) >= kStage ? blk : -(blk + 1);
+    seg_code[s] = blk;  // sparse segments were moved to the residual CSR
+    (void)b;
     seg_tile[s] = k >> bb;
   }
 }
@@ -283,6 +328,9 @@ __global__ void k_bmt_tile_ptr(int64_t nseg, const uint32_t* __restrict__ seg_ti
 struct BmtArgs {
   int64_t ncols;
   const uint8_t* wide;  // rows finished by the row kernel instead
+  const int64_t* res_rowptr;  // [n + 1] residual (sparse-block) entries per row
+  const int32_t* res_col;
+  const float* res_w;
   const int64_t* tile_seg;
   const int32_t* seg_code;
   const int64_t* seg_slice;
@@ -324,44 +372,41 @@ __device__ __forceinline__ void gather_fma(float (&acc)[FIN], float w, int c, co
   }
 }
 
-template <int FIN, bool STAGED>
-__device__ __forceinline__ void run_slices(const BmtArgs& b, int64_t s, const float* zs, const float* zg,
-                                           float* accs, int lane, int warp, uint64_t pol_s, uint64_t pol_z) {
-  constexpr int NW = kThreads / 32;
-  const int64_t sl_end = b.seg_slice[s + 1];
-  for (int64_t sl = b.seg_slice[s] + warp; sl < sl_end; sl += NW) {
-    const int64_t off = b.slice_off[sl];
-    const int64_t steps = (b.slice_off[sl + 1] - off) / 128;
-    const int row = b.slice_rows[sl * 32 + lane];
-    float acc[FIN];
+// one slice: lane = one row's run, summed in its (conflict-scheduled) order
+template <int FIN>
+__device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t sl, const float* zs, float* accs, int lane,
+                                          uint64_t pol_s) {
+  const int64_t off = b.slice_off[sl];
+  const int64_t steps = (b.slice_off[sl + 1] - off) / 128;
+  const int row = b.slice_rows[sl * 32 + lane];
+  float acc[FIN];
 #pragma unroll
-    for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
-    const uint16_t* cp = b.col + off + 4 * lane;
-    const float* wp = b.w + off + 4 * lane;
-#pragma unroll 2
-    for (int64_t k = 0; k < steps; ++k) {
-      const uint2 cv = ld_stream_v2u32(cp + k * 128, pol_s);
-      const float4 wv = ld_stream_v4f32(wp + k * 128, pol_s);
-      gather_fma<FIN, STAGED>(acc, wv.x, (int)(cv.x & 0xffff), zs, zg, pol_z);
-      gather_fma<FIN, STAGED>(acc, wv.y, (int)(cv.x >> 16), zs, zg, pol_z);
-      gather_fma<FIN, STAGED>(acc, wv.z, (int)(cv.y & 0xffff), zs, zg, pol_z);
-      gather_fma<FIN, STAGED>(acc, wv.w, (int)(cv.y >> 16), zs, zg, pol_z);
-    }
-    if (row != 0xffff) {
+  for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
+  const uint16_t* cp = b.col + off + 4 * lane;
+  const float* wp = b.w + off + 4 * lane;
+#pragma unroll 4
+  for (int64_t k = 0; k < steps; ++k) {
+    const uint2 cv = ld_stream_v2u32(cp + k * 128, pol_s);
+    const float4 wv = ld_stream_v4f32(wp + k * 128, pol_s);
+    gather_fma<FIN, true>(acc, wv.x, (int)(cv.x & 0xffff), zs, nullptr, 0);
+    gather_fma<FIN, true>(acc, wv.y, (int)(cv.x >> 16), zs, nullptr, 0);
+    gather_fma<FIN, true>(acc, wv.z, (int)(cv.y & 0xffff), zs, nullptr, 0);
+    gather_fma<FIN, true>(acc, wv.w, (int)(cv.y >> 16), zs, nullptr, 0);
+  }
+  if (row != 0xffff) {
 #pragma unroll
-      for (int f = 0; f < FIN; ++f) accs[row * FIN + f] += acc[f];
-    }
+    for (int f = 0; f < FIN; ++f) accs[row * FIN + f] += acc[f];
   }
 }
 
 template <int FIN, int FOUT>
 __global__ void __launch_bounds__(kThreads, 2) k_hop_bmt(HopArgs a, BmtArgs b) {
   extern __shared__ float4 smem_f4[];
+  __shared__ int slice_ctr;
   float* zs = reinterpret_cast<float*>(smem_f4);  // [(kC + 1) * FIN], row kC stays zero
   float* accs = zs + (kC + 1) * FIN;                // [kR * FIN]
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  const int warp = tid >> 5;
   const int64_t tile = blockIdx.x;
   const int64_t r0 = tile * kR;
   const int nrows = (int)min((int64_t)kR, a.n - r0);
@@ -370,27 +415,59 @@ __global__ void __launch_bounds__(kThreads, 2) k_hop_bmt(HopArgs a, BmtArgs b) {
   for (int i = tid; i < nrows * FIN; i += kThreads) accs[i] = 0.f;
   const int64_t s_end = b.tile_seg[tile + 1];
   for (int64_t s = b.tile_seg[tile]; s < s_end; ++s) {
-    const int code = b.seg_code[s];
-    const bool staged = code >= 0;
-    const int64_t cbase = (int64_t)(staged ? code : -code - 1) * kC;
+    const int64_t cbase = (int64_t)b.seg_code[s] * kC;
     const float* zg = a.zin + cbase * FIN;
-    // every row has one run per segment, but consecutive segments touch the
-    // same rows: finish the previous segment (accumulators and zs) first
+    // finish the previous segment: its lanes may still read zs and update the
+    // accumulators of rows this segment touches again
     __syncthreads();
-    if (staged) {
-      const int64_t cend = min(cbase + kC, b.ncols);
-      const int nf = (int)((cend - cbase) * FIN);
-      const int nv = nf / 4;
-      const float4* src = reinterpret_cast<const float4*>(zg);
-      float4* dst = reinterpret_cast<float4*>(zs);
+    const int64_t cend = min(cbase + kC, b.ncols);
+    const int nf = (int)((cend - cbase) * FIN);
+    const int nv = nf / 4;
+    const float4* src = reinterpret_cast<const float4*>(zg);
+    float4* dst = reinterpret_cast<float4*>(zs);
 #pragma unroll 4
-      for (int i = tid; i < nv; i += kThreads) dst[i] = src[i];
-      for (int i = nv * 4 + tid; i < nf; i += kThreads) zs[i] = zg[i];
-      for (int i = nf + tid; i < (kC + 1) * FIN; i += kThreads) zs[i] = 0.f;  // short last block + padding row
-      __syncthreads();
-      run_slices<FIN, true>(b, s, zs, zg, accs, lane, warp, pol_s, pol_z);
-    } else {
-      run_slices<FIN, false>(b, s, zs, zg, accs, lane, warp, pol_s, pol_z);
+    for (int i = tid; i < nv; i += kThreads) dst[i] = src[i];
+    for (int i = nv * 4 + tid; i < nf; i += kThreads) zs[i] = zg[i];
+    for (int i = nf + tid; i < (kC + 1) * FIN; i += kThreads) zs[i] = 0.f;  // short last block + padding row
+    if (tid == 0) slice_ctr = 0;
+    __syncthreads();
+    // slices of a segment touch distinct rows, so the warp that takes a slice
+    // does not change any result: balance them dynamically
+    const int64_t sl0 = b.seg_slice[s];
+    const int nsl = (int)(b.seg_slice[s + 1] - sl0);
+    for (;;) {
+      int j = 0;
+      if (lane == 0) j = atomicAdd(&slice_ctr, 1);
+      j = __shfl_sync(0xffffffffu, j, 0);
+      if (j >= nsl) break;
+      run_slice<FIN>(b, sl0 + j, zs, accs, lane, pol_s);
+    }
+  }
+  __syncthreads();
+  // residual entries (sparse blocks: pad / macro columns), 8 lanes per row, from L2
+  {
+    constexpr int G = 8;
+    const int sub = lane & (G - 1);
+    const unsigned gmask = 0xffu << (lane & ~(G - 1));
+    for (int rr = tid / G; rr < nrows; rr += kThreads / G) {
+      const int64_t beg = b.res_rowptr[r0 + rr], end = b.res_rowptr[r0 + rr + 1];
+      if (beg == end) continue;  // uniform in the group
+      float acc[FIN];
+#pragma unroll
+      for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
+      for (int64_t k = beg + sub; k < end; k += G) {
+        const VecF<FIN> q = ld_z<FIN>(a.zin + (int64_t)b.res_col[k] * FIN, pol_z);
+        const float wk = b.res_w[k];
+#pragma unroll
+        for (int f = 0; f < FIN; ++f) acc[f] = fmaf(wk, q.v[f], acc[f]);
+      }
+#pragma unroll
+      for (int off = G / 2; off > 0; off >>= 1)
+#pragma unroll
+        for (int f = 0; f < FIN; ++f) acc[f] += __shfl_xor_sync(gmask, acc[f], off, G);
+      if (sub == 0)
+#pragma unroll
+        for (int f = 0; f < FIN; ++f) accs[rr * FIN + f] += acc[f];
     }
   }
   __syncthreads();
@@ -521,6 +598,71 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
     ctx->launches += 4;
   }
   // entries [0, nnz) are the kept ones; wide rows' entries sorted past them
+  // 2b. sparse segments -> residual CSR (gathered from L2 by the tile's rows);
+  //     dense segments stay in the sliced copy
+  {
+    DevBuf<uint8_t> seg_head(ctx, nnz), run_head(ctx, nnz);
+    DevBuf<unsigned long long> cnt0(ctx, 2);
+    DevBuf<int64_t> nsel0(ctx, 2);
+    GIFT_CUDA(cudaMemsetAsync(cnt0.p, 0, 2 * sizeof(unsigned long long), st));
+    k_bmt_heads<<<grid_for(nnz, kBlock), kBlock, 0, st>>>(nnz, key_s.p, pay_s.p, seg_head.p, run_head.p, cnt0.p);
+    GIFT_LAUNCH_CHECK(ctx);
+    const int64_t nseg0 = (int64_t)fetch(ctx, cnt0.p);
+    DevBuf<int64_t> seg0(ctx, nseg0 + 1);
+    select_positions(ctx, seg_head.p, nnz, seg0.p, nsel0.p);
+    run_head.reset();
+    DevBuf<uint8_t>& sparse = seg_head;  // reuse
+    DevBuf<uint8_t> dense(ctx, nnz);
+    k_flag_sparse<<<(unsigned)std::min<int64_t>(nseg0, 65535), 256, 0, st>>>(nseg0, seg0.p, nnz, sparse.p, dense.p);
+    GIFT_LAUNCH_CHECK(ctx);
+    // residual entries
+    DevBuf<uint32_t> rk(ctx, nnz);
+    DevBuf<uint64_t> rp(ctx, nnz);
+    size_t bytes = 0;
+    GIFT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, key_s.p, sparse.p, rk.p, nsel0.p, nnz, st));
+    {
+      DevBuf<char> tmp(ctx, bytes);
+      GIFT_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, key_s.p, sparse.p, rk.p, nsel0.p, nnz, st));
+      GIFT_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, pay_s.p, sparse.p, rp.p, nsel0.p + 1, nnz, st));
+    }
+    const int64_t nres = fetch(ctx, nsel0.p);
+    B.res_rowptr = static_cast<int64_t*>(csr_alloc(ctx, c, (n + 1) * sizeof(int64_t)));
+    B.res_col = static_cast<int32_t*>(csr_alloc(ctx, c, (nres + 1) * sizeof(int32_t)));
+    B.res_w = static_cast<float*>(csr_alloc(ctx, c, (nres + 1) * sizeof(float)));
+    if (nres > 0) {
+      DevBuf<uint32_t> rkey(ctx, nres), rkey_s2(ctx, nres);
+      DevBuf<uint64_t> rpay(ctx, nres), rpay_s2(ctx, nres);
+      k_residual_keys<<<grid_for(nres, kBlock), kBlock, 0, st>>>(nres, rk.p, rp.p, bb, rkey.p, rpay.p);
+      GIFT_LAUNCH_CHECK(ctx);
+      const int row_bits = bit_length((uint64_t)(n > 1 ? n - 1 : 1));
+      GIFT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, rkey.p, rkey_s2.p, rpay.p, rpay_s2.p, nres, 0,
+                                                row_bits, st));
+      DevBuf<char> tmp(ctx, bytes);
+      GIFT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, rkey.p, rkey_s2.p, rpay.p, rpay_s2.p, nres, 0,
+                                                row_bits, st));
+      ctx->launches += 4;
+      k_residual_split<<<grid_for(nres + 1, kBlock), kBlock, 0, st>>>(nres, rkey_s2.p, rpay_s2.p, n, B.res_rowptr,
+                                                                      B.res_col, B.res_w);
+      GIFT_LAUNCH_CHECK(ctx);
+    } else {
+      GIFT_CUDA(cudaMemsetAsync(B.res_rowptr, 0, (n + 1) * sizeof(int64_t), st));
+    }
+    B.nres = nres;
+    // compact the dense entries (order preserved)
+    DevBuf<uint32_t> k2(ctx, nnz - nres + 1);
+    DevBuf<uint64_t> p2(ctx, nnz - nres + 1);
+    GIFT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, key_s.p, dense.p, k2.p, nsel0.p, nnz, st));
+    {
+      DevBuf<char> tmp(ctx, bytes);
+      GIFT_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, key_s.p, dense.p, k2.p, nsel0.p, nnz, st));
+      GIFT_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, pay_s.p, dense.p, p2.p, nsel0.p + 1, nnz, st));
+    }
+    ctx->launches += 8;
+    nnz -= nres;
+    key_s = std::move(k2);
+    pay_s = std::move(p2);
+  }
+  if (nnz <= 0) return false;
   // 3. segment and run heads; segment index of every entry
   DevBuf<unsigned long long> counts(ctx, 2);
   DevBuf<int64_t> nsel(ctx, 2);
@@ -594,7 +736,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   if (env_int("GIFT_BMT_SCHEDULE", 1)) {
     DevBuf<uint16_t> tcol(ctx, total + 8);
     DevBuf<float> tw(ctx, total + 8);
-    k_slice_schedule<<<grid_for(nslices * 4, 128, 1LL << 30), 128, 0, st>>>(nslices, B.slice_off, B.col, B.w, tcol.p,
+    k_slice_schedule<<<grid_for(nslices * 2, 128, 1LL << 30), 128, 0, st>>>(nslices, B.slice_off, B.col, B.w, tcol.p,
                                                                            tw.p);
     GIFT_LAUNCH_CHECK(ctx);
   }
@@ -630,7 +772,7 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
     B.ok = bmt_build(ctx, c, csr_w32_public(ctx, c));
   }
   if (!B.ok) return false;
-  BmtArgs b{c->n, B.wide, B.tile_seg, B.seg_code, B.seg_slice, B.slice_off, B.slice_rows, B.col, B.w};
+  BmtArgs b{c->n, B.wide, B.res_rowptr, B.res_col, B.res_w, B.tile_seg, B.seg_code, B.seg_slice, B.slice_off, B.slice_rows, B.col, B.w};
   switch (fin) {
     case 1: launch_bmt_out<1>(ctx, a, b, B.ntiles, fout); break;
     case 2: launch_bmt_out<2>(ctx, a, b, B.ntiles, fout); break;

@@ -140,6 +140,10 @@ struct Csr {
     int64_t ntiles = 0, nseg = 0, nslices = 0, slots = 0, nwide = 0;
     uint8_t* wide = nullptr;        // [n] rows left to the row kernel (span > kWide blocks)
     int32_t* wide_rows = nullptr;   // [nwide]
+    int64_t nres = 0;               // entries in sparse (tile, block) segments
+    int64_t* res_rowptr = nullptr;  // [n + 1] residual CSR of those entries
+    int32_t* res_col = nullptr;
+    float* res_w = nullptr;
     int64_t* tile_seg = nullptr;    // [ntiles + 1] segment range of each row tile
     int32_t* seg_code = nullptr;    // [nseg] staged column block, or -(block + 1): gather from L2
     int64_t* seg_slice = nullptr;   // [nseg + 1] slice range of each segment
