@@ -618,8 +618,10 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
     // residual entries
     DevBuf<uint32_t> rk(ctx, nnz);
     DevBuf<uint64_t> rp(ctx, nnz);
-    size_t bytes = 0;
+    size_t bytes = 0, bytes2 = 0;
     GIFT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, key_s.p, sparse.p, rk.p, nsel0.p, nnz, st));
+    GIFT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes2, pay_s.p, sparse.p, rp.p, nsel0.p + 1, nnz, st));
+    bytes = std::max(bytes, bytes2);
     {
       DevBuf<char> tmp(ctx, bytes);
       GIFT_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, key_s.p, sparse.p, rk.p, nsel0.p, nnz, st));
@@ -652,6 +654,8 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
     DevBuf<uint32_t> k2(ctx, nnz - nres + 1);
     DevBuf<uint64_t> p2(ctx, nnz - nres + 1);
     GIFT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, key_s.p, dense.p, k2.p, nsel0.p, nnz, st));
+    GIFT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes2, pay_s.p, dense.p, p2.p, nsel0.p + 1, nnz, st));
+    bytes = std::max(bytes, bytes2);
     {
       DevBuf<char> tmp(ctx, bytes);
       GIFT_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, key_s.p, dense.p, k2.p, nsel0.p, nnz, st));
