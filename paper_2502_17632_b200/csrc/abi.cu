@@ -162,6 +162,12 @@ int gift_ctx_destroy(gift_ctx* ctx) {
   for (int i = 0; i < 4; ++i)
     if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+    cudaEventDestroy(ctx->fork_ev);
+    cudaEventDestroy(ctx->join_ev);
+  }
   delete ctx;
   GIFT_API_END
 }
@@ -357,8 +363,16 @@ int gift_place_host(gift_ctx* ctx, int64_t n_cells, int64_t n_nets, const int64_
       GIFT_CUDA(cudaMemcpyAsync(dmask.p, h_fixed_mask, n, cudaMemcpyHostToDevice, st));
       GIFT_CUDA(cudaMemcpyAsync(dpos.p, h_fixed_pos, 2 * n * sizeof(double), cudaMemcpyHostToDevice, st));
     }
-    gift::filter(ctx, c, n_terms, h_sigma, h_k, h_alpha, 2, GIFT_DTYPE_F32, dg.p, out_dtype, dout.p,
-                 h_fixed_mask ? dmask.p : nullptr, h_fixed_mask ? dpos.p : nullptr, h_region, precision);
+    const bool bmt = ctx->bmt_enabled;
+    ctx->bmt_enabled = false;  // one-shot graph: the row kernel, no tiled copy
+    try {
+      gift::filter(ctx, c, n_terms, h_sigma, h_k, h_alpha, 2, GIFT_DTYPE_F32, dg.p, out_dtype, dout.p,
+                   h_fixed_mask ? dmask.p : nullptr, h_fixed_mask ? dpos.p : nullptr, h_region, precision);
+    } catch (...) {
+      ctx->bmt_enabled = bmt;
+      throw;
+    }
+    ctx->bmt_enabled = bmt;
     GIFT_CUDA(cudaMemcpyAsync(h_out, dout.p, out_b, cudaMemcpyDeviceToHost, st));
     GIFT_CUDA(cudaStreamSynchronize(st));
     if (nnz_out) *nnz_out = c->nnz;

@@ -768,6 +768,8 @@ void launch_row_list(Ctx* ctx, const HopArgs& base, const int32_t* rows, int64_t
 
 bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
   if (env_int("GIFT_BMT", 1) == 0 || !c->sorted_rows) return false;
+  // building the tiled copy costs ~a few hops; only resident graphs amortise it
+  if (!ctx->bmt_enabled && !c->bmt.ok) return false;
   if (c->n < env_int("GIFT_BMT_MIN_ROWS", 262144) || c->mean_row < env_int("GIFT_BMT_MIN_MEAN", 96)) return false;
   if (a.row_begin != 0 || a.n != c->n || a.part_in || a.part_out) return false;
   Csr::Bmt& B = c->bmt;
@@ -776,13 +778,30 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
     B.ok = bmt_build(ctx, c, csr_w32_public(ctx, c));
   }
   if (!B.ok) return false;
+  // the wide rows (pads / macros, long rows) run concurrently on a side stream:
+  // disjoint output rows, same input signal
+  const bool fork = B.nwide > 0;
+  if (fork) {
+    if (!ctx->side) {
+      GIFT_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+      GIFT_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+      GIFT_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+    }
+    GIFT_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
+    GIFT_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+    cudaStream_t main = ctx->stream;
+    ctx->stream = ctx->side;
+    launch_row_list(ctx, a, B.wide_rows, B.nwide, fin, fout, 32);
+    ctx->stream = main;
+    GIFT_CUDA(cudaEventRecord(ctx->join_ev, ctx->side));
+  }
   BmtArgs b{c->n, B.wide, B.res_rowptr, B.res_col, B.res_w, B.tile_seg, B.seg_code, B.seg_slice, B.slice_off, B.slice_rows, B.col, B.w};
   switch (fin) {
     case 1: launch_bmt_out<1>(ctx, a, b, B.ntiles, fout); break;
     case 2: launch_bmt_out<2>(ctx, a, b, B.ntiles, fout); break;
     default: launch_bmt_out<4>(ctx, a, b, B.ntiles, fout); break;
   }
-  if (B.nwide > 0) launch_row_list(ctx, a, B.wide_rows, B.nwide, fin, fout, 32);
+  if (fork) GIFT_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
   return true;
 }
 

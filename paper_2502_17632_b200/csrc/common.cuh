@@ -45,8 +45,11 @@ void check_cuda(cudaError_t e, const char* what, const char* file, int line);
 struct Ctx {
   int device = 0;
   cudaStream_t stream = 0;
+  cudaStream_t side = nullptr;    // forked work (BMT wide rows), joined back with events
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   int64_t launches = 0;
   int num_sms = 148;
+  bool bmt_enabled = true;        // false: one-shot calls skip building the tiled copy
   // grow-only scratch arenas, reused across calls on this context
   void* scratch[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t scratch_bytes[4] = {0, 0, 0, 0};
