@@ -8,7 +8,8 @@
 // are banded (nets live in +-W index windows): a tile of rows touches only a
 // few column blocks.  BMT stores a reordered copy of the matrix:
 //
-//   row tiles of kR = 2048 rows x column blocks of kC = 4096 columns;
+//   row tiles of kR = 2048 rows (8192 for short-row graphs, see tile_rows_for)
+//   x column blocks of kC = 4096 columns;
 //   a SEGMENT = the entries of one (tile, block) pair; segments tile-major,
 //   blocks ascending;
 //   inside a segment, every row's run of entries goes to one lane of a
@@ -35,6 +36,8 @@
 #include <algorithm>
 #include <climits>
 #include <cstring>
+#include <mutex>
+#include <set>
 
 #include "common.cuh"
 #include "hop.cuh"
@@ -43,10 +46,11 @@ namespace gift {
 
 namespace {
 
-constexpr int kR = 2048;          // rows per tile (11 bits)
+// rows per tile: 2048, or 8192 when rows are short (few entries per
+// (tile, block) segment would make the 64 KB block staging dominate)
+int tile_rows_for(double mean_row) { return mean_row >= 160.0 ? 2048 : 8192; }
 constexpr int kCbits = 12;
 constexpr int kC = 1 << kCbits;   // columns per block; column kC = zero padding row
-constexpr int kThreads = 512;
 constexpr int kStage = 1024;      // a segment with >= kStage entries stages its block
 constexpr int kBlock = 256;
 constexpr int kWide = 8;          // rows touching more column blocks run on the row kernel
@@ -88,7 +92,8 @@ __global__ void k_wide_rows(int64_t n, const int64_t* __restrict__ indptr, const
 // sort key (tile, block) and payload (weight bits, row in tile, column in block);
 // wide rows get the sentinel key and sort past the kept entries
 __global__ void k_bmt_keys(int64_t nnz, const int32_t* __restrict__ row_of, const int32_t* __restrict__ col,
-                           const float* __restrict__ w, int bb, const uint8_t* __restrict__ wide, uint32_t sentinel,
+                           const float* __restrict__ w, int bb, int kR, const uint8_t* __restrict__ wide,
+                           uint32_t sentinel,
                            uint32_t* __restrict__ key, uint64_t* __restrict__ payload) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t r = (uint32_t)row_of[k], c = (uint32_t)col[k];
@@ -275,13 +280,13 @@ __global__ void k_flag_sparse(int64_t nseg, const int64_t* __restrict__ seg_star
 
 // residual entry -> (global row key, payload with global column)
 __global__ void k_residual_keys(int64_t m, const uint32_t* __restrict__ key, const uint64_t* __restrict__ pay, int bb,
-                                uint32_t* __restrict__ rkey, uint64_t* __restrict__ rpay) {
+                                int kR, uint32_t* __restrict__ rkey, uint64_t* __restrict__ rpay) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t kk = key[k];
     const uint64_t p = pay[k];
     const uint32_t tile = kk >> bb, blk = kk & ((1u << bb) - 1);
     const uint32_t rowl = (uint32_t)p >> kCbits, coll = (uint32_t)p & (kC - 1);
-    rkey[k] = tile * kR + rowl;
+    rkey[k] = tile * (uint32_t)kR + rowl;
     rpay[k] = (p & 0xffffffff00000000ULL) | (uint64_t)(blk * (uint32_t)kC + coll);
   }
 }
@@ -327,6 +332,7 @@ __global__ void k_bmt_tile_ptr(int64_t nseg, const uint32_t* __restrict__ seg_ti
 
 struct BmtArgs {
   int64_t ncols;
+  int tile_rows;
   const uint8_t* wide;  // rows finished by the row kernel instead
   const int64_t* res_rowptr;  // [n + 1] residual (sparse-block) entries per row
   const int32_t* res_col;
@@ -399,8 +405,9 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t sl, const fl
   }
 }
 
-template <int FIN, int FOUT>
-__global__ void __launch_bounds__(kThreads, 2) k_hop_bmt(HopArgs a, BmtArgs b) {
+template <int FIN, int FOUT, int kThreads>
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a, BmtArgs b) {
+  const int kR = b.tile_rows;
   extern __shared__ float4 smem_f4[];
   __shared__ int slice_ctr;
   float* zs = reinterpret_cast<float*>(smem_f4);  // [(kC + 1) * FIN], row kC stays zero
@@ -480,18 +487,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_hop_bmt(HopArgs a, BmtArgs b) {
   }
 }
 
-size_t bmt_smem(int fin) { return (size_t)(kC + 1) * fin * 4 + (size_t)kR * fin * 4; }
+size_t bmt_smem(int fin, int kR) { return (size_t)(kC + 1) * fin * 4 + (size_t)kR * fin * 4; }
 
 template <int FIN, int FOUT>
 void launch_bmt(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles) {
-  auto kern = k_hop_bmt<FIN, FOUT>;
-  static bool configured = false;  // one flag per template instance
-  const size_t smem = bmt_smem(FIN);
-  if (!configured) {
-    GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
+  // 2048-row tiles: 2 CTAs x 512 threads per SM; 8192-row tiles: 1 CTA x 1024
+  auto kern = b.tile_rows > 2048 ? k_hop_bmt<FIN, FOUT, 1024> : k_hop_bmt<FIN, FOUT, 512>;
+  const int tpb = b.tile_rows > 2048 ? 1024 : 512;
+  const size_t smem = bmt_smem(FIN, b.tile_rows);
+  static std::mutex mu;
+  static std::set<const void*> configured;  // dynamic smem opt-in once per instance
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (configured.insert((const void*)kern).second)
+      GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   }
-  kern<<<(unsigned)ntiles, kThreads, smem, ctx->stream>>>(a, b);
+  kern<<<(unsigned)ntiles, tpb, smem, ctx->stream>>>(a, b);
   GIFT_LAUNCH_CHECK(ctx);
 }
 
@@ -535,6 +546,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   Csr::Bmt& B = c->bmt;
   cudaStream_t st = ctx->stream;
   const int64_t n = c->n, nnz_all = c->nnz;
+  const int kR = tile_rows_for(c->mean_row);
   const int64_t ntiles = (n + kR - 1) / kR;
   const int64_t nblocks = (n + kC - 1) / kC;
   const int bb = bit_length((uint64_t)(nblocks > 1 ? nblocks - 1 : 1));
@@ -585,7 +597,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   {
     DevBuf<uint32_t> key(ctx, nnz_all);
     DevBuf<uint64_t> pay(ctx, nnz_all);
-    k_bmt_keys<<<grid_for(nnz_all, kBlock), kBlock, 0, st>>>(nnz_all, row_of.p, c->indices, w32, bb, B.wide, sentinel,
+    k_bmt_keys<<<grid_for(nnz_all, kBlock), kBlock, 0, st>>>(nnz_all, row_of.p, c->indices, w32, bb, kR, B.wide, sentinel,
                                                              key.p, pay.p);
     GIFT_LAUNCH_CHECK(ctx);
     row_of.reset();
@@ -634,7 +646,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
     if (nres > 0) {
       DevBuf<uint32_t> rkey(ctx, nres), rkey_s2(ctx, nres);
       DevBuf<uint64_t> rpay(ctx, nres), rpay_s2(ctx, nres);
-      k_residual_keys<<<grid_for(nres, kBlock), kBlock, 0, st>>>(nres, rk.p, rp.p, bb, rkey.p, rpay.p);
+      k_residual_keys<<<grid_for(nres, kBlock), kBlock, 0, st>>>(nres, rk.p, rp.p, bb, kR, rkey.p, rpay.p);
       GIFT_LAUNCH_CHECK(ctx);
       const int row_bits = bit_length((uint64_t)(n > 1 ? n - 1 : 1));
       GIFT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, rkey.p, rkey_s2.p, rpay.p, rpay_s2.p, nres, 0,
@@ -754,6 +766,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   GIFT_LAUNCH_CHECK(ctx);
   GIFT_CUDA(cudaStreamSynchronize(st));
   B.ntiles = ntiles;
+  B.tile_rows = kR;
   B.nwide = nwide;
   B.nseg = nseg;
   B.nslices = nslices;
@@ -795,7 +808,7 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
     ctx->stream = main;
     GIFT_CUDA(cudaEventRecord(ctx->join_ev, ctx->side));
   }
-  BmtArgs b{c->n, B.wide, B.res_rowptr, B.res_col, B.res_w, B.tile_seg, B.seg_code, B.seg_slice, B.slice_off, B.slice_rows, B.col, B.w};
+  BmtArgs b{c->n, B.tile_rows, B.wide, B.res_rowptr, B.res_col, B.res_w, B.tile_seg, B.seg_code, B.seg_slice, B.slice_off, B.slice_rows, B.col, B.w};
   switch (fin) {
     case 1: launch_bmt_out<1>(ctx, a, b, B.ntiles, fout); break;
     case 2: launch_bmt_out<2>(ctx, a, b, B.ntiles, fout); break;
