@@ -53,7 +53,7 @@ constexpr int kCbits = 12;
 constexpr int kC = 1 << kCbits;   // columns per block; column kC = zero padding row
 constexpr int kStage = 1024;      // a segment with >= kStage entries stages its block
 constexpr int kBlock = 256;
-constexpr int kWide = 8;          // rows touching more column blocks run on the row kernel
+constexpr int kWide = 8;          // rows touching > max(kWide, 3 x mean) blocks run on the row kernel
 
 __global__ void k_mark_rows(int64_t n, const int64_t* __restrict__ indptr, int32_t* __restrict__ mark) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
@@ -68,21 +68,33 @@ __global__ void k_iota64(int64_t n, int64_t* __restrict__ p) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = i;
 }
 
-// rows whose entries span more than kWide column blocks (pads / macros wired
-// all over the die): one CTA would walk every block for them, so they stay on
-// the row kernel
-__global__ void k_wide_rows(int64_t n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ col,
-                            uint8_t* __restrict__ wide, unsigned long long* __restrict__ n_wide,
-                            unsigned long long* __restrict__ wide_nnz) {
+// rows whose entries span many more column blocks than a typical row (pads /
+// macros wired all over the die): one CTA would walk every block for them, so
+// they stay on the row kernel.  Pass 1 counts blocks per row, pass 2 flags.
+__global__ void k_row_nblocks(int64_t n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ col,
+                              uint16_t* __restrict__ nb_out, unsigned long long* __restrict__ total) {
+  unsigned long long acc = 0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
     int nb = 0, prev = -1;
-    for (int64_t k = indptr[r]; k < indptr[r + 1] && nb <= kWide; ++k) {
+    for (int64_t k = indptr[r]; k < indptr[r + 1] && nb < 65535; ++k) {
       const int b = col[k] >> kCbits;
       nb += b != prev;
       prev = b;
     }
-    wide[r] = nb > kWide;
-    if (nb > kWide) {
+    nb_out[r] = (uint16_t)nb;
+    acc += nb;
+  }
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) atomicAdd(total, acc);
+}
+
+__global__ void k_wide_rows(int64_t n, const int64_t* __restrict__ indptr, const uint16_t* __restrict__ nb, int limit,
+                            uint8_t* __restrict__ wide, unsigned long long* __restrict__ n_wide,
+                            unsigned long long* __restrict__ wide_nnz) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const bool wd = nb[r] > limit;
+    wide[r] = wd;
+    if (wd) {
       atomicAdd(n_wide, 1ULL);
       atomicAdd(wide_nnz, (unsigned long long)(indptr[r + 1] - indptr[r]));
     }
@@ -557,9 +569,14 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   B.wide = static_cast<uint8_t*>(csr_alloc(ctx, c, n));
   int64_t nwide = 0, nnz = c->nnz;
   {
-    DevBuf<unsigned long long> wc(ctx, 2);
-    GIFT_CUDA(cudaMemsetAsync(wc.p, 0, 2 * sizeof(unsigned long long), st));
-    k_wide_rows<<<grid_for(n, kBlock), kBlock, 0, st>>>(n, c->indptr, c->indices, B.wide, wc.p, wc.p + 1);
+    DevBuf<unsigned long long> wc(ctx, 3);
+    GIFT_CUDA(cudaMemsetAsync(wc.p, 0, 3 * sizeof(unsigned long long), st));
+    DevBuf<uint16_t> nb(ctx, n);
+    k_row_nblocks<<<grid_for(n, kBlock), kBlock, 0, st>>>(n, c->indptr, c->indices, nb.p, wc.p + 2);
+    GIFT_LAUNCH_CHECK(ctx);
+    const double mean_nb = (double)fetch(ctx, wc.p + 2) / (double)(n > 0 ? n : 1);
+    const int limit = std::max(kWide, (int)(3.0 * mean_nb + 0.5));
+    k_wide_rows<<<grid_for(n, kBlock), kBlock, 0, st>>>(n, c->indptr, nb.p, limit, B.wide, wc.p, wc.p + 1);
     GIFT_LAUNCH_CHECK(ctx);
     unsigned long long h[2];
     GIFT_CUDA(cudaMemcpyAsync(h, wc.p, sizeof(h), cudaMemcpyDeviceToHost, st));
