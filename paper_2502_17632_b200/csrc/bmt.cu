@@ -800,7 +800,7 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
   if (env_int("GIFT_BMT", 1) == 0 || !c->sorted_rows) return false;
   // building the tiled copy costs ~a few hops; only resident graphs amortise it
   if (!ctx->bmt_enabled && !c->bmt.ok) return false;
-  if (c->n < env_int("GIFT_BMT_MIN_ROWS", 262144) || c->mean_row < env_int("GIFT_BMT_MIN_MEAN", 96)) return false;
+  if (c->n < env_int("GIFT_BMT_MIN_ROWS", 262144) || c->mean_row < env_int("GIFT_BMT_MIN_MEAN", 32)) return false;
   if (a.row_begin != 0 || a.n != c->n || a.part_in || a.part_out) return false;
   Csr::Bmt& B = c->bmt;
   if (!B.ready) {
