@@ -192,6 +192,21 @@ int gift_pack_fp32(gift_ctx* ctx, int64_t n, int wcols, int nch, const float* co
 int gift_gather_rows_f32(gift_ctx* ctx, int64_t n_idx, int F, const int64_t* d_idx, const float* d_src,
                          float* d_dst);
 
+/* ---- placement metrics: consumers of the filter output --
+ * fp64, fixed reduction trees (deterministic; numpy's pairwise / BLAS order
+ * is not reproduced, agreement ~1e-15 relative). */
+/* quadratic_wirelength(adj, g)  metrics.py:63-74; d_g fp64 [n, 2]. */
+int gift_quadratic_wirelength(gift_ctx* ctx, const gift_csr* adj, const double* d_g, double* h_out);
+/* laplacian(adj) = D - A  graph.py:161-164 (bit-exact: zeros dropped like csr_minus_csr). */
+int gift_laplacian(gift_ctx* ctx, gift_csr* adj, gift_csr** out);
+/* rayleigh_smoothness(lap, col, center)  metrics.py:77-92 -> numerator c^T L c and
+ * denominator c^T c (the caller raises ZeroSignalError on a ~0 denominator). */
+int gift_rayleigh_parts(gift_ctx* ctx, const gift_csr* lap, const double* d_col, int center, double* h_num,
+                        double* h_den);
+/* hpwl(design, g)  metrics.py:95-112; pin offsets nullable (zero). */
+int gift_hpwl(gift_ctx* ctx, int64_t n_nets, const int64_t* d_net_start, const int32_t* d_pin_cell,
+              const double* d_pin_dx, const double* d_pin_dy, const double* d_g, double* h_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -14,6 +14,7 @@ from .errors import (
     IsolatedNodeError,
     NonSymmetricError,
     TooLargeForDenseError,
+    ZeroSignalError,
 )
 from .gift import (
     DEFAULT_TERMS,
@@ -34,6 +35,7 @@ from .graph import (
     from_coo,
     normalized_augmented_adjacency,
 )
+from .metrics import hpwl, laplacian, quadratic_wirelength, rayleigh_smoothness
 from .netlist import Cell, Design, FlatDesign, Net, Pin, Region, Row
 
 __version__ = "0.1.0"
@@ -43,5 +45,6 @@ __all__ = [
     "DimensionMismatchError", "FilterTerm", "FlatDesign", "GiftConfig", "GiftPlaceError", "IsolatedNodeError",
     "Net", "NonSymmetricError", "Pin", "Region", "Row", "SparseSymMatrix", "TooLargeForDenseError",
     "apply_operator_power", "as_device_matrix", "build_clique_graph", "from_coo", "gift_filter", "gift_place",
-    "gift_place_arrays", "initial_signal", "normalized_augmented_adjacency",
+    "gift_place_arrays", "hpwl", "initial_signal", "laplacian", "normalized_augmented_adjacency",
+    "quadratic_wirelength", "rayleigh_smoothness", "ZeroSignalError",
 ]

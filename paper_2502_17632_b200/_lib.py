@@ -77,6 +77,11 @@ SIGNATURES = [
     ("gift_hop_fp32", c_int, [c_vp, c_vp, c_vp]),
     ("gift_pack_fp32", c_int, [c_vp, c_i64, c_int, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_int, c_vp]),
     ("gift_gather_rows_f32", c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp]),
+    # placement metrics (metrics.py)
+    ("gift_quadratic_wirelength", c_int, [c_vp, c_vp, c_vp, c_dp]),
+    ("gift_laplacian", c_int, [c_vp, c_vp, ctypes.POINTER(c_vp)]),
+    ("gift_rayleigh_parts", c_int, [c_vp, c_vp, c_vp, c_int, c_dp, c_dp]),
+    ("gift_hpwl", c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_dp]),
 ]
 
 _lib = None

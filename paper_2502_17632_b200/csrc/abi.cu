@@ -31,6 +31,12 @@ void gather_rows_f32(Ctx* ctx, int64_t n_idx, int F, const int64_t* idx, const f
 Csr* csr_from_arrays(Ctx* ctx, int64_t n_rows, int64_t nnz, const int64_t* d_indptr, const int32_t* d_indices,
                      const double* d_values);
 
+double quadratic_wirelength(Ctx* ctx, const Csr* c, const double* g);
+double hpwl(Ctx* ctx, int64_t n_nets, const int64_t* net_start, const int32_t* pin_cell, const double* pdx,
+            const double* pdy, const double* g);
+void rayleigh_parts(Ctx* ctx, const Csr* lap, const double* col, bool center, double* num, double* den);
+Csr* laplacian(Ctx* ctx, Csr* adj);
+
 static thread_local Error t_err{GIFT_OK, "", -1};
 
 void set_error(int code, const std::string& msg, int64_t arg) { t_err = Error{code, msg, arg}; }
@@ -434,6 +440,40 @@ int gift_gather_rows_f32(gift_ctx* ctx, int64_t n_idx, int F, const int64_t* d_i
   require(ctx, GIFT_ERR_VALUE, "null argument");
   DeviceGuard g(ctx->device);
   gift::gather_rows_f32(ctx, n_idx, F, d_idx, d_src, d_dst);
+  GIFT_API_END
+}
+
+int gift_quadratic_wirelength(gift_ctx* ctx, const gift_csr* adj, const double* d_g, double* h_out) {
+  GIFT_API_BEGIN
+  require(ctx && adj && h_out, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  *h_out = gift::quadratic_wirelength(ctx, adj, d_g);
+  GIFT_API_END
+}
+
+int gift_laplacian(gift_ctx* ctx, gift_csr* adj, gift_csr** out) {
+  GIFT_API_BEGIN
+  require(ctx && adj && out, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  *out = static_cast<gift_csr*>(gift::laplacian(ctx, adj));
+  GIFT_API_END
+}
+
+int gift_rayleigh_parts(gift_ctx* ctx, const gift_csr* lap, const double* d_col, int center, double* h_num,
+                        double* h_den) {
+  GIFT_API_BEGIN
+  require(ctx && lap && h_num && h_den, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  gift::rayleigh_parts(ctx, lap, d_col, center != 0, h_num, h_den);
+  GIFT_API_END
+}
+
+int gift_hpwl(gift_ctx* ctx, int64_t n_nets, const int64_t* d_net_start, const int32_t* d_pin_cell,
+              const double* d_pin_dx, const double* d_pin_dy, const double* d_g, double* h_out) {
+  GIFT_API_BEGIN
+  require(ctx && h_out, GIFT_ERR_VALUE, "null argument");
+  DeviceGuard g(ctx->device);
+  *h_out = gift::hpwl(ctx, n_nets, d_net_start, d_pin_cell, d_pin_dx, d_pin_dy, d_g);
   GIFT_API_END
 }
 

@@ -206,6 +206,25 @@ def main() -> None:
     out["adversary__values"] = up.data.astype(np.float64)
     meta["cases"]["adversary"] = {"n": n, "nnz": int(up.nnz)}
 
+    # ---- metrics consumers (§8(f)): laplacian (exact), S, R, HPWL ----
+    for name in ("kat_brute", "dupnets", "rand_graph1"):
+        if name.startswith("rand"):
+            coo = out[f"{name}__coo"]
+            adj = gp.from_coo(int(out[f"{name}__n"][0]), coo[0].astype(np.int64), coo[1].astype(np.int64), coo[2])
+        else:
+            n_ = int(out[f"{name}__n"][0])
+            adj = gp.build_clique_graph(ref_design(n_, [list(map(int, out[f"{name}__pin_cell"][a:b]))
+                                                        for a, b in zip(out[f"{name}__net_start"][:-1],
+                                                                        out[f"{name}__net_start"][1:])]))
+        lap = gp.laplacian(adj)
+        out[f"{name}__lap__indptr"] = np.asarray(lap.indptr, dtype=np.int64)
+        out[f"{name}__lap__indices"] = np.asarray(lap.indices, dtype=np.int64)
+        out[f"{name}__lap__values"] = np.asarray(lap.values, dtype=np.float64)
+        g = out[f"{name}__g"]
+        out[f"{name}__qwl"] = np.array([gp.quadratic_wirelength(adj, g)])
+        out[f"{name}__rayleigh"] = np.array([gp.rayleigh_smoothness(lap, g[:, 0]),
+                                             gp.rayleigh_smoothness(lap, g[:, 1], center=False)])
+
     # ---- BASELINE config 0 ----
     fd = synth.generate("c0", seed=1)
     d = fd.to_design(gp)
@@ -225,6 +244,11 @@ def main() -> None:
         "g0_sha": h(g0), "filter_g32_sha": h(filt), "place_sha": h(placed),
     }
     meta["cases"]["c0"] = c0
+    out["c0__qwl"] = np.array([gp.quadratic_wirelength(adj, g0), gp.quadratic_wirelength(adj, placed)])
+    out["c0__hpwl"] = np.array([gp.hpwl(d, g0), gp.hpwl(d, placed)])
+    lap0 = gp.laplacian(adj)
+    out["c0__rayleigh"] = np.array([gp.rayleigh_smoothness(lap0, placed[:, 0]),
+                                    gp.rayleigh_smoothness(lap0, placed[:, 1])])
     sample = np.arange(0, adj.n, 97)
     out["c0__sample_rows"] = sample
     out["c0__degrees_sample"] = np.asarray(adj.degrees)[sample]

@@ -424,3 +424,49 @@ def test_bmt_hop_matches_oracle_and_row_kernel(gb, orc, monkeypatch, config, sca
     placed, _ = gb.gift_place(fd, adj, gb.GiftConfig(seed=3, jitter_scale=10.0))
     mask = fd.fixed_mask()
     assert np.array_equal(placed[mask], fd.fixed_positions()[mask])
+
+
+# ----------------------------------------------- §8(f) metrics consumers --
+
+@pytest.mark.parametrize("case", ["kat_brute", "dupnets", "rand_graph1"])
+def test_metrics_match_reference(gb, golden, case):
+    if case.startswith("rand"):
+        coo = golden[f"{case}__coo"]
+        adj = gb.from_coo(int(golden[f"{case}__n"][0]), coo[0].astype(np.int64), coo[1].astype(np.int64), coo[2])
+    else:
+        n, _ = (int(x) for x in golden[f"{case}__n"])
+        adj = gb.build_clique_graph(flat(gb, golden[f"{case}__net_start"], golden[f"{case}__pin_cell"], n))
+    lap = gb.laplacian(adj)
+    csr_equal(lap, golden[f"{case}__lap__indptr"], golden[f"{case}__lap__indices"], golden[f"{case}__lap__values"],
+              f"{case} laplacian")
+    g = golden[f"{case}__g"]
+    assert gb.quadratic_wirelength(adj, g) == pytest.approx(float(golden[f"{case}__qwl"][0]), rel=1e-12)
+    r = golden[f"{case}__rayleigh"]
+    assert gb.rayleigh_smoothness(lap, g[:, 0]) == pytest.approx(float(r[0]), rel=1e-12)
+    assert gb.rayleigh_smoothness(lap, g[:, 1], center=False) == pytest.approx(float(r[1]), rel=1e-12)
+
+
+def test_c0_metrics_and_smoothing(gb, golden):
+    from paper_2502_17632_b200 import synth
+
+    fd = synth.generate("c0", seed=1)
+    adj = gb.build_clique_graph(fd)
+    cfg = gb.GiftConfig(seed=0, jitter_scale=10.0, precision="fp64")
+    g0 = gb.initial_signal(fd, cfg)
+    placed, _ = gb.gift_place(fd, adj, cfg)
+    q = golden["c0__qwl"]
+    h = golden["c0__hpwl"]
+    assert gb.quadratic_wirelength(adj, g0) == pytest.approx(float(q[0]), rel=1e-12)
+    assert gb.quadratic_wirelength(adj, placed) == pytest.approx(float(q[1]), rel=1e-12)
+    assert gb.hpwl(fd, g0) == pytest.approx(float(h[0]), rel=1e-12)
+    assert gb.hpwl(fd.to_design(), placed) == pytest.approx(float(h[1]), rel=1e-12)
+    lap = gb.laplacian(adj)
+    r = golden["c0__rayleigh"]
+    assert gb.rayleigh_smoothness(lap, placed[:, 0]) == pytest.approx(float(r[0]), rel=1e-10)
+    # the filter smooths: S and R drop (acceptance criterion of the reference, test_acceptance.py:241-271)
+    assert gb.quadratic_wirelength(adj, placed) < gb.quadratic_wirelength(adj, g0)
+    assert gb.rayleigh_smoothness(lap, placed[:, 1]) < gb.rayleigh_smoothness(lap, g0[:, 1])
+    with pytest.raises(gb.ZeroSignalError):
+        gb.rayleigh_smoothness(lap, np.full(adj.n, 3.0))
+    with pytest.raises(gb.DimensionMismatchError):
+        gb.quadratic_wirelength(adj, np.zeros((3, 2)))
