@@ -392,11 +392,8 @@ __device__ __forceinline__ void gather_fma(float (&acc)[FIN], float w, int c, co
 
 // one slice: lane = one row's run, summed in its (conflict-scheduled) order
 template <int FIN>
-__device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t sl, const float* zs, float* accs, int lane,
-                                          uint64_t pol_s) {
-  const int64_t off = b.slice_off[sl];
-  const int64_t steps = (b.slice_off[sl + 1] - off) / 128;
-  const int row = b.slice_rows[sl * 32 + lane];
+__device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int64_t steps, int row, const float* zs,
+                                          float* accs, int lane, uint64_t pol_s) {
   float acc[FIN];
 #pragma unroll
   for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
@@ -454,12 +451,35 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a
     // does not change any result: balance them dynamically
     const int64_t sl0 = b.seg_slice[s];
     const int nsl = (int)(b.seg_slice[s + 1] - sl0);
-    for (;;) {
+    // the next slice's index and metadata are fetched before the current one
+    // runs, so their latency hides behind its stream
+    auto grab = [&]() {
       int j = 0;
       if (lane == 0) j = atomicAdd(&slice_ctr, 1);
-      j = __shfl_sync(0xffffffffu, j, 0);
-      if (j >= nsl) break;
-      run_slice<FIN>(b, sl0 + j, zs, accs, lane, pol_s);
+      return __shfl_sync(0xffffffffu, j, 0);
+    };
+    int j = grab();
+    int64_t off = 0, end = 0;
+    int row = 0xffff;
+    if (j < nsl) {
+      off = b.slice_off[sl0 + j];
+      end = b.slice_off[sl0 + j + 1];
+      row = b.slice_rows[(sl0 + j) * 32 + lane];
+    }
+    while (j < nsl) {
+      const int jn = grab();
+      int64_t off_n = 0, end_n = 0;
+      int row_n = 0xffff;
+      if (jn < nsl) {
+        off_n = b.slice_off[sl0 + jn];
+        end_n = b.slice_off[sl0 + jn + 1];
+        row_n = b.slice_rows[(sl0 + jn) * 32 + lane];
+      }
+      run_slice<FIN>(b, off, (end - off) / 128, row, zs, accs, lane, pol_s);
+      j = jn;
+      off = off_n;
+      end = end_n;
+      row = row_n;
     }
   }
   __syncthreads();
