@@ -317,6 +317,20 @@ __global__ void k_residual_split(int64_t m, const uint32_t* __restrict__ rkey, c
   }
 }
 
+// final layout: one 768-byte record per (slice, step of 4): 32 lanes x 4 u16
+// columns, then 32 lanes x 4 f32 weights -- a warp step reads one contiguous
+// record (one DRAM stream per warp instead of two)
+__global__ void k_interleave(int64_t total, const uint16_t* __restrict__ col, const float* __restrict__ w,
+                             uint8_t* __restrict__ data) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = q / 128;
+    const int r = (int)(q % 128);  // lane * 4 + j
+    uint8_t* rec = data + t * 768;
+    reinterpret_cast<uint16_t*>(rec)[r] = col[q];
+    reinterpret_cast<float*>(rec + 256)[r] = w[q];
+  }
+}
+
 __global__ void k_fill_u16(int64_t m, uint16_t v, uint16_t* __restrict__ p) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
@@ -345,6 +359,7 @@ __global__ void k_bmt_tile_ptr(int64_t nseg, const uint32_t* __restrict__ seg_ti
 struct BmtArgs {
   int64_t ncols;
   int tile_rows;
+  const uint8_t* data;  // 768-byte step records (k_interleave)
   const uint8_t* wide;  // rows finished by the row kernel instead
   const int64_t* res_rowptr;  // [n + 1] residual (sparse-block) entries per row
   const int32_t* res_col;
@@ -354,8 +369,6 @@ struct BmtArgs {
   const int64_t* seg_slice;
   const int64_t* slice_off;
   const uint16_t* slice_rows;
-  const uint16_t* col;
-  const float* w;
 };
 
 __device__ __forceinline__ uint2 ld_stream_v2u32(const void* p, uint64_t pol) {
@@ -397,12 +410,13 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int64_t
   float acc[FIN];
 #pragma unroll
   for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
-  const uint16_t* cp = b.col + off + 4 * lane;
-  const float* wp = b.w + off + 4 * lane;
+  const uint8_t* rec = b.data + (off / 128) * 768;
+  const uint8_t* cp = rec + 8 * lane;
+  const uint8_t* wp = rec + 256 + 16 * lane;
 #pragma unroll 4
   for (int64_t k = 0; k < steps; ++k) {
-    const uint2 cv = ld_stream_v2u32(cp + k * 128, pol_s);
-    const float4 wv = ld_stream_v4f32(wp + k * 128, pol_s);
+    const uint2 cv = ld_stream_v2u32(cp + k * 768, pol_s);
+    const float4 wv = ld_stream_v4f32(reinterpret_cast<const float*>(wp + k * 768), pol_s);
     gather_fma<FIN, true>(acc, wv.x, (int)(cv.x & 0xffff), zs, nullptr, 0);
     gather_fma<FIN, true>(acc, wv.y, (int)(cv.x >> 16), zs, nullptr, 0);
     gather_fma<FIN, true>(acc, wv.z, (int)(cv.y & 0xffff), zs, nullptr, 0);
@@ -775,24 +789,31 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   const int64_t total = fetch(ctx, B.slice_off + nslices);
   // 6. scatter entries into slices; padding = column kC (zero signal row), weight 0
   B.slice_rows = static_cast<uint16_t*>(csr_alloc(ctx, c, (nslices * 32 + 1) * sizeof(uint16_t)));
-  B.col = static_cast<uint16_t*>(csr_alloc(ctx, c, (total + 8) * sizeof(uint16_t)));
-  B.w = static_cast<float*>(csr_alloc(ctx, c, (total + 8) * sizeof(float)));
+  DevBuf<uint16_t> colb(ctx, total + 8);
+  DevBuf<float> wb(ctx, total + 8);
+  uint16_t* const bcol = colb.p;
+  float* const bw = wb.p;
   k_fill_u16<<<grid_for(nslices * 32, kBlock), kBlock, 0, st>>>(nslices * 32, 0xffff, B.slice_rows);
   GIFT_LAUNCH_CHECK(ctx);
-  k_fill_u16<<<grid_for(total, kBlock), kBlock, 0, st>>>(total, (uint16_t)kC, B.col);
+  k_fill_u16<<<grid_for(total, kBlock), kBlock, 0, st>>>(total, (uint16_t)kC, bcol);
   GIFT_LAUNCH_CHECK(ctx);
-  GIFT_CUDA(cudaMemsetAsync(B.w, 0, total * sizeof(float), st));
+  GIFT_CUDA(cudaMemsetAsync(bw, 0, total * sizeof(float), st));
   k_scatter_runs<<<(unsigned)std::min<int64_t>(nseg, 65535), 256, 0, st>>>(
-      nseg, seg_run.p, B.seg_slice, run_perm.p, run_start.p, nruns, nnz, pay_s.p, B.slice_off, B.slice_rows, B.col,
-      B.w);
+      nseg, seg_run.p, B.seg_slice, run_perm.p, run_start.p, nruns, nnz, pay_s.p, B.slice_off, B.slice_rows, bcol,
+      bw);
   GIFT_LAUNCH_CHECK(ctx);
   if (env_int("GIFT_BMT_SCHEDULE", 1)) {
     DevBuf<uint16_t> tcol(ctx, total + 8);
     DevBuf<float> tw(ctx, total + 8);
-    k_slice_schedule<<<grid_for(nslices * 2, 128, 1LL << 30), 128, 0, st>>>(nslices, B.slice_off, B.col, B.w, tcol.p,
+    k_slice_schedule<<<grid_for(nslices * 2, 128, 1LL << 30), 128, 0, st>>>(nslices, B.slice_off, bcol, bw, tcol.p,
                                                                            tw.p);
     GIFT_LAUNCH_CHECK(ctx);
   }
+  B.data = static_cast<uint8_t*>(csr_alloc(ctx, c, (total / 128 + 1) * 768));
+  k_interleave<<<grid_for(total, kBlock), kBlock, 0, st>>>(total, bcol, bw, B.data);
+  GIFT_LAUNCH_CHECK(ctx);
+  colb.reset();
+  wb.reset();
   // 7. segment codes and tile -> segment ranges
   B.seg_code = static_cast<int32_t*>(csr_alloc(ctx, c, (nseg + 1) * sizeof(int32_t)));
   B.tile_seg = static_cast<int64_t*>(csr_alloc(ctx, c, (ntiles + 1) * sizeof(int64_t)));
@@ -845,7 +866,7 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
     ctx->stream = main;
     GIFT_CUDA(cudaEventRecord(ctx->join_ev, ctx->side));
   }
-  BmtArgs b{c->n, B.tile_rows, B.wide, B.res_rowptr, B.res_col, B.res_w, B.tile_seg, B.seg_code, B.seg_slice, B.slice_off, B.slice_rows, B.col, B.w};
+  BmtArgs b{c->n, B.tile_rows, B.data, B.wide, B.res_rowptr, B.res_col, B.res_w, B.tile_seg, B.seg_code, B.seg_slice, B.slice_off, B.slice_rows};
   switch (fin) {
     case 1: launch_bmt_out<1>(ctx, a, b, B.ntiles, fout); break;
     case 2: launch_bmt_out<2>(ctx, a, b, B.ntiles, fout); break;

@@ -153,8 +153,8 @@ struct Csr {
     int64_t* seg_slice = nullptr;   // [nseg + 1] slice range of each segment
     int64_t* slice_off = nullptr;   // [nslices + 1] first slot of each slice
     uint16_t* slice_rows = nullptr; // [nslices * 32] row in tile per lane (0xffff: none)
-    uint16_t* col = nullptr;        // [slots] column in block (kC = padding)
-    float* w = nullptr;             // [slots]
+    uint8_t* data = nullptr;        // [slots / 128] 768-byte records: 32x4 u16 columns (kC = padding),
+                                    // then 32x4 f32 weights
   } bmt;
   std::vector<void*> owned;       // everything above, freed on destroy
 };
