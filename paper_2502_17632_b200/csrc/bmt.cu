@@ -50,7 +50,8 @@ namespace {
 // (tile, block) segment would make the 64 KB block staging dominate)
 int tile_rows_for(double mean_row) { return mean_row >= 160.0 ? 2048 : 8192; }
 constexpr int kCbits = 12;
-constexpr int kC = 1 << kCbits;   // columns per block; column kC = zero padding row
+constexpr int kC = 1 << kCbits;   // columns per block; columns kC .. kC+15 = zero padding rows
+constexpr int kPadRows = 16;      // one zero row per bank residue mod 16 (padding never conflicts)
 constexpr int kStage = 1024;      // a segment with >= kStage entries stages its block
 constexpr int kBlock = 256;
 constexpr int kWide = 8;          // rows touching > max(kWide, 3 x mean) blocks run on the row kernel
@@ -228,12 +229,18 @@ __global__ void k_slice_schedule(int64_t nslices, const int64_t* __restrict__ sl
     const int lane0 = (int)(g % 2) * 16;
     const int64_t off = slice_off[sl];
     const int64_t L = (slice_off[sl + 1] - off) / 32;  // slots per lane
-    int cnt[16][16];
+    int cnt[16][16], cnt_real0[16];
     int64_t next[16][16];
-    for (int l = 0; l < 16; ++l)
+    for (int l = 0; l < 16; ++l) {
+      cnt_real0[l] = 0;
       for (int r = 0; r < 16; ++r) cnt[l][r] = 0;
+    }
     for (int l = 0; l < 16; ++l)
-      for (int64_t k = 0; k < L; ++k) cnt[l][col[off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4)] & 15]++;
+      for (int64_t k = 0; k < L; ++k) {
+        const int cv = col[off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4)];
+        cnt[l][cv & 15]++;
+        cnt_real0[l] += ((cv & 15) == 0 && cv < kC);
+      }
     for (int l = 0; l < 16; ++l) {
       int64_t base = off + (int64_t)(lane0 + l) * L;
       int64_t pos[16];
@@ -254,9 +261,13 @@ __global__ void k_slice_schedule(int64_t nslices, const int64_t* __restrict__ sl
       unsigned used16 = 0, used8[2] = {0, 0};
       for (int l = 0; l < 16; ++l) {
         const int q = l >> 3;
+        // padding (column kC, bucket 0, sorted after real residue-0 entries since
+        // kC is the largest value) is a wildcard: it can sit on any zero row
+        // kC + r, so it takes a residue no other lane of its half / quarter uses
+        const int64_t pad_first = next[l][0] + cnt_real0[l];
         int best = -1, bestc = 0, ok8 = -1, ok8c = 0, any = -1, anyc = 0;
         for (int r = 0; r < 16; ++r) {
-          const int c = cnt[l][r];
+          const int c = (r == 0) ? cnt_real0[l] : cnt[l][r];
           if (c <= 0) continue;
           if (c > anyc) { anyc = c; any = r; }
           if (!(used8[q] & (1u << (r & 7)))) {
@@ -264,12 +275,31 @@ __global__ void k_slice_schedule(int64_t nslices, const int64_t* __restrict__ sl
             if (!(used16 & (1u << r)) && c > bestc) { bestc = c; best = r; }
           }
         }
-        const int r = best >= 0 ? best : (ok8 >= 0 ? ok8 : any);  // every lane has L entries: any >= 0
+        const int64_t slot = off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4);
+        const int pads = cnt[l][0] - cnt_real0[l];
+        if (best < 0 && pads > 0) {
+          // no conflict-free real entry: place a padding slot on a free zero row
+          int r = -1;
+          for (int t = 0; t < 16 && r < 0; ++t)
+            if (!(used16 & (1u << t)) && !(used8[q] & (1u << (t & 7)))) r = t;
+          if (r < 0)
+            for (int t = 0; t < 16 && r < 0; ++t)
+              if (!(used8[q] & (1u << (t & 7)))) r = t;
+          if (r < 0) r = 0;
+          used16 |= 1u << r;
+          used8[q] |= 1u << (r & 7);
+          const int64_t src = pad_first + (pads - 1);
+          cnt[l][0]--;
+          col[slot] = (uint16_t)(kC + r);
+          w[slot] = tw[src];
+          continue;
+        }
+        const int r = best >= 0 ? best : (ok8 >= 0 ? ok8 : (any >= 0 ? any : 0));
         used16 |= 1u << r;
         used8[q] |= 1u << (r & 7);
         const int64_t src = next[l][r]++;
         cnt[l][r]--;
-        const int64_t slot = off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4);
+        if (r == 0) cnt_real0[l]--;
         col[slot] = tcol[src];
         w[slot] = tw[src];
       }
@@ -277,49 +307,6 @@ __global__ void k_slice_schedule(int64_t nslices, const int64_t* __restrict__ sl
   }
 }
 
-// entries of sparse segments (fewer than kStage entries: pad / macro columns)
-__global__ void k_flag_sparse(int64_t nseg, const int64_t* __restrict__ seg_start, int64_t nnz,
-                              uint8_t* __restrict__ sparse, uint8_t* __restrict__ dense) {
-  for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
-    const int64_t a = seg_start[sg], b = sg + 1 < nseg ? seg_start[sg + 1] : nnz;
-    const uint8_t sp = (b - a) < kStage;
-    for (int64_t k = a + threadIdx.x; k < b; k += blockDim.x) {
-      sparse[k] = sp;
-      dense[k] = !sp;
-    }
-  }
-}
-
-// residual entry -> (global row key, payload with global column)
-__global__ void k_residual_keys(int64_t m, const uint32_t* __restrict__ key, const uint64_t* __restrict__ pay, int bb,
-                                int kR, uint32_t* __restrict__ rkey, uint64_t* __restrict__ rpay) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t kk = key[k];
-    const uint64_t p = pay[k];
-    const uint32_t tile = kk >> bb, blk = kk & ((1u << bb) - 1);
-    const uint32_t rowl = (uint32_t)p >> kCbits, coll = (uint32_t)p & (kC - 1);
-    rkey[k] = tile * (uint32_t)kR + rowl;
-    rpay[k] = (p & 0xffffffff00000000ULL) | (uint64_t)(blk * (uint32_t)kC + coll);
-  }
-}
-
-__global__ void k_residual_split(int64_t m, const uint32_t* __restrict__ rkey, const uint64_t* __restrict__ rpay,
-                                 int64_t n, int64_t* __restrict__ rowptr, int32_t* __restrict__ col,
-                                 float* __restrict__ w) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= m; k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = k < m ? (int64_t)rkey[k] : n;
-    const int64_t rp = k > 0 ? (int64_t)rkey[k - 1] : -1;
-    for (int64_t t = rp + 1; t <= r; ++t) rowptr[t] = k;
-    if (k < m) {
-      col[k] = (int32_t)(uint32_t)rpay[k];
-      w[k] = __uint_as_float((uint32_t)(rpay[k] >> 32));
-    }
-  }
-}
-
-// final layout: one 768-byte record per (slice, step of 4): 32 lanes x 4 u16
-// columns, then 32 lanes x 4 f32 weights -- a warp step reads one contiguous
-// record (one DRAM stream per warp instead of two)
 __global__ void k_interleave(int64_t total, const uint16_t* __restrict__ col, const float* __restrict__ w,
                              uint8_t* __restrict__ data) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
@@ -383,7 +370,7 @@ template <int FIN, bool STAGED>
 __device__ __forceinline__ void gather_fma(float (&acc)[FIN], float w, int c, const float* zs, const float* zg,
                                            uint64_t pol_z) {
   if constexpr (STAGED) {
-    const float* zp = zs + c * FIN;  // c == kC hits the zero row
+    const float* zp = zs + c * FIN;  // c >= kC hits a zero row
     if constexpr (FIN == 4) {
       const float4 q = *reinterpret_cast<const float4*>(zp);
       acc[0] = fmaf(w, q.x, acc[0]); acc[1] = fmaf(w, q.y, acc[1]);
@@ -433,8 +420,8 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a
   const int kR = b.tile_rows;
   extern __shared__ float4 smem_f4[];
   __shared__ int slice_ctr;
-  float* zs = reinterpret_cast<float*>(smem_f4);  // [(kC + 1) * FIN], row kC stays zero
-  float* accs = zs + (kC + 1) * FIN;                // [kR * FIN]
+  float* zs = reinterpret_cast<float*>(smem_f4);  // [(kC + kPadRows) * FIN], rows >= kC stay zero
+  float* accs = zs + (kC + kPadRows) * FIN;         // [kR * FIN]
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int64_t tile = blockIdx.x;
@@ -458,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a
 #pragma unroll 4
     for (int i = tid; i < nv; i += kThreads) dst[i] = src[i];
     for (int i = nv * 4 + tid; i < nf; i += kThreads) zs[i] = zg[i];
-    for (int i = nf + tid; i < (kC + 1) * FIN; i += kThreads) zs[i] = 0.f;  // short last block + padding row
+    for (int i = nf + tid; i < (kC + kPadRows) * FIN; i += kThreads) zs[i] = 0.f;  // short block + padding rows
     if (tid == 0) slice_ctr = 0;
     __syncthreads();
     // slices of a segment touch distinct rows, so the warp that takes a slice
@@ -533,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a
   }
 }
 
-size_t bmt_smem(int fin, int kR) { return (size_t)(kC + 1) * fin * 4 + (size_t)kR * fin * 4; }
+size_t bmt_smem(int fin, int kR) { return (size_t)(kC + kPadRows) * fin * 4 + (size_t)kR * fin * 4; }
 
 template <int FIN, int FOUT>
 void launch_bmt(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles) {
