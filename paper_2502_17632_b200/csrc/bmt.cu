@@ -307,6 +307,49 @@ __global__ void k_slice_schedule(int64_t nslices, const int64_t* __restrict__ sl
   }
 }
 
+// entries of sparse segments (fewer than kStage entries: pad / macro columns)
+__global__ void k_flag_sparse(int64_t nseg, const int64_t* __restrict__ seg_start, int64_t nnz,
+                              uint8_t* __restrict__ sparse, uint8_t* __restrict__ dense) {
+  for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+    const int64_t a = seg_start[sg], b = sg + 1 < nseg ? seg_start[sg + 1] : nnz;
+    const uint8_t sp = (b - a) < kStage;
+    for (int64_t k = a + threadIdx.x; k < b; k += blockDim.x) {
+      sparse[k] = sp;
+      dense[k] = !sp;
+    }
+  }
+}
+
+// residual entry -> (global row key, payload with global column)
+__global__ void k_residual_keys(int64_t m, const uint32_t* __restrict__ key, const uint64_t* __restrict__ pay, int bb,
+                                int kR, uint32_t* __restrict__ rkey, uint64_t* __restrict__ rpay) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t kk = key[k];
+    const uint64_t p = pay[k];
+    const uint32_t tile = kk >> bb, blk = kk & ((1u << bb) - 1);
+    const uint32_t rowl = (uint32_t)p >> kCbits, coll = (uint32_t)p & (kC - 1);
+    rkey[k] = tile * (uint32_t)kR + rowl;
+    rpay[k] = (p & 0xffffffff00000000ULL) | (uint64_t)(blk * (uint32_t)kC + coll);
+  }
+}
+
+__global__ void k_residual_split(int64_t m, const uint32_t* __restrict__ rkey, const uint64_t* __restrict__ rpay,
+                                 int64_t n, int64_t* __restrict__ rowptr, int32_t* __restrict__ col,
+                                 float* __restrict__ w) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= m; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = k < m ? (int64_t)rkey[k] : n;
+    const int64_t rp = k > 0 ? (int64_t)rkey[k - 1] : -1;
+    for (int64_t t = rp + 1; t <= r; ++t) rowptr[t] = k;
+    if (k < m) {
+      col[k] = (int32_t)(uint32_t)rpay[k];
+      w[k] = __uint_as_float((uint32_t)(rpay[k] >> 32));
+    }
+  }
+}
+
+// final layout: one 768-byte record per (slice, step of 4): 32 lanes x 4 u16
+// columns, then 32 lanes x 4 f32 weights -- a warp step reads one contiguous
+// record (one DRAM stream per warp instead of two)
 __global__ void k_interleave(int64_t total, const uint16_t* __restrict__ col, const float* __restrict__ w,
                              uint8_t* __restrict__ data) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
