@@ -207,6 +207,23 @@ int gift_rayleigh_parts(gift_ctx* ctx, const gift_csr* lap, const double* d_col,
 int gift_hpwl(gift_ctx* ctx, int64_t n_nets, const int64_t* d_net_start, const int32_t* d_pin_cell,
               const double* d_pin_dx, const double* d_pin_dy, const double* d_g, double* h_out);
 
+/* ---- .pl writer: write_placement  netlist.py:503-522 --
+ * Formats the Bookshelf placement text byte-identically to the reference:
+ * "UCLA pl 1.0\n\n", then per cell i in order
+ * "<name>\t<llx>\t<lly>\t: N[ /FIXED]\n" with llx = cx - width/2,
+ * lly = cy - height/2 (fp64) printed like Python's f"{v:.6f}" (correctly
+ * rounded, ties to even, "-0.000000", "nan", "inf").  d_pos: fp64 [n, 2]
+ * centres; d_width/d_height nullable (1.0); d_fixed nullable (no /FIXED).
+ * Names: d_names + d_name_off[n + 1] (concatenated bytes), or, when d_names is
+ * NULL, "<h_name_prefix><i>" (the FlatDesign / benchgen convention "c<i>").
+ * d_out == NULL: only *h_len = exact text size.  Otherwise d_out must hold
+ * cap >= that size; the text is written and *h_len set.  |coordinate| >= 2^107
+ * is rejected (GIFT_ERR_VALUE) instead of printed inexactly. */
+int gift_format_placement(gift_ctx* ctx, int64_t n, const double* d_pos, const double* d_width,
+                          const double* d_height, const uint8_t* d_fixed, const char* d_names,
+                          const int64_t* d_name_off, const char* h_name_prefix, char* d_out, int64_t cap,
+                          int64_t* h_len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -37,11 +37,12 @@ from .graph import (
 )
 from .metrics import hpwl, laplacian, quadratic_wirelength, rayleigh_smoothness
 from .netlist import Cell, Design, FlatDesign, Net, Pin, Region, Row
+from .plio import PL_PRECISION, format_placement, write_placement
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "DEFAULT_TERMS", "DENSE_LIMIT", "JITTER_REGION_FRACTION", "Cell", "Design", "DeviceError",
+    "DEFAULT_TERMS", "DENSE_LIMIT", "PL_PRECISION", "format_placement", "write_placement", "JITTER_REGION_FRACTION", "Cell", "Design", "DeviceError",
     "DimensionMismatchError", "FilterTerm", "FlatDesign", "GiftConfig", "GiftPlaceError", "IsolatedNodeError",
     "Net", "NonSymmetricError", "Pin", "Region", "Row", "SparseSymMatrix", "TooLargeForDenseError",
     "apply_operator_power", "as_device_matrix", "build_clique_graph", "from_coo", "gift_filter", "gift_place",

@@ -82,6 +82,8 @@ SIGNATURES = [
     ("gift_laplacian", c_int, [c_vp, c_vp, ctypes.POINTER(c_vp)]),
     ("gift_rayleigh_parts", c_int, [c_vp, c_vp, c_vp, c_int, c_dp, c_dp]),
     ("gift_hpwl", c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_dp]),
+    ("gift_format_placement", c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_char_p, c_vp,
+                                      c_i64, c_i64p]),
 ]
 
 _lib = None

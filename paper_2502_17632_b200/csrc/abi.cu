@@ -36,6 +36,9 @@ double hpwl(Ctx* ctx, int64_t n_nets, const int64_t* net_start, const int32_t* p
             const double* pdy, const double* g);
 void rayleigh_parts(Ctx* ctx, const Csr* lap, const double* col, bool center, double* num, double* den);
 Csr* laplacian(Ctx* ctx, Csr* adj);
+int64_t format_placement(Ctx* ctx, int64_t n, const double* pos, const double* width, const double* height,
+                         const uint8_t* fixed, const char* names, const int64_t* name_off, const char* prefix,
+                         char* out, int64_t cap);
 
 static thread_local Error t_err{GIFT_OK, "", -1};
 
@@ -168,6 +171,7 @@ int gift_ctx_destroy(gift_ctx* ctx) {
   for (int i = 0; i < 4; ++i)
     if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (auto& kv : ctx->tile_ctr) cudaFree(kv.second);
   if (ctx->side) {
     cudaStreamSynchronize(ctx->side);
     cudaStreamDestroy(ctx->side);
@@ -474,6 +478,19 @@ int gift_hpwl(gift_ctx* ctx, int64_t n_nets, const int64_t* d_net_start, const i
   require(ctx && h_out, GIFT_ERR_VALUE, "null argument");
   DeviceGuard g(ctx->device);
   *h_out = gift::hpwl(ctx, n_nets, d_net_start, d_pin_cell, d_pin_dx, d_pin_dy, d_g);
+  GIFT_API_END
+}
+
+int gift_format_placement(gift_ctx* ctx, int64_t n, const double* d_pos, const double* d_width,
+                          const double* d_height, const uint8_t* d_fixed, const char* d_names,
+                          const int64_t* d_name_off, const char* h_name_prefix, char* d_out, int64_t cap,
+                          int64_t* h_len) {
+  GIFT_API_BEGIN
+  require(ctx && h_len && n >= 0, GIFT_ERR_VALUE, "null argument");
+  require(n == 0 || d_pos, GIFT_ERR_VALUE, "null positions");
+  DeviceGuard g(ctx->device);
+  *h_len = gift::format_placement(ctx, n, d_pos, d_width, d_height, d_fixed, d_names, d_name_off, h_name_prefix,
+                                  d_out, cap);
   GIFT_API_END
 }
 

@@ -36,7 +36,9 @@
 #include <algorithm>
 #include <climits>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <vector>
 #include <set>
 
 #include "common.cuh"
@@ -386,6 +388,21 @@ __global__ void k_bmt_tile_ptr(int64_t nseg, const uint32_t* __restrict__ seg_ti
   }
 }
 
+// estimated cost of a tile for the persistent scheduler: stored slots (6 B
+// each), one staged block per dense segment, residual entries (gathered from
+// L2) and the per-row epilogue
+__global__ void k_tile_cost(int64_t ntiles, int kR, int64_t n, const int64_t* __restrict__ tile_seg,
+                            const int64_t* __restrict__ seg_slice, const int64_t* __restrict__ slice_off,
+                            const int64_t* __restrict__ res_rowptr, int64_t* __restrict__ cost) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s0 = tile_seg[t], s1 = tile_seg[t + 1];
+    const int64_t slots = slice_off[seg_slice[s1]] - slice_off[seg_slice[s0]];
+    const int64_t r0 = t * kR, r1 = min(n, r0 + kR);
+    const int64_t res = res_rowptr[r1] - res_rowptr[r0];
+    cost[t] = 6 * slots + 32768 * (s1 - s0) + 32 * res + 16 * (r1 - r0);
+  }
+}
+
 struct BmtArgs {
   int64_t ncols;
   int tile_rows;
@@ -399,6 +416,9 @@ struct BmtArgs {
   const int64_t* seg_slice;
   const int64_t* slice_off;
   const uint16_t* slice_rows;
+  const int32_t* tile_order;  // persistent mode: tiles by decreasing cost
+  unsigned* ctr;              // persistent mode: [next tile, finished CTAs]; null = one CTA per tile
+  int64_t ntiles;
 };
 
 __device__ __forceinline__ uint2 ld_stream_v2u32(const void* p, uint64_t pol) {
@@ -459,19 +479,14 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int64_t
 }
 
 template <int FIN, int FOUT, int kThreads>
-__global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a, BmtArgs b) {
-  const int kR = b.tile_rows;
+__device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int64_t tile, int kR, int tid, int lane,
+                                         uint64_t pol_s, uint64_t pol_z) {
   extern __shared__ float4 smem_f4[];
   __shared__ int slice_ctr;
   float* zs = reinterpret_cast<float*>(smem_f4);  // [(kC + kPadRows) * FIN], rows >= kC stay zero
   float* accs = zs + (kC + kPadRows) * FIN;         // [kR * FIN]
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int64_t tile = blockIdx.x;
   const int64_t r0 = tile * kR;
   const int nrows = (int)min((int64_t)kR, a.n - r0);
-  const uint64_t pol_s = policy_evict_first();
-  const uint64_t pol_z = policy_evict_last();
   for (int i = tid; i < nrows * FIN; i += kThreads) accs[i] = 0.f;
   const int64_t s_end = b.tile_seg[tile + 1];
   for (int64_t s = b.tile_seg[tile]; s < s_end; ++s) {
@@ -563,6 +578,43 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a
   }
 }
 
+template <int FIN, int FOUT, int kThreads>
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a, BmtArgs b) {
+  const int kR = b.tile_rows;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const uint64_t pol_s = policy_evict_first();
+  const uint64_t pol_z = policy_evict_last();
+  __shared__ int64_t tile_sh;
+  if (!b.ctr) {  // one CTA per tile; the block scheduler issues low blockIdx first
+    const int64_t tile = b.tile_order ? b.tile_order[blockIdx.x] : blockIdx.x;
+    bmt_tile<FIN, FOUT, kThreads>(a, b, tile, kR, tid, lane, pol_s, pol_z);
+    return;
+  }
+  // persistent CTAs take tiles costliest first from a global counter (the
+  // last CTA to finish resets it for the next launch on the stream); tiles
+  // are independent (disjoint output rows), so the assignment never changes
+  // a result
+  for (;;) {
+    if (tid == 0) {
+      const unsigned t = atomicAdd(&b.ctr[0], 1u);
+      tile_sh = t < (unsigned long long)b.ntiles ? b.tile_order[t] : -1;
+    }
+    __syncthreads();  // also: the previous tile's epilogue is done with accs
+    const int64_t tile = tile_sh;
+    __syncthreads();
+    if (tile < 0) break;
+    bmt_tile<FIN, FOUT, kThreads>(a, b, tile, kR, tid, lane, pol_s, pol_z);
+  }
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&b.ctr[1], 1u) == gridDim.x - 1) {
+      b.ctr[0] = 0;
+      b.ctr[1] = 0;
+    }
+  }
+}
+
 size_t bmt_smem(int fin, int kR) { return (size_t)(kC + kPadRows) * fin * 4 + (size_t)kR * fin * 4; }
 
 template <int FIN, int FOUT>
@@ -578,7 +630,24 @@ void launch_bmt(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles) {
     if (configured.insert((const void*)kern).second)
       GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   }
-  kern<<<(unsigned)ntiles, tpb, smem, ctx->stream>>>(a, b);
+  unsigned grid = (unsigned)ntiles;
+  if (b.ctr) {
+    static std::mutex mu2;
+    static std::map<const void*, int> occ;  // resident CTAs per SM, per instance
+    int per_sm = 0;
+    {
+      std::lock_guard<std::mutex> lk(mu2);
+      auto it = occ.find((const void*)kern);
+      if (it == occ.end()) {
+        GIFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tpb, smem));
+        occ[(const void*)kern] = per_sm;
+      } else {
+        per_sm = it->second;
+      }
+    }
+    grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)std::max(per_sm, 1) * ctx->num_sms);
+  }
+  kern<<<grid, tpb, smem, ctx->stream>>>(a, b);
   GIFT_LAUNCH_CHECK(ctx);
 }
 
@@ -852,6 +921,21 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   GIFT_LAUNCH_CHECK(ctx);
   k_bmt_tile_ptr<<<grid_for(nseg + 1, kBlock), kBlock, 0, st>>>(nseg, seg_tile.p, ntiles, B.tile_seg);
   GIFT_LAUNCH_CHECK(ctx);
+  // 8. persistent-scheduler order: costliest tiles first (host sort of ntiles keys)
+  B.tile_order = static_cast<int32_t*>(csr_alloc(ctx, c, (ntiles + 1) * sizeof(int32_t)));
+  {
+    DevBuf<int64_t> cost(ctx, ntiles);
+    k_tile_cost<<<grid_for(ntiles, kBlock), kBlock, 0, st>>>(ntiles, kR, n, B.tile_seg, B.seg_slice, B.slice_off,
+                                                            B.res_rowptr, cost.p);
+    GIFT_LAUNCH_CHECK(ctx);
+    std::vector<int64_t> hc(ntiles);
+    GIFT_CUDA(cudaMemcpyAsync(hc.data(), cost.p, ntiles * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GIFT_CUDA(cudaStreamSynchronize(st));
+    std::vector<int32_t> order(ntiles);
+    for (int64_t t = 0; t < ntiles; ++t) order[t] = (int32_t)t;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return hc[x] > hc[y]; });
+    GIFT_CUDA(cudaMemcpyAsync(B.tile_order, order.data(), ntiles * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  }
   GIFT_CUDA(cudaStreamSynchronize(st));
   B.ntiles = ntiles;
   B.tile_rows = kR;
@@ -896,7 +980,20 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
     ctx->stream = main;
     GIFT_CUDA(cudaEventRecord(ctx->join_ev, ctx->side));
   }
-  BmtArgs b{c->n, B.tile_rows, B.data, B.wide, B.res_rowptr, B.res_col, B.res_w, B.tile_seg, B.seg_code, B.seg_slice, B.slice_off, B.slice_rows};
+  unsigned* ctr = nullptr;
+  const int32_t* order = env_int("GIFT_BMT_LPT", 1) ? B.tile_order : nullptr;
+  if (env_int("GIFT_BMT_PERSIST", 0)) {
+    order = B.tile_order;
+    unsigned*& slot = ctx->tile_ctr[ctx->stream];
+    if (!slot) {
+      GIFT_CUDA(cudaMalloc(&slot, 2 * sizeof(unsigned)));
+      GIFT_CUDA(cudaMemsetAsync(slot, 0, 2 * sizeof(unsigned), ctx->stream));
+    }
+    ctr = slot;
+  }
+  BmtArgs b{c->n,         B.tile_rows,  B.data,      B.wide,      B.res_rowptr, B.res_col,     B.res_w,
+            B.tile_seg,   B.seg_code,   B.seg_slice, B.slice_off, B.slice_rows, order,         ctr,
+            B.ntiles};
   switch (fin) {
     case 1: launch_bmt_out<1>(ctx, a, b, B.ntiles, fout); break;
     case 2: launch_bmt_out<2>(ctx, a, b, B.ntiles, fout); break;

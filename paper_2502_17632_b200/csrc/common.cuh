@@ -50,6 +50,9 @@ struct Ctx {
   int64_t launches = 0;
   int num_sms = 148;
   bool bmt_enabled = true;        // false: one-shot calls skip building the tiled copy
+  // persistent BMT tile scheduler counters [next tile, finished CTAs], one
+  // pair per stream (launches on one stream never overlap; self-resetting)
+  std::map<cudaStream_t, unsigned*> tile_ctr;
   // grow-only scratch arenas, reused across calls on this context
   void* scratch[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t scratch_bytes[4] = {0, 0, 0, 0};
@@ -149,6 +152,7 @@ struct Csr {
     int32_t* res_col = nullptr;
     float* res_w = nullptr;
     int64_t* tile_seg = nullptr;    // [ntiles + 1] segment range of each row tile
+    int32_t* tile_order = nullptr;  // [ntiles] tiles by decreasing estimated cost (persistent CTAs take them in order)
     int32_t* seg_code = nullptr;    // [nseg] staged column block, or -(block + 1): gather from L2
     int64_t* seg_slice = nullptr;   // [nseg + 1] slice range of each segment
     int64_t* slice_off = nullptr;   // [nslices + 1] first slot of each slice

@@ -254,6 +254,42 @@ def main() -> None:
     out["c0__degrees_sample"] = np.asarray(adj.degrees)[sample]
     out["c0__filter_g32_sample"] = filt[sample]
     out["c0__place_sample"] = placed[sample]
+
+    # ---- .pl writer (§8(f) row 4): the reference's write_placement bytes ----
+    import tempfile
+    rng = np.random.default_rng(20261020)
+    edge_cx = [0.5078125, 1e22, -1e-9 + 0.5, 2.5e-6 + 0.5, float("nan"), float("inf"), -float("inf"), 5e-324,
+               123456789.1234565, 1e15 + 0.5, -0.0, 0.5, -2.5, 0.0000005 + 0.5, 1.0000005, 999999.9999995]
+    n_pl = 64
+    cells = []
+    for i in range(n_pl):
+        w = [1.0, 2.0, 3.0, 0.5, 1e-3, 0.0][i % 6]
+        name = ["c%d" % i, "cell_%03d" % i, "u\u00e9%d" % i, "x/y[%d]" % i][i % 4]
+        fixed = i % 5 == 0
+        cells.append(gp.Cell(id=i, name=name, width=w, height=[1.0, 2.0, 0.25][i % 3], fixed=fixed,
+                             fixed_pos=(0.0, 0.0) if fixed else None))
+    pl = rng.normal(0.0, 1e4, size=(n_pl, 2))
+    pl[: len(edge_cx), 0] = edge_cx
+    pl[: len(edge_cx), 1] = edge_cx[::-1]
+    pl[20:30] = np.round(pl[20:30], 7) + 5e-7  # near-ties at the 6th decimal
+    pl[17] = (-0.0, 0.0078125)   # width 0: "-0.000000", an exact tie (to even)
+    pl[35] = (-1e-9, -4e-7)      # negatives that round to "-0.000000"
+    pl[41] = (2.0 ** 100, -(2.0 ** 90) - 0.0)  # wide integer parts (exact %.6f of large binaries)
+    dpl = gp.Design(cells=cells, nets=[], region=gp.Region(0.0, 0.0, 10.0, 10.0))
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "edge.pl")
+        gp.write_placement(dpl, pl, path)
+        text = open(path, "rb").read()
+        out["pl_edge__pos"] = pl
+        out["pl_edge__width"] = np.array([c.width for c in cells])
+        out["pl_edge__height"] = np.array([c.height for c in cells])
+        out["pl_edge__fixed"] = np.array([c.fixed for c in cells], dtype=np.uint8)
+        out["pl_edge__names"] = np.frombuffer("\n".join(c.name for c in cells).encode(), dtype=np.uint8)
+        out["pl_edge__text"] = np.frombuffer(text, dtype=np.uint8)
+        path = os.path.join(td, "c0.pl")
+        gp.write_placement(d, placed, path)
+        text = open(path, "rb").read()
+        meta["cases"]["pl_c0"] = {"bytes": len(text), "sha": hashlib.sha256(text).hexdigest()}
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
     with open(os.path.join(HERE, "golden_meta.json"), "w") as f:
         json.dump(meta, f, indent=1, sort_keys=True)
