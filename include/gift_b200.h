@@ -47,6 +47,7 @@ extern "C" {
 #define GIFT_ERR_CUDA 6
 #define GIFT_ERR_OOM 7
 #define GIFT_ERR_INTERNAL 8
+#define GIFT_ERR_PARSE 9 /* Bookshelf reader: message "<file>\t<lineno>\t<code>\t<value>\t<text>" */
 
 #define GIFT_PREC_FP32 0        /* fused fp32 bank: pre-scaled recurrence, chains fused */
 #define GIFT_PREC_FP64_EXACT 1  /* reference operation order, fp64, bit-exact */
@@ -56,6 +57,7 @@ extern "C" {
 
 typedef struct gift_ctx gift_ctx; /* device + stream + workspace */
 typedef struct gift_csr gift_csr; /* immutable symmetric CSR (SparseSymMatrix, graph.py:48-111) */
+typedef struct gift_bookshelf gift_bookshelf; /* a parsed design (parse_design, netlist.py:418-458) */
 
 /* ---- context --------------------------------------------------------- */
 int gift_ctx_create(int device, gift_ctx** out);
@@ -223,6 +225,36 @@ int gift_format_placement(gift_ctx* ctx, int64_t n, const double* d_pos, const d
                           const double* d_height, const uint8_t* d_fixed, const char* d_names,
                           const int64_t* d_name_off, const char* h_name_prefix, char* d_out, int64_t cap,
                           int64_t* h_len);
+
+/* ---- Bookshelf reader: parse_design  netlist.py:418-458 --
+ * Parses the .nodes, .nets and .pl texts (host bytes, as read from disk; the
+ * .aux manifest and .scl rows are the caller's) on the device with the
+ * reference's semantics: data lines (comments, blanks, "UCLA" headers
+ * skipped; universal newlines), cell ids in .nodes order, NetDegree blocks,
+ * pin offsets after the first ':' token, the last .pl line of a cell wins,
+ * fixed = "terminal" or /FIXED, fixed centre = lower-left + size / 2.
+ * Numbers follow Python float()/int() exactly.  On the first malformed line
+ * (in line order, as the reference raises) the call fails with
+ * GIFT_ERR_PARSE and gift_last_error() = "<file 0/1/2>\t<lineno>\t<code>\t
+ * <value>\t<text>" (codes in paper_2502_17632_b200/bookshelf.py). */
+int gift_bookshelf_parse(gift_ctx* ctx, const char* h_nodes, int64_t nodes_len, const char* h_nets,
+                         int64_t nets_len, const char* h_pl, int64_t pl_len, gift_bookshelf** out);
+/* h_sizes[10] = n_cells, n_nets, n_pins, n_fixed, NumTerminals declared (-1: none),
+ * cell-name bytes, net-name bytes, .pl lines naming undeclared cells, cells with a
+ * .pl line, 0;  h_bbox[4] = lower-left/upper-right of the placed rectangles. */
+int gift_bookshelf_info(const gift_bookshelf* bs, int64_t* h_sizes, double* h_bbox);
+/* Device views (valid until destroy): the pin table feeds gift_build_clique_graph. */
+int gift_bookshelf_device(const gift_bookshelf* bs, const int64_t** d_net_start, const int32_t** d_pin_cell,
+                          const double** d_pin_dx, const double** d_pin_dy, const double** d_width,
+                          const double** d_height, const uint8_t** d_fixed, const double** d_fixed_pos);
+/* Copy out to host arrays (each pointer nullable): net_start [n_nets+1], pin_cell /
+ * pin_dx / pin_dy [n_pins], width / height / fixed [n_cells], fixed_pos [n_cells, 2]
+ * (NaN on movable rows), names as bytes + [count+1] offsets. */
+int gift_bookshelf_copy(gift_ctx* ctx, const gift_bookshelf* bs, int64_t* h_net_start, int32_t* h_pin_cell,
+                        double* h_pin_dx, double* h_pin_dy, double* h_width, double* h_height, uint8_t* h_fixed,
+                        double* h_fixed_pos, char* h_cell_names, int64_t* h_cell_name_off, char* h_net_names,
+                        int64_t* h_net_name_off);
+int gift_bookshelf_destroy(gift_ctx* ctx, gift_bookshelf* bs);
 
 #ifdef __cplusplus
 }

@@ -7,9 +7,14 @@ sm_100a CUDA (libgiftb200.so, C ABI in include/gift_b200.h).  Same names,
 argument meaning and exception classes as `giftplace/__init__.py:26-38`.
 """
 
+from .bookshelf import aux_files, parse_design, read_design
 from .errors import (
+    DanglingPinError,
     DeviceError,
     DimensionMismatchError,
+    DuplicateCellError,
+    MalformedLineError,
+    MissingFileError,
     GiftPlaceError,
     IsolatedNodeError,
     NonSymmetricError,
@@ -42,7 +47,9 @@ from .plio import PL_PRECISION, format_placement, write_placement
 __version__ = "0.1.0"
 
 __all__ = [
-    "DEFAULT_TERMS", "DENSE_LIMIT", "PL_PRECISION", "format_placement", "write_placement", "JITTER_REGION_FRACTION", "Cell", "Design", "DeviceError",
+    "DEFAULT_TERMS", "DENSE_LIMIT", "PL_PRECISION", "format_placement", "write_placement",
+    "DanglingPinError", "DuplicateCellError", "MalformedLineError", "MissingFileError", "aux_files",
+    "parse_design", "read_design", "JITTER_REGION_FRACTION", "Cell", "Design", "DeviceError",
     "DimensionMismatchError", "FilterTerm", "FlatDesign", "GiftConfig", "GiftPlaceError", "IsolatedNodeError",
     "Net", "NonSymmetricError", "Pin", "Region", "Row", "SparseSymMatrix", "TooLargeForDenseError",
     "apply_operator_power", "as_device_matrix", "build_clique_graph", "from_coo", "gift_filter", "gift_place",

@@ -84,6 +84,12 @@ SIGNATURES = [
     ("gift_hpwl", c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_dp]),
     ("gift_format_placement", c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_char_p, c_vp,
                                       c_i64, c_i64p]),
+    ("gift_bookshelf_parse", c_int, [c_vp, ctypes.c_char_p, c_i64, ctypes.c_char_p, c_i64, ctypes.c_char_p, c_i64,
+                                     ctypes.POINTER(c_vp)]),
+    ("gift_bookshelf_info", c_int, [c_vp, c_i64p, c_dp]),
+    ("gift_bookshelf_device", c_int, [c_vp] + [ctypes.POINTER(c_vp)] * 8),
+    ("gift_bookshelf_copy", c_int, [c_vp, c_vp] + [c_vp] * 12),
+    ("gift_bookshelf_destroy", c_int, [c_vp, c_vp]),
 ]
 
 _lib = None

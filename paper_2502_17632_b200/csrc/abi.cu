@@ -36,6 +36,10 @@ double hpwl(Ctx* ctx, int64_t n_nets, const int64_t* net_start, const int32_t* p
             const double* pdy, const double* g);
 void rayleigh_parts(Ctx* ctx, const Csr* lap, const double* col, bool center, double* num, double* den);
 Csr* laplacian(Ctx* ctx, Csr* adj);
+struct Bookshelf;
+Bookshelf* bookshelf_parse(Ctx* ctx, const char* h_nodes, int64_t n_nodes, const char* h_nets, int64_t n_nets,
+                           const char* h_pl, int64_t n_pl);
+void bookshelf_destroy(Ctx* ctx, Bookshelf* B);
 int64_t format_placement(Ctx* ctx, int64_t n, const double* pos, const double* width, const double* height,
                          const uint8_t* fixed, const char* names, const int64_t* name_off, const char* prefix,
                          char* out, int64_t cap);
@@ -491,6 +495,93 @@ int gift_format_placement(gift_ctx* ctx, int64_t n, const double* d_pos, const d
   DeviceGuard g(ctx->device);
   *h_len = gift::format_placement(ctx, n, d_pos, d_width, d_height, d_fixed, d_names, d_name_off, h_name_prefix,
                                   d_out, cap);
+  GIFT_API_END
+}
+
+struct gift_bookshelf {
+  gift::Bookshelf* b;
+};
+
+int gift_bookshelf_parse(gift_ctx* ctx, const char* h_nodes, int64_t nodes_len, const char* h_nets,
+                         int64_t nets_len, const char* h_pl, int64_t pl_len, gift_bookshelf** out) {
+  GIFT_API_BEGIN
+  require(ctx && out, GIFT_ERR_VALUE, "null argument");
+  require(nodes_len >= 0 && nets_len >= 0 && pl_len >= 0, GIFT_ERR_VALUE, "negative length");
+  require((h_nodes || !nodes_len) && (h_nets || !nets_len) && (h_pl || !pl_len), GIFT_ERR_VALUE, "null text");
+  *out = nullptr;
+  DeviceGuard g(ctx->device);
+  gift::Bookshelf* b = gift::bookshelf_parse(ctx, h_nodes, nodes_len, h_nets, nets_len, h_pl, pl_len);
+  *out = new gift_bookshelf{b};
+  GIFT_API_END
+}
+
+int gift_bookshelf_info(const gift_bookshelf* bs, int64_t* h_sizes, double* h_bbox) {
+  GIFT_API_BEGIN
+  require(bs && bs->b, GIFT_ERR_VALUE, "null handle");
+  const gift::Bookshelf& B = *bs->b;
+  if (h_sizes) {
+    const int64_t v[10] = {B.n_cells, B.n_nets, B.n_pins, B.n_fixed, B.n_terminals_decl,
+                           B.cell_name_bytes, B.net_name_bytes, B.pl_unknown, B.n_placed, 0};
+    for (int i = 0; i < 10; ++i) h_sizes[i] = v[i];
+  }
+  if (h_bbox)
+    for (int i = 0; i < 4; ++i) h_bbox[i] = B.bbox[i];
+  GIFT_API_END
+}
+
+int gift_bookshelf_device(const gift_bookshelf* bs, const int64_t** d_net_start, const int32_t** d_pin_cell,
+                          const double** d_pin_dx, const double** d_pin_dy, const double** d_width,
+                          const double** d_height, const uint8_t** d_fixed, const double** d_fixed_pos) {
+  GIFT_API_BEGIN
+  require(bs && bs->b, GIFT_ERR_VALUE, "null handle");
+  const gift::Bookshelf& B = *bs->b;
+  if (d_net_start) *d_net_start = B.net_start;
+  if (d_pin_cell) *d_pin_cell = B.pin_cell;
+  if (d_pin_dx) *d_pin_dx = B.pin_dx;
+  if (d_pin_dy) *d_pin_dy = B.pin_dy;
+  if (d_width) *d_width = B.width;
+  if (d_height) *d_height = B.height;
+  if (d_fixed) *d_fixed = B.fixed;
+  if (d_fixed_pos) *d_fixed_pos = B.fixed_pos;
+  GIFT_API_END
+}
+
+int gift_bookshelf_copy(gift_ctx* ctx, const gift_bookshelf* bs, int64_t* h_net_start, int32_t* h_pin_cell,
+                        double* h_pin_dx, double* h_pin_dy, double* h_width, double* h_height, uint8_t* h_fixed,
+                        double* h_fixed_pos, char* h_cell_names, int64_t* h_cell_name_off, char* h_net_names,
+                        int64_t* h_net_name_off) {
+  GIFT_API_BEGIN
+  require(ctx && bs && bs->b, GIFT_ERR_VALUE, "null handle");
+  DeviceGuard g(ctx->device);
+  const gift::Bookshelf& B = *bs->b;
+  cudaStream_t st = ctx->stream;
+  auto cp = [&](void* dst, const void* src, int64_t bytes) {
+    if (dst && bytes > 0) GIFT_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, st));
+  };
+  cp(h_net_start, B.net_start, (B.n_nets + 1) * 8);
+  cp(h_pin_cell, B.pin_cell, B.n_pins * 4);
+  cp(h_pin_dx, B.pin_dx, B.n_pins * 8);
+  cp(h_pin_dy, B.pin_dy, B.n_pins * 8);
+  cp(h_width, B.width, B.n_cells * 8);
+  cp(h_height, B.height, B.n_cells * 8);
+  cp(h_fixed, B.fixed, B.n_cells);
+  cp(h_fixed_pos, B.fixed_pos, B.n_cells * 16);
+  cp(h_cell_names, B.cell_names, B.cell_name_bytes);
+  cp(h_cell_name_off, B.cell_name_off, (B.n_cells + 1) * 8);
+  cp(h_net_names, B.net_names, B.net_name_bytes);
+  cp(h_net_name_off, B.net_name_off, (B.n_nets + 1) * 8);
+  GIFT_CUDA(cudaStreamSynchronize(st));
+  GIFT_API_END
+}
+
+int gift_bookshelf_destroy(gift_ctx* ctx, gift_bookshelf* bs) {
+  GIFT_API_BEGIN
+  if (!bs) return GIFT_OK;
+  require(ctx, GIFT_ERR_VALUE, "null context");
+  DeviceGuard g(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  gift::bookshelf_destroy(ctx, bs->b);
+  delete bs;
   GIFT_API_END
 }
 

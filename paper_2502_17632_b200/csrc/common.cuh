@@ -163,6 +163,20 @@ struct Csr {
   std::vector<void*> owned;       // everything above, freed on destroy
 };
 
+// a parsed Bookshelf design (bookshelf.cu): device arrays owned by the handle
+struct Bookshelf {
+  int64_t n_cells = 0, n_nets = 0, n_pins = 0, n_terminals_decl = -1, n_fixed = 0;
+  int64_t cell_name_bytes = 0, net_name_bytes = 0, pl_unknown = 0, n_placed = 0;
+  double bbox[4] = {0, 0, 0, 0};
+  std::vector<void*> owned;
+  int64_t* net_start = nullptr;
+  int32_t* pin_cell = nullptr;
+  double *pin_dx = nullptr, *pin_dy = nullptr, *width = nullptr, *height = nullptr, *fixed_pos = nullptr;
+  uint8_t* fixed = nullptr;
+  char *cell_names = nullptr, *net_names = nullptr;
+  int64_t *cell_name_off = nullptr, *net_name_off = nullptr;
+};
+
 void* csr_alloc(Ctx* ctx, Csr* c, size_t bytes);
 void csr_destroy(Csr* c);
 

@@ -180,7 +180,8 @@ class FlatDesign:
     """
 
     def __init__(self, net_start, pin_cell, fixed_mask, fixed_pos, region: Region,
-                 widths=None, heights=None, meta: dict | None = None) -> None:
+                 widths=None, heights=None, meta: dict | None = None, pin_dx=None, pin_dy=None,
+                 cell_names=None, net_names=None) -> None:
         self.net_start = np.ascontiguousarray(net_start, dtype=np.int64)
         self.pin_cell = np.ascontiguousarray(pin_cell)
         self._mask = np.ascontiguousarray(fixed_mask, dtype=bool)
@@ -190,6 +191,12 @@ class FlatDesign:
         self.widths = np.ones(n) if widths is None else np.asarray(widths, dtype=float)
         self.heights = np.ones(n) if heights is None else np.asarray(heights, dtype=float)
         self.meta = dict(meta or {})
+        # optional (a parsed Bookshelf design has them; synthetic designs do not):
+        # pin offsets from the cell centre, and names as (uint8 bytes, int64 offsets)
+        self.pin_dx = None if pin_dx is None else np.ascontiguousarray(pin_dx, dtype=np.float64)
+        self.pin_dy = None if pin_dy is None else np.ascontiguousarray(pin_dy, dtype=np.float64)
+        self.cell_names = cell_names
+        self.net_names = net_names
 
     @property
     def num_cells(self) -> int:
@@ -218,8 +225,25 @@ class FlatDesign:
         return self._fixed_pos.copy()
 
     def pin_table(self):
+        if self.pin_dx is not None:
+            return (self.net_start, self.pin_cell, self.pin_dx, self.pin_dy)
         z = np.zeros(self.num_pins)
         return (self.net_start, self.pin_cell, z, z)
+
+    @staticmethod
+    def _names(packed, count: int, default: str) -> list[str]:
+        if packed is None:
+            return [f"{default}{i}" for i in range(count)]
+        data, off = packed
+        raw = bytes(np.asarray(data, dtype=np.uint8))
+        return [raw[off[i]:off[i + 1]].decode() for i in range(count)]
+
+    def cell_name_list(self) -> list[str]:
+        """Cell names: parsed ones, else "c<i>" (FlatDesign.to_design / benchgen convention)."""
+        return self._names(self.cell_names, self.num_cells, "c")
+
+    def net_name_list(self) -> list[str]:
+        return self._names(self.net_names, self.num_nets, "n")
 
     def to_design(self, module=None) -> Design:
         """Materialise the object model (this package's, or `module`'s classes --
@@ -231,18 +255,28 @@ class FlatDesign:
         R = getattr(mod, "Region", Region)
         D = getattr(mod, "Design", Design)
         cells = []
+        cnames = self.cell_name_list()
         for i in range(self.num_cells):
             if self._mask[i]:
-                cells.append(C(id=i, name=f"c{i}", width=float(self.widths[i]), height=float(self.heights[i]),
+                cells.append(C(id=i, name=cnames[i], width=float(self.widths[i]), height=float(self.heights[i]),
                                fixed=True, fixed_pos=(float(self._fixed_pos[i, 0]), float(self._fixed_pos[i, 1]))))
             else:
-                cells.append(C(id=i, name=f"c{i}", width=float(self.widths[i]), height=float(self.heights[i])))
+                cells.append(C(id=i, name=cnames[i], width=float(self.widths[i]), height=float(self.heights[i])))
         pc = self.pin_cell.tolist()
         ns = self.net_start.tolist()
-        nets = [Nt(id=e, name=f"n{e}", pins=[P(cell=c) for c in pc[ns[e]:ns[e + 1]]])
-                for e in range(self.num_nets)]
+        nnames = self.net_name_list()
+        if self.pin_dx is not None:
+            dx, dy = self.pin_dx.tolist(), self.pin_dy.tolist()
+            nets = [Nt(id=e, name=nnames[e], pins=[P(cell=pc[k], dx=dx[k], dy=dy[k]) for k in range(ns[e], ns[e + 1])])
+                    for e in range(self.num_nets)]
+        else:
+            nets = [Nt(id=e, name=nnames[e], pins=[P(cell=c) for c in pc[ns[e]:ns[e + 1]]])
+                    for e in range(self.num_nets)]
         r = self.region
-        return D(cells=cells, nets=nets, region=R(r.xmin, r.ymin, r.xmax, r.ymax))
+        RowC = getattr(mod, "Row", Row)
+        rows = [RowC(y=w.y, height=w.height, x=w.x, num_sites=w.num_sites, site_width=w.site_width)
+                for w in getattr(r, "rows", [])]
+        return D(cells=cells, nets=nets, region=R(r.xmin, r.ymin, r.xmax, r.ymax, rows=rows))
 
 
 def pin_arrays(design) -> tuple[np.ndarray, np.ndarray]:
