@@ -926,41 +926,54 @@ std::string host_line(Ctx* ctx, const char* h, const Lines& L, int64_t d) {
 
 int64_t lineno_of(Ctx* ctx, const Lines& L, int64_t d) { return fetch1(ctx, L.line.p + d) + 1; }
 
-// lines the device left undecided: re-parse on the host from the caller's buffer
-template <class Rec, Rec (*HostParse)(const char*, int)>
-void host_fixup(Ctx* ctx, const char* h, const Lines& L, Rec* rec) {
-  if (L.nd == 0) return;
-  std::vector<Rec> hr(L.nd);
-  // only the slow flags are needed; records are small, copy all once (rare path check first)
-  GIFT_CUDA(cudaMemcpyAsync(hr.data(), rec, L.nd * sizeof(Rec), cudaMemcpyDeviceToHost, ctx->stream));
-  std::vector<int64_t> hb(L.nd), hl(L.nd);
-  GIFT_CUDA(cudaMemcpyAsync(hb.data(), L.beg.p, L.nd * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-  GIFT_CUDA(cudaMemcpyAsync(hl.data(), L.len.p, L.nd * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-  GIFT_CUDA(cudaStreamSynchronize(ctx->stream));
-  bool any = false;
-  for (int64_t d = 0; d < L.nd; ++d)
-    if (hr[d].slow) {
-      hr[d] = HostParse(h + hb[d], (int)hl[d]);
-      any = true;
-    }
-  if (any) GIFT_CUDA(cudaMemcpyAsync(rec, hr.data(), L.nd * sizeof(Rec), cudaMemcpyHostToDevice, ctx->stream));
-  GIFT_CUDA(cudaStreamSynchronize(ctx->stream));
+template <class Rec>
+__global__ void k_slow_flags(int64_t nd, const Rec* __restrict__ rec, uint8_t* __restrict__ flag) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < nd; d += (int64_t)gridDim.x * blockDim.x)
+    flag[d] = rec[d].slow ? 1 : 0;
 }
 
 template <class Rec>
-__global__ void k_count_slow(int64_t nd, const Rec* __restrict__ rec, unsigned long long* __restrict__ cnt) {
-  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < nd; d += (int64_t)gridDim.x * blockDim.x)
-    if (rec[d].slow) atomicAdd(cnt, 1ull);
+__global__ void k_slow_gather(int64_t ns, const int64_t* __restrict__ idx, const int64_t* __restrict__ beg,
+                              const int64_t* __restrict__ len, int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x) {
+    out[2 * i] = beg[idx[i]];
+    out[2 * i + 1] = len[idx[i]];
+  }
 }
 
+template <class Rec>
+__global__ void k_slow_scatter(int64_t ns, const int64_t* __restrict__ idx, const Rec* __restrict__ fixed,
+                               Rec* __restrict__ rec) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x)
+    rec[idx[i]] = fixed[i];
+}
+
+// lines the device left undecided (rare number spellings): re-parse just those
+// on the host from the caller's buffer with the same line parser + strtod
 template <class Rec, Rec (*HostParse)(const char*, int)>
 void resolve_slow(Ctx* ctx, const char* h, const Lines& L, Rec* rec) {
   if (L.nd == 0) return;
-  DevBuf<unsigned long long> cnt(ctx, 1);
-  GIFT_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
-  k_count_slow<Rec><<<grid_for(L.nd, kBlock), kBlock, 0, ctx->stream>>>(L.nd, rec, cnt.p);
+  cudaStream_t st = ctx->stream;
+  DevBuf<uint8_t> flag(ctx, L.nd);
+  DevBuf<int64_t> idx(ctx, L.nd), cnt(ctx, 2);
+  k_slow_flags<Rec><<<grid_for(L.nd, kBlock), kBlock, 0, st>>>(L.nd, rec, flag.p);
   GIFT_LAUNCH_CHECK(ctx);
-  if (fetch1(ctx, cnt.p)) host_fixup<Rec, HostParse>(ctx, h, L, rec);
+  flagged_positions(ctx, flag.p, L.nd, idx.p, cnt.p);
+  const int64_t ns = fetch1(ctx, cnt.p);
+  if (ns == 0) return;
+  DevBuf<int64_t> bl(ctx, 2 * ns);
+  k_slow_gather<Rec><<<grid_for(ns, kBlock), kBlock, 0, st>>>(ns, idx.p, L.beg.p, L.len.p, bl.p);
+  GIFT_LAUNCH_CHECK(ctx);
+  std::vector<int64_t> hbl(2 * ns);
+  GIFT_CUDA(cudaMemcpyAsync(hbl.data(), bl.p, 2 * ns * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GIFT_CUDA(cudaStreamSynchronize(st));
+  std::vector<Rec> hr(ns);
+  for (int64_t i = 0; i < ns; ++i) hr[i] = HostParse(h + hbl[2 * i], (int)hbl[2 * i + 1]);
+  DevBuf<Rec> fixed(ctx, ns);
+  GIFT_CUDA(cudaMemcpyAsync(fixed.p, hr.data(), ns * sizeof(Rec), cudaMemcpyHostToDevice, st));
+  k_slow_scatter<Rec><<<grid_for(ns, kBlock), kBlock, 0, st>>>(ns, idx.p, fixed.p, rec);
+  GIFT_LAUNCH_CHECK(ctx);
+  GIFT_CUDA(cudaStreamSynchronize(st));
 }
 
 NodeRec node_dev(const char* s, int n) { return parse_node_line<true>(s, n); }
