@@ -353,7 +353,8 @@ def main() -> None:
     h_out = torch.empty((r1 - r0, 2), dtype=torch.float64).pin_memory()
 
     if world == 1:
-        e2e_api = "gift_filter_host (C ABI, pinned host buffers)"
+        e2e_api = ("gift_filter_host (C ABI, pinned host buffers; output written in place by the final hop)"
+                   if os.environ.get("GIFT_ZERO_COPY", "1") != "0" else "gift_filter_host (C ABI, pinned host buffers)")
 
         def step_e2e():
             _lib.check(lib.gift_filter_host(ctx, adj.handle, 3, sp_, kp_, ap_, 2, _lib.GIFT_DTYPE_F32,
@@ -386,8 +387,13 @@ def main() -> None:
     if world > 1:
         dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
     e2e_value = nnz_op * HOPS * k_e2e / float(t_e.item())
-    h2d = (g32.nbytes + mask.nbytes + fpos.nbytes) // 1 if world == 1 else \
-        int(h_g.numel() * 4 + h_mask.numel() + h_pos.numel() * 8)
+    zero_copy = world == 1 and os.environ.get("GIFT_ZERO_COPY", "1") != "0"
+    if zero_copy:  # pinned buffers used in place: fixed centres cross the bus for fixed rows only
+        h2d = g32.nbytes + mask.nbytes + int(mask.sum()) * 16
+    elif world == 1:
+        h2d = g32.nbytes + mask.nbytes + fpos.nbytes
+    else:
+        h2d = int(h_g.numel() * 4 + h_mask.numel() + h_pos.numel() * 8)
     d2h = (r1 - r0) * 2 * 8
 
     # ---- CPU baseline (rank 0, N = 1) ----

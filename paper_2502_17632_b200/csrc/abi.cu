@@ -323,6 +323,17 @@ int gift_filter(gift_ctx* ctx, gift_csr* adj, int n_terms, const double* h_sigma
   GIFT_API_END
 }
 
+// device address of a page-locked, mapped host buffer; nullptr for pageable memory
+static void* mapped_host(const void* h) {
+  if (!h) return nullptr;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return (at.type == cudaMemoryTypeHost && at.devicePointer) ? at.devicePointer : nullptr;
+}
+
 int gift_filter_host(gift_ctx* ctx, gift_csr* adj, int n_terms, const double* h_sigma, const int64_t* h_k,
                      const double* h_alpha, int64_t ncols, int in_dtype, const void* h_g, int out_dtype, void* h_out,
                      const uint8_t* h_fixed_mask, const double* h_fixed_pos, const double* h_region, int precision) {
@@ -333,17 +344,26 @@ int gift_filter_host(gift_ctx* ctx, gift_csr* adj, int n_terms, const double* h_
   const int64_t n = adj->n;
   const size_t in_b = (size_t)(n * ncols) * (in_dtype == GIFT_DTYPE_F64 ? 8 : 4);
   const size_t out_b = (size_t)(n * ncols) * (out_dtype == GIFT_DTYPE_F64 ? 8 : 4);
-  gift::DevBuf<char> dg(ctx, in_b), dout(ctx, out_b);
+  // Pinned (page-locked, mapped) host buffers are used in place: the fused
+  // fp32 bank writes each output row exactly once, from its final hop, so the
+  // placement streams to the host while that hop runs instead of after it;
+  // fixed centres are read only for fixed rows.  Pageable buffers are staged.
+  const char* zc_env = std::getenv("GIFT_ZERO_COPY");
+  const bool zc = !(zc_env && zc_env[0] == '0');
+  void* z_out = (zc && precision == GIFT_PREC_FP32) ? mapped_host(h_out) : nullptr;
+  const double* z_pos = (zc && h_fixed_mask) ? static_cast<const double*>(mapped_host(h_fixed_pos)) : nullptr;
+  gift::DevBuf<char> dg(ctx, in_b), dout(ctx, z_out ? 0 : out_b);
   gift::DevBuf<uint8_t> dmask(ctx, h_fixed_mask ? n : 0);
-  gift::DevBuf<double> dpos(ctx, h_fixed_mask ? 2 * n : 0);
+  gift::DevBuf<double> dpos(ctx, (h_fixed_mask && !z_pos) ? 2 * n : 0);
   GIFT_CUDA(cudaMemcpyAsync(dg.p, h_g, in_b, cudaMemcpyHostToDevice, st));
   if (h_fixed_mask) {
     GIFT_CUDA(cudaMemcpyAsync(dmask.p, h_fixed_mask, n, cudaMemcpyHostToDevice, st));
-    GIFT_CUDA(cudaMemcpyAsync(dpos.p, h_fixed_pos, 2 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (!z_pos) GIFT_CUDA(cudaMemcpyAsync(dpos.p, h_fixed_pos, 2 * n * sizeof(double), cudaMemcpyHostToDevice, st));
   }
-  gift::filter(ctx, adj, n_terms, h_sigma, h_k, h_alpha, ncols, in_dtype, dg.p, out_dtype, dout.p,
-               h_fixed_mask ? dmask.p : nullptr, h_fixed_mask ? dpos.p : nullptr, h_region, precision);
-  GIFT_CUDA(cudaMemcpyAsync(h_out, dout.p, out_b, cudaMemcpyDeviceToHost, st));
+  gift::filter(ctx, adj, n_terms, h_sigma, h_k, h_alpha, ncols, in_dtype, dg.p, out_dtype, z_out ? z_out : dout.p,
+               h_fixed_mask ? dmask.p : nullptr, h_fixed_mask ? (z_pos ? z_pos : dpos.p) : nullptr, h_region,
+               precision);
+  if (!z_out) GIFT_CUDA(cudaMemcpyAsync(h_out, dout.p, out_b, cudaMemcpyDeviceToHost, st));
   GIFT_CUDA(cudaStreamSynchronize(st));
   GIFT_API_END
 }
