@@ -388,26 +388,32 @@ int gift_place_host(gift_ctx* ctx, int64_t n_cells, int64_t n_nets, const int64_
   try {
     const int64_t n = n_cells;
     const size_t out_b = (size_t)(n * 2) * (out_dtype == GIFT_DTYPE_F64 ? 8 : 4);
+    // pinned host buffers in place, as in gift_filter_host
+    const char* zc_env = std::getenv("GIFT_ZERO_COPY");
+    const bool zc = !(zc_env && zc_env[0] == '0');
+    void* z_out = (zc && precision == GIFT_PREC_FP32) ? mapped_host(h_out) : nullptr;
+    const double* z_pos = (zc && h_fixed_mask) ? static_cast<const double*>(mapped_host(h_fixed_pos)) : nullptr;
     gift::DevBuf<float> dg(ctx, 2 * n);
-    gift::DevBuf<char> dout(ctx, out_b);
+    gift::DevBuf<char> dout(ctx, z_out ? 0 : out_b);
     gift::DevBuf<uint8_t> dmask(ctx, n);
-    gift::DevBuf<double> dpos(ctx, 2 * n);
+    gift::DevBuf<double> dpos(ctx, z_pos ? 0 : 2 * n);
     GIFT_CUDA(cudaMemcpyAsync(dg.p, h_g, 2 * n * sizeof(float), cudaMemcpyHostToDevice, st));
     if (h_fixed_mask) {
       GIFT_CUDA(cudaMemcpyAsync(dmask.p, h_fixed_mask, n, cudaMemcpyHostToDevice, st));
-      GIFT_CUDA(cudaMemcpyAsync(dpos.p, h_fixed_pos, 2 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+      if (!z_pos) GIFT_CUDA(cudaMemcpyAsync(dpos.p, h_fixed_pos, 2 * n * sizeof(double), cudaMemcpyHostToDevice, st));
     }
     const bool bmt = ctx->bmt_enabled;
     ctx->bmt_enabled = false;  // one-shot graph: the row kernel, no tiled copy
     try {
-      gift::filter(ctx, c, n_terms, h_sigma, h_k, h_alpha, 2, GIFT_DTYPE_F32, dg.p, out_dtype, dout.p,
-                   h_fixed_mask ? dmask.p : nullptr, h_fixed_mask ? dpos.p : nullptr, h_region, precision);
+      gift::filter(ctx, c, n_terms, h_sigma, h_k, h_alpha, 2, GIFT_DTYPE_F32, dg.p, out_dtype,
+                   z_out ? z_out : dout.p, h_fixed_mask ? dmask.p : nullptr,
+                   h_fixed_mask ? (z_pos ? z_pos : dpos.p) : nullptr, h_region, precision);
     } catch (...) {
       ctx->bmt_enabled = bmt;
       throw;
     }
     ctx->bmt_enabled = bmt;
-    GIFT_CUDA(cudaMemcpyAsync(h_out, dout.p, out_b, cudaMemcpyDeviceToHost, st));
+    if (!z_out) GIFT_CUDA(cudaMemcpyAsync(h_out, dout.p, out_b, cudaMemcpyDeviceToHost, st));
     GIFT_CUDA(cudaStreamSynchronize(st));
     if (nnz_out) *nnz_out = c->nnz;
   } catch (...) {

@@ -952,11 +952,11 @@ const float* csr_w32_public(Ctx* ctx, Csr* c);
 void launch_row_list(Ctx* ctx, const HopArgs& base, const int32_t* rows, int64_t nrows, int fin, int fout, int G);
 
 bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
-  if (env_int("GIFT_BMT", 1) == 0 || !c->sorted_rows) return false;
+  if (env_int("GIFT_BMT", 1) == 0 || !c->sorted_rows || !c->square) return false;
   // building the tiled copy costs ~a few hops; only resident graphs amortise it
   if (!ctx->bmt_enabled && !c->bmt.ok) return false;
   if (c->n < env_int("GIFT_BMT_MIN_ROWS", 262144) || c->mean_row < env_int("GIFT_BMT_MIN_MEAN", 32)) return false;
-  if (a.row_begin != 0 || a.n != c->n || a.part_in || a.part_out) return false;
+  if (a.row_begin != 0 || a.n != c->n || a.part_in) return false;  // part_out: the epilogue writes partials
   Csr::Bmt& B = c->bmt;
   if (!B.ready) {
     B.ready = true;

@@ -140,6 +140,7 @@ struct Csr {
   std::map<double, double*> s64;  // sigma -> 1/sqrt(d+sigma)   (fp64, exact)
   std::map<double, float*> s32;   // sigma -> fp32 rounding of s64
   bool sorted_rows = true;        // columns ascending within every row (canonical CSR)
+  bool square = true;             // every column < n (a full graph, or a shard's local block)
   // sliced block-major copy of the matrix for the fp32 hop (bmt.cu), lazy
   struct Bmt {
     bool ready = false, ok = false;

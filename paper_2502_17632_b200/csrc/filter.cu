@@ -752,7 +752,10 @@ void hop_fp32(Ctx* ctx, Csr* c, const gift_hop_desc* d) {
   a.fixed_mask = d->fixed_mask;
   a.fixed_pos = d->fixed_pos;
   memcpy(a.reg.v, d->region, sizeof(a.reg.v));
-  launch_hop(ctx, c, a, d->fin, d->fout, pick_group_lanes(c->mean_row), false);
+  // the tiled hop serves whole square blocks (a shard's local part, which may
+  // write partial sums); the ghost part (part_in) stays on the row kernel
+  const bool tiled = a.row_begin == 0 && a.n == c->n && !a.part_in;
+  launch_hop(ctx, c, a, d->fin, d->fout, pick_group_lanes(c->mean_row), tiled);
 }
 
 void pack_fp32(Ctx* ctx, int64_t n, int wcols, int nch, const float* const* s, int in_dtype, const void* g,
@@ -777,6 +780,19 @@ void gather_rows_f32(Ctx* ctx, int64_t n_idx, int F, const int64_t* idx, const f
   GIFT_LAUNCH_CHECK(ctx);
 }
 
+// bit 0: some row has a column descent; bit 1: some column >= n_rows (not square)
+__global__ void k_block_shape(int64_t n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ col,
+                              int* __restrict__ flags) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    int f = 0;
+    for (int64_t k = indptr[r]; k < indptr[r + 1]; ++k) {
+      if (k > indptr[r] && col[k] < col[k - 1]) f |= 1;
+      if (col[k] < 0 || (int64_t)col[k] >= n) f |= 2;
+    }
+    if (f) atomicOr(flags, f);
+  }
+}
+
 Csr* csr_from_arrays(Ctx* ctx, int64_t n_rows, int64_t nnz, const int64_t* d_indptr, const int32_t* d_indices,
                      const double* d_values) {
   Csr* c = new gift_csr();
@@ -788,12 +804,24 @@ Csr* csr_from_arrays(Ctx* ctx, int64_t n_rows, int64_t nnz, const int64_t* d_ind
   c->values = static_cast<double*>(csr_alloc(ctx, c, (nnz > 0 ? nnz : 1) * sizeof(double)));
   c->mean_row = n_rows > 0 ? (double)nnz / n_rows : 0.0;
   c->has_diagonal = true;
-  c->sorted_rows = false;  // remapped shard blocks: owned columns first, ghosts after
   GIFT_CUDA(cudaMemcpyAsync(c->indptr, d_indptr, (n_rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream));
   if (nnz > 0) {
     GIFT_CUDA(cudaMemcpyAsync(c->indices, d_indices, nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
     GIFT_CUDA(cudaMemcpyAsync(c->values, d_values, nnz * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   }
+  // a shard's local block (owned columns, remapped in order) is square with
+  // ascending columns and can take the tiled hop; ghost blocks cannot
+  DevBuf<int> flags(ctx, 1);
+  GIFT_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int), ctx->stream));
+  if (n_rows > 0) {
+    k_block_shape<<<grid_for(n_rows, kBlock), kBlock, 0, ctx->stream>>>(n_rows, c->indptr, c->indices, flags.p);
+    GIFT_LAUNCH_CHECK(ctx);
+  }
+  int h = 0;
+  GIFT_CUDA(cudaMemcpyAsync(&h, flags.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  GIFT_CUDA(cudaStreamSynchronize(ctx->stream));
+  c->sorted_rows = (h & 1) == 0;
+  c->square = (h & 2) == 0;
   return c;
 }
 

@@ -343,17 +343,23 @@ def _flat(nets):
 
 # ---------------------------------------------------------- sharded path --
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, world):
+@pytest.mark.parametrize("world,tiled", [(2, False), (4, False), (2, True), (3, True)])
+def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, monkeypatch, world, tiled):
     """The multi-GPU code path (partition, ghost pack, split local/ghost hops,
     fused epilogue) with `world` virtual ranks as threads on one device; the
     all-to-all is replaced by stream-ordered device copies (ThreadExchange),
-    so no kernel ever waits on another."""
+    so no kernel ever waits on another.  `tiled`: the local blocks take the
+    block-major tiled hop (forced below its size threshold), writing partial
+    sums that the ghost hop completes."""
     import threading
 
     import torch
 
     from paper_2502_17632_b200 import shard, synth
+
+    if tiled:
+        monkeypatch.setenv("GIFT_BMT_MIN_ROWS", "1")
+        monkeypatch.setenv("GIFT_BMT_MIN_MEAN", "1")
 
     fd = synth.generate("c2", seed=4, scale=0.02, window=600)
     adj = gb.build_clique_graph(fd, max_clique_pins=200)
