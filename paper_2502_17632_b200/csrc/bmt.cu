@@ -50,7 +50,11 @@ namespace {
 
 // rows per tile: 2048, or 8192 when rows are short (few entries per
 // (tile, block) segment would make the 64 KB block staging dominate)
-int tile_rows_for(double mean_row) { return mean_row >= 160.0 ? 2048 : 8192; }
+int tile_rows_for(double mean_row) {
+  const int forced = env_int("GIFT_BMT_TILE_ROWS", 0);  // 2048 / 4096 / 8192 (tuning)
+  if (forced == 2048 || forced == 4096 || forced == 8192) return forced;
+  return mean_row >= 160.0 ? 2048 : 8192;
+}
 constexpr int kCbits = 12;
 constexpr int kC = 1 << kCbits;   // columns per block; columns kC .. kC+15 = zero padding rows
 constexpr int kPadRows = 16;      // one zero row per bank residue mod 16 (padding never conflicts)
@@ -478,69 +482,49 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int64_t
   }
 }
 
-template <int FIN, int FOUT, int kThreads>
-__device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int64_t tile, int kR, int tid, int lane,
-                                         uint64_t pol_s, uint64_t pol_z) {
-  extern __shared__ float4 smem_f4[];
-  __shared__ int slice_ctr;
-  float* zs = reinterpret_cast<float*>(smem_f4);  // [(kC + kPadRows) * FIN], rows >= kC stay zero
-  float* accs = zs + (kC + kPadRows) * FIN;         // [kR * FIN]
-  const int64_t r0 = tile * kR;
-  const int nrows = (int)min((int64_t)kR, a.n - r0);
-  for (int i = tid; i < nrows * FIN; i += kThreads) accs[i] = 0.f;
-  const int64_t s_end = b.tile_seg[tile + 1];
-  for (int64_t s = b.tile_seg[tile]; s < s_end; ++s) {
-    const int64_t cbase = (int64_t)b.seg_code[s] * kC;
-    const float* zg = a.zin + cbase * FIN;
-    // finish the previous segment: its lanes may still read zs and update the
-    // accumulators of rows this segment touches again
-    __syncthreads();
-    const int64_t cend = min(cbase + kC, b.ncols);
-    const int nf = (int)((cend - cbase) * FIN);
-    const int nv = nf / 4;
-    const float4* src = reinterpret_cast<const float4*>(zg);
-    float4* dst = reinterpret_cast<float4*>(zs);
-#pragma unroll 4
-    for (int i = tid; i < nv; i += kThreads) dst[i] = src[i];
-    for (int i = nv * 4 + tid; i < nf; i += kThreads) zs[i] = zg[i];
-    for (int i = nf + tid; i < (kC + kPadRows) * FIN; i += kThreads) zs[i] = 0.f;  // short block + padding rows
-    if (tid == 0) slice_ctr = 0;
-    __syncthreads();
-    // slices of a segment touch distinct rows, so the warp that takes a slice
-    // does not change any result: balance them dynamically
-    const int64_t sl0 = b.seg_slice[s];
-    const int nsl = (int)(b.seg_slice[s + 1] - sl0);
-    // the next slice's index and metadata are fetched before the current one
-    // runs, so their latency hides behind its stream
-    auto grab = [&]() {
-      int j = 0;
-      if (lane == 0) j = atomicAdd(&slice_ctr, 1);
-      return __shfl_sync(0xffffffffu, j, 0);
-    };
-    int j = grab();
-    int64_t off = 0, end = 0;
-    int row = 0xffff;
-    if (j < nsl) {
-      off = b.slice_off[sl0 + j];
-      end = b.slice_off[sl0 + j + 1];
-      row = b.slice_rows[(sl0 + j) * 32 + lane];
-    }
-    while (j < nsl) {
-      const int jn = grab();
-      int64_t off_n = 0, end_n = 0;
-      int row_n = 0xffff;
-      if (jn < nsl) {
-        off_n = b.slice_off[sl0 + jn];
-        end_n = b.slice_off[sl0 + jn + 1];
-        row_n = b.slice_rows[(sl0 + jn) * 32 + lane];
-      }
-      run_slice<FIN>(b, off, (end - off) / 128, row, zs, accs, lane, pol_s);
-      j = jn;
-      off = off_n;
-      end = end_n;
-      row = row_n;
-    }
+// the slices of segment s: warps take them dynamically from *ctr (slices touch
+// distinct rows, so the assignment never changes a result)
+template <int FIN>
+__device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, const float* zs, float* accs, int* ctr,
+                                               int lane, uint64_t pol_s) {
+  const int64_t sl0 = b.seg_slice[s];
+  const int nsl = (int)(b.seg_slice[s + 1] - sl0);
+  // the next slice's index and metadata are fetched before the current one
+  // runs, so their latency hides behind its stream
+  auto grab = [&]() {
+    int j = 0;
+    if (lane == 0) j = atomicAdd(ctr, 1);
+    return __shfl_sync(0xffffffffu, j, 0);
+  };
+  int j = grab();
+  int64_t off = 0, end = 0;
+  int row = 0xffff;
+  if (j < nsl) {
+    off = b.slice_off[sl0 + j];
+    end = b.slice_off[sl0 + j + 1];
+    row = b.slice_rows[(sl0 + j) * 32 + lane];
   }
+  while (j < nsl) {
+    const int jn = grab();
+    int64_t off_n = 0, end_n = 0;
+    int row_n = 0xffff;
+    if (jn < nsl) {
+      off_n = b.slice_off[sl0 + jn];
+      end_n = b.slice_off[sl0 + jn + 1];
+      row_n = b.slice_rows[(sl0 + jn) * 32 + lane];
+    }
+    run_slice<FIN>(b, off, (end - off) / 128, row, zs, accs, lane, pol_s);
+    j = jn;
+    off = off_n;
+    end = end_n;
+    row = row_n;
+  }
+}
+
+// after the segments: residual entries, then the fused row epilogue
+template <int FIN, int FOUT, int kThreads>
+__device__ __forceinline__ void bmt_tile_finish(const HopArgs& a, const BmtArgs& b, int64_t r0, int nrows,
+                                                float* accs, int tid, int lane, uint64_t pol_z) {
   __syncthreads();
   // residual entries (sparse blocks: pad / macro columns), 8 lanes per row, from L2
   {
@@ -578,7 +562,96 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
   }
 }
 
+// one staging buffer: stage, barrier, slices, barrier
 template <int FIN, int FOUT, int kThreads>
+__device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int64_t tile, int kR, int tid, int lane,
+                                         uint64_t pol_s, uint64_t pol_z) {
+  extern __shared__ float4 smem_f4[];
+  __shared__ int slice_ctr;
+  float* zs = reinterpret_cast<float*>(smem_f4);  // [(kC + kPadRows) * FIN], rows >= kC stay zero
+  float* accs = zs + (kC + kPadRows) * FIN;         // [kR * FIN]
+  const int64_t r0 = tile * kR;
+  const int nrows = (int)min((int64_t)kR, a.n - r0);
+  for (int i = tid; i < nrows * FIN; i += kThreads) accs[i] = 0.f;
+  const int64_t s_end = b.tile_seg[tile + 1];
+  for (int64_t s = b.tile_seg[tile]; s < s_end; ++s) {
+    const int64_t cbase = (int64_t)b.seg_code[s] * kC;
+    const float* zg = a.zin + cbase * FIN;
+    // finish the previous segment: its lanes may still read zs and update the
+    // accumulators of rows this segment touches again
+    __syncthreads();
+    const int64_t cend = min(cbase + kC, b.ncols);
+    const int nf = (int)((cend - cbase) * FIN);
+    const int nv = nf / 4;
+    const float4* src = reinterpret_cast<const float4*>(zg);
+    float4* dst = reinterpret_cast<float4*>(zs);
+#pragma unroll 4
+    for (int i = tid; i < nv; i += kThreads) dst[i] = src[i];
+    for (int i = nv * 4 + tid; i < nf; i += kThreads) zs[i] = zg[i];
+    for (int i = nf + tid; i < (kC + kPadRows) * FIN; i += kThreads) zs[i] = 0.f;  // short block + padding rows
+    if (tid == 0) slice_ctr = 0;
+    __syncthreads();
+    segment_slices<FIN>(b, s, zs, accs, &slice_ctr, lane, pol_s);
+  }
+  bmt_tile_finish<FIN, FOUT, kThreads>(a, b, r0, nrows, accs, tid, lane, pol_z);
+}
+
+// cp.async (16 B, L2 hint) of segment s's signal block into zs; a ragged tail
+// (an odd row count at F = 2 in the last block) is copied by plain stores
+template <int FIN, int kThreads>
+__device__ __forceinline__ void stage_async(const HopArgs& a, const BmtArgs& b, int64_t s, float* zs, int tid,
+                                            uint64_t pol) {
+  const int64_t cbase = (int64_t)b.seg_code[s] * kC;
+  const int64_t cend = min(cbase + kC, b.ncols);
+  const int nf = (int)((cend - cbase) * FIN);
+  const int nv = nf / 4;
+  const float* zg = a.zin + cbase * FIN;
+  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(zs);
+  for (int i = tid; i < nv; i += kThreads)
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dst + 16u * (uint32_t)i),
+                 "l"(zg + 4 * (int64_t)i), "l"(pol)
+                 : "memory");
+  for (int i = nv * 4 + tid; i < nf; i += kThreads) zs[i] = zg[i];
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// two staging buffers: segment s + 1's block streams in (cp.async) while the
+// warps run segment s's slices; one barrier per segment
+template <int FIN, int FOUT, int kThreads>
+__device__ __forceinline__ void bmt_tile_db(const HopArgs& a, const BmtArgs& b, int64_t tile, int kR, int tid,
+                                            int lane, uint64_t pol_s, uint64_t pol_z) {
+  extern __shared__ float4 smem_f4[];
+  __shared__ int slice_ctr2[2];
+  constexpr int zrows = (kC + kPadRows) * FIN;
+  float* zs0 = reinterpret_cast<float*>(smem_f4);
+  float* zs1 = zs0 + zrows;
+  float* accs = zs1 + zrows;  // [kR * FIN]
+  const int64_t r0 = tile * kR;
+  const int nrows = (int)min((int64_t)kR, a.n - r0);
+  for (int i = tid; i < nrows * FIN; i += kThreads) accs[i] = 0.f;
+  for (int i = kC * FIN + tid; i < zrows; i += kThreads) {  // padding rows: zero in both buffers
+    zs0[i] = 0.f;
+    zs1[i] = 0.f;
+  }
+  if (tid == 0) slice_ctr2[0] = 0;
+  const int64_t s0 = b.tile_seg[tile], s1 = b.tile_seg[tile + 1];
+  if (s0 < s1) stage_async<FIN, kThreads>(a, b, s0, zs0, tid, pol_z);
+  for (int64_t s = s0; s < s1; ++s) {
+    const int buf = (int)((s - s0) & 1);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    // segment s is staged (every thread's copies), and every warp is done with
+    // segment s - 1: its buffer, counter and accumulator updates
+    __syncthreads();
+    if (s + 1 < s1) {
+      stage_async<FIN, kThreads>(a, b, s + 1, buf ? zs0 : zs1, tid, pol_z);
+      if (tid == 0) slice_ctr2[buf ^ 1] = 0;
+    }
+    segment_slices<FIN>(b, s, buf ? zs1 : zs0, accs, &slice_ctr2[buf], lane, pol_s);
+  }
+  bmt_tile_finish<FIN, FOUT, kThreads>(a, b, r0, nrows, accs, tid, lane, pol_z);
+}
+
+template <int FIN, int FOUT, int kThreads, bool DB>
 __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a, BmtArgs b) {
   const int kR = b.tile_rows;
   const int tid = threadIdx.x;
@@ -588,7 +661,10 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a
   __shared__ int64_t tile_sh;
   if (!b.ctr) {  // one CTA per tile; the block scheduler issues low blockIdx first
     const int64_t tile = b.tile_order ? b.tile_order[blockIdx.x] : blockIdx.x;
-    bmt_tile<FIN, FOUT, kThreads>(a, b, tile, kR, tid, lane, pol_s, pol_z);
+    if constexpr (DB)
+      bmt_tile_db<FIN, FOUT, kThreads>(a, b, tile, kR, tid, lane, pol_s, pol_z);
+    else
+      bmt_tile<FIN, FOUT, kThreads>(a, b, tile, kR, tid, lane, pol_s, pol_z);
     return;
   }
   // persistent CTAs take tiles costliest first from a global counter (the
@@ -604,7 +680,10 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a
     const int64_t tile = tile_sh;
     __syncthreads();
     if (tile < 0) break;
-    bmt_tile<FIN, FOUT, kThreads>(a, b, tile, kR, tid, lane, pol_s, pol_z);
+    if constexpr (DB)
+      bmt_tile_db<FIN, FOUT, kThreads>(a, b, tile, kR, tid, lane, pol_s, pol_z);
+    else
+      bmt_tile<FIN, FOUT, kThreads>(a, b, tile, kR, tid, lane, pol_s, pol_z);
   }
   if (tid == 0) {
     __threadfence();
@@ -617,38 +696,44 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a
 
 size_t bmt_smem(int fin, int kR) { return (size_t)(kC + kPadRows) * fin * 4 + (size_t)kR * fin * 4; }
 
-template <int FIN, int FOUT>
-void launch_bmt(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles) {
-  // 2048-row tiles: 2 CTAs x 512 threads per SM; 8192-row tiles: 1 CTA x 1024
-  auto kern = b.tile_rows > 2048 ? k_hop_bmt<FIN, FOUT, 1024> : k_hop_bmt<FIN, FOUT, 512>;
-  const int tpb = b.tile_rows > 2048 ? 1024 : 512;
-  const size_t smem = bmt_smem(FIN, b.tile_rows);
+size_t bmt_smem_db(int fin, int kR) { return bmt_smem(fin, kR) + (size_t)(kC + kPadRows) * fin * 4; }
+
+template <int FIN, int FOUT, bool DB>
+void launch_bmt_k(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, int tpb, size_t smem) {
+  auto kern = tpb == 1024 ? k_hop_bmt<FIN, FOUT, 1024, DB> : k_hop_bmt<FIN, FOUT, 512, DB>;
   static std::mutex mu;
-  static std::set<const void*> configured;  // dynamic smem opt-in once per instance
+  static std::map<const void*, int> occ;  // resident CTAs per SM per instance (after the smem opt-in)
+  int per_sm = 0;
   {
     std::lock_guard<std::mutex> lk(mu);
-    if (configured.insert((const void*)kern).second)
-      GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    auto it = occ.find((const void*)kern);
+    if (it == occ.end()) {
+      GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      GIFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tpb, smem));
+      occ[(const void*)kern] = per_sm;
+    } else {
+      per_sm = it->second;
+    }
   }
   unsigned grid = (unsigned)ntiles;
-  if (b.ctr) {
-    static std::mutex mu2;
-    static std::map<const void*, int> occ;  // resident CTAs per SM, per instance
-    int per_sm = 0;
-    {
-      std::lock_guard<std::mutex> lk(mu2);
-      auto it = occ.find((const void*)kern);
-      if (it == occ.end()) {
-        GIFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tpb, smem));
-        occ[(const void*)kern] = per_sm;
-      } else {
-        per_sm = it->second;
-      }
-    }
-    grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)std::max(per_sm, 1) * ctx->num_sms);
-  }
+  if (b.ctr) grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)std::max(per_sm, 1) * ctx->num_sms);
   kern<<<grid, tpb, smem, ctx->stream>>>(a, b);
   GIFT_LAUNCH_CHECK(ctx);
+}
+
+template <int FIN, int FOUT>
+void launch_bmt(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles) {
+  // 2048-row tiles: 2 CTAs x 512 threads per SM; taller tiles: 1 CTA x 1024.
+  // Double-buffered staging when both buffers fit at that occupancy.
+  const int tpb = b.tile_rows > 2048 ? 1024 : 512;
+  const int per_sm = tpb == 512 ? 2 : 1;
+  const size_t smem1 = bmt_smem(FIN, b.tile_rows), smem2 = bmt_smem_db(FIN, b.tile_rows);
+  const bool db = env_int("GIFT_BMT_DB", 1) && ((uintptr_t)a.zin & 15) == 0 &&
+                  (size_t)per_sm * (smem2 + 3 * 1024) <= 228 * 1024;
+  if (db)
+    launch_bmt_k<FIN, FOUT, true>(ctx, a, b, ntiles, tpb, smem2);
+  else
+    launch_bmt_k<FIN, FOUT, false>(ctx, a, b, ntiles, tpb, smem1);
 }
 
 template <int FIN>
