@@ -708,7 +708,12 @@ void launch_bmt_k(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, 
     std::lock_guard<std::mutex> lk(mu);
     auto it = occ.find((const void*)kern);
     if (it == occ.end()) {
-      GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      int optin = 0;
+      GIFT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+      cudaFuncAttributes fa{};
+      GIFT_CUDA(cudaFuncGetAttributes(&fa, kern));
+      GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     optin - (int)fa.sharedSizeBytes));
       GIFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tpb, smem));
       occ[(const void*)kern] = per_sm;
     } else {

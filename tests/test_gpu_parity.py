@@ -404,13 +404,19 @@ def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, monkeypatch, world,
     assert rel_l2(full, single) <= FP32_TOL
 
 
-@pytest.mark.parametrize("config,scale,cap", [("c2", 0.05, 200), ("c3", 0.03, 200), ("c1", 0.2, None),
-                                              ("c0", 1.0, None), ("c2", 0.01, None)])
-def test_bmt_hop_matches_oracle_and_row_kernel(gb, orc, monkeypatch, config, scale, cap):
+@pytest.mark.parametrize("config,scale,cap,tile_rows,db", [
+    ("c2", 0.05, 200, 0, 1), ("c3", 0.03, 200, 0, 1), ("c1", 0.2, None, 0, 1), ("c0", 1.0, None, 0, 1),
+    ("c2", 0.01, None, 0, 1), ("c2", 0.05, 200, 4096, 1), ("c1", 0.2, None, 4096, 1), ("c3", 0.03, 200, 2048, 0),
+    ("c1", 0.2, None, 8192, 0)])
+def test_bmt_hop_matches_oracle_and_row_kernel(gb, orc, monkeypatch, config, scale, cap, tile_rows, db):
     """Force the block-major tiled hop (bmt.cu) on small graphs (it is normally
     reserved for >= 256k rows) and check it against the oracle and the
-    row-parallel kernel."""
+    row-parallel kernel; tile heights 2048 / 4096 / 8192, single- and
+    double-buffered block staging."""
     from paper_2502_17632_b200 import synth
+
+    monkeypatch.setenv("GIFT_BMT_TILE_ROWS", str(tile_rows))
+    monkeypatch.setenv("GIFT_BMT_DB", str(db))
 
     fd = synth.generate(config, seed=6, scale=scale, window=900)
     ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, cap)
