@@ -44,6 +44,11 @@
 #include "common.cuh"
 #include "hop.cuh"
 
+
+#ifndef GIFT_BMT_STREAM
+#define GIFT_BMT_STREAM 0  // 1: static per-warp record streams per segment; 0: dynamic slice grabbing
+#endif
+
 namespace gift {
 
 namespace {
@@ -177,6 +182,27 @@ __global__ void k_seg_slices(int64_t nseg, const int64_t* __restrict__ seg_run, 
 }
 
 // slot count of each slice: its longest (first) run rounded up to 4, x 32 lanes
+// static split of a segment's slices over the NW warps of a CTA, balanced by
+// steps: warp w takes the slices whose first step lies in [w T / NW, (w+1) T / NW)
+__global__ void k_warp_split(int64_t nseg, int nw, const int64_t* __restrict__ seg_slice,
+                             const int64_t* __restrict__ slice_off, int32_t* __restrict__ split) {
+  const int64_t total = nseg * (nw + 1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sg = i / (nw + 1);
+    const int w = (int)(i % (nw + 1));
+    const int64_t sl0 = seg_slice[sg], sl1 = seg_slice[sg + 1];
+    const int64_t base = slice_off[sl0], T = (slice_off[sl1] - base) / 128;
+    const int64_t target = (T * w) / nw;
+    int64_t lo = sl0, hi = sl1;  // first slice with start step >= target
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if ((slice_off[mid] - base) / 128 < target) lo = mid + 1;
+      else hi = mid;
+    }
+    split[i] = (int32_t)(w == nw ? sl1 - sl0 : lo - sl0);
+  }
+}
+
 __global__ void k_slice_len(int64_t nseg, const int64_t* __restrict__ seg_run, const int64_t* __restrict__ seg_slice,
                             const uint64_t* __restrict__ rkey_s, int64_t* __restrict__ slice_slots) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
@@ -423,6 +449,7 @@ struct BmtArgs {
   const int32_t* tile_order;  // persistent mode: tiles by decreasing cost
   unsigned* ctr;              // persistent mode: [next tile, finished CTAs]; null = one CTA per tile
   int64_t ntiles;
+  const int32_t* split;       // [nseg * (NW + 1)] static warp split of each segment's slices; null = dynamic
 };
 
 __device__ __forceinline__ uint2 ld_stream_v2u32(const void* p, uint64_t pol) {
@@ -458,7 +485,16 @@ __device__ __forceinline__ void gather_fma(float (&acc)[FIN], float w, int c, co
 }
 
 // one slice: lane = one row's run, summed in its (conflict-scheduled) order
-template <int FIN>
+// PF: steps of matrix records kept in flight per lane by an explicit software
+// pipeline (0: plain unrolled loop).  Measured on B200 (tools/ab: c3 / c4):
+// long runs (2048-row tiles) gain at F <= 2 with 3 (F = 4 spills and loses),
+// short runs (taller tiles, 1 CTA per SM) gain with 2.
+template <int FIN, int kThreads>
+__host__ __device__ constexpr int bmt_pf() {
+  return kThreads == 512 ? (FIN == 4 ? 0 : 3) : 2;
+}
+
+template <int FIN, int PF>
 __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int64_t steps, int row, const float* zs,
                                           float* accs, int lane, uint64_t pol_s) {
   float acc[FIN];
@@ -467,6 +503,37 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int64_t
   const uint8_t* rec = b.data + (off / 128) * 768;
   const uint8_t* cp = rec + 8 * lane;
   const uint8_t* wp = rec + 256 + 16 * lane;
+if constexpr (PF > 0) {
+  // software pipeline: the record of step k + D is requested as soon as step k's
+  // registers are consumed, so D steps of loads are always in flight (a plain
+  // unrolled loop restarts its loads every unroll block and exposes the latency)
+  constexpr int D = PF;
+  uint2 cq[D];
+  float4 wq[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+    if (d < steps) {
+      cq[d] = ld_stream_v2u32(cp + d * 768, pol_s);
+      wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + d * 768), pol_s);
+    }
+  for (int64_t k = 0; k < steps; k += D) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const uint2 cv = cq[d];
+      const float4 wv = wq[d];
+      if (k + d + D < steps) {
+        cq[d] = ld_stream_v2u32(cp + (k + d + D) * 768, pol_s);
+        wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + (k + d + D) * 768), pol_s);
+      }
+      if (k + d < steps) {
+        gather_fma<FIN, true>(acc, wv.x, (int)(cv.x & 0xffff), zs, nullptr, 0);
+        gather_fma<FIN, true>(acc, wv.y, (int)(cv.x >> 16), zs, nullptr, 0);
+        gather_fma<FIN, true>(acc, wv.z, (int)(cv.y & 0xffff), zs, nullptr, 0);
+        gather_fma<FIN, true>(acc, wv.w, (int)(cv.y >> 16), zs, nullptr, 0);
+      }
+    }
+  }
+} else {
 #pragma unroll 4
   for (int64_t k = 0; k < steps; ++k) {
     const uint2 cv = ld_stream_v2u32(cp + k * 768, pol_s);
@@ -476,6 +543,7 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int64_t
     gather_fma<FIN, true>(acc, wv.z, (int)(cv.y & 0xffff), zs, nullptr, 0);
     gather_fma<FIN, true>(acc, wv.w, (int)(cv.y >> 16), zs, nullptr, 0);
   }
+}
   if (row != 0xffff) {
 #pragma unroll
     for (int f = 0; f < FIN; ++f) accs[row * FIN + f] += acc[f];
@@ -484,7 +552,7 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int64_t
 
 // the slices of segment s: warps take them dynamically from *ctr (slices touch
 // distinct rows, so the assignment never changes a result)
-template <int FIN>
+template <int FIN, int PF>
 __device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, const float* zs, float* accs, int* ctr,
                                                int lane, uint64_t pol_s) {
   const int64_t sl0 = b.seg_slice[s];
@@ -513,11 +581,82 @@ __device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, cons
       end_n = b.slice_off[sl0 + jn + 1];
       row_n = b.slice_rows[(sl0 + jn) * 32 + lane];
     }
-    run_slice<FIN>(b, off, (end - off) / 128, row, zs, accs, lane, pol_s);
+    run_slice<FIN, PF>(b, off, (end - off) / 128, row, zs, accs, lane, pol_s);
     j = jn;
     off = off_n;
     end = end_n;
     row = row_n;
+  }
+}
+
+// the slices of segment s as ONE record stream per warp: the warp owns a
+// contiguous range of slices (static split, balanced by steps), so its loads
+// run ahead across slice boundaries; at a boundary each lane adds its run to
+// its row's accumulator and switches row (boundaries are warp-uniform)
+template <int FIN, int PF, int NW>
+__device__ __forceinline__ void segment_stream(const BmtArgs& b, int64_t s, const float* zs, float* accs, int warp,
+                                               int lane, uint64_t pol_s) {
+  const int64_t sl0 = b.seg_slice[s];
+  const int32_t* sp = b.split + s * (NW + 1);
+  int64_t j = sl0 + sp[warp];
+  const int64_t j1 = sl0 + sp[warp + 1];
+  if (j >= j1) return;
+  const int64_t off0 = b.slice_off[j];
+  const int64_t total = (b.slice_off[j1] - off0) / 128;
+  const uint8_t* rec = b.data + (off0 / 128) * 768;
+  const uint8_t* cp = rec + 8 * lane;
+  const uint8_t* wp = rec + 256 + 16 * lane;
+  int64_t bound = (b.slice_off[j + 1] - off0) / 128;
+  int row = b.slice_rows[j * 32 + lane];
+  int64_t bound_n = total;
+  int row_n = 0xffff;
+  if (j + 1 < j1) {
+    bound_n = (b.slice_off[j + 2] - off0) / 128;
+    row_n = b.slice_rows[(j + 1) * 32 + lane];
+  }
+  float acc[FIN];
+#pragma unroll
+  for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
+  constexpr int D = PF > 0 ? PF : 2;
+  uint2 cq[D];
+  float4 wq[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+    if (d < total) {
+      cq[d] = ld_stream_v2u32(cp + d * 768, pol_s);
+      wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + d * 768), pol_s);
+    }
+  for (int64_t k = 0; k < total; k += D) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const uint2 cv = cq[d];
+      const float4 wv = wq[d];
+      if (k + d + D < total) {
+        cq[d] = ld_stream_v2u32(cp + (k + d + D) * 768, pol_s);
+        wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + (k + d + D) * 768), pol_s);
+      }
+      if (k + d < total) {
+        gather_fma<FIN, true>(acc, wv.x, (int)(cv.x & 0xffff), zs, nullptr, 0);
+        gather_fma<FIN, true>(acc, wv.y, (int)(cv.x >> 16), zs, nullptr, 0);
+        gather_fma<FIN, true>(acc, wv.z, (int)(cv.y & 0xffff), zs, nullptr, 0);
+        gather_fma<FIN, true>(acc, wv.w, (int)(cv.y >> 16), zs, nullptr, 0);
+        if (k + d + 1 == bound) {  // end of this slice (same step for every lane)
+          if (row != 0xffff) {
+#pragma unroll
+            for (int f = 0; f < FIN; ++f) accs[row * FIN + f] += acc[f];
+          }
+#pragma unroll
+          for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
+          ++j;
+          row = row_n;
+          bound = bound_n;
+          if (j + 1 < j1) {
+            bound_n = (b.slice_off[j + 2] - off0) / 128;
+            row_n = b.slice_rows[(j + 1) * 32 + lane];
+          }
+        }
+      }
+    }
   }
 }
 
@@ -591,7 +730,11 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
     for (int i = nf + tid; i < (kC + kPadRows) * FIN; i += kThreads) zs[i] = 0.f;  // short block + padding rows
     if (tid == 0) slice_ctr = 0;
     __syncthreads();
-    segment_slices<FIN>(b, s, zs, accs, &slice_ctr, lane, pol_s);
+#if GIFT_BMT_STREAM
+    segment_stream<FIN, bmt_pf<FIN, kThreads>(), kThreads / 32>(b, s, zs, accs, tid >> 5, lane, pol_s);
+#else
+    segment_slices<FIN, bmt_pf<FIN, kThreads>()>(b, s, zs, accs, &slice_ctr, lane, pol_s);
+#endif
   }
   bmt_tile_finish<FIN, FOUT, kThreads>(a, b, r0, nrows, accs, tid, lane, pol_z);
 }
@@ -646,7 +789,12 @@ __device__ __forceinline__ void bmt_tile_db(const HopArgs& a, const BmtArgs& b, 
       stage_async<FIN, kThreads>(a, b, s + 1, buf ? zs0 : zs1, tid, pol_z);
       if (tid == 0) slice_ctr2[buf ^ 1] = 0;
     }
-    segment_slices<FIN>(b, s, buf ? zs1 : zs0, accs, &slice_ctr2[buf], lane, pol_s);
+#if GIFT_BMT_STREAM
+    segment_stream<FIN, bmt_pf<FIN, kThreads>(), kThreads / 32>(b, s, buf ? zs1 : zs0, accs, tid >> 5, lane,
+                                                                pol_s);
+#else
+    segment_slices<FIN, bmt_pf<FIN, kThreads>()>(b, s, buf ? zs1 : zs0, accs, &slice_ctr2[buf], lane, pol_s);
+#endif
   }
   bmt_tile_finish<FIN, FOUT, kThreads>(a, b, r0, nrows, accs, tid, lane, pol_z);
 }
@@ -976,6 +1124,13 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   B.slice_off = static_cast<int64_t*>(csr_alloc(ctx, c, (nslices + 1) * sizeof(int64_t)));
   exclusive_sum(ctx, slots.p, B.slice_off, nslices + 1);
   const int64_t total = fetch(ctx, B.slice_off + nslices);
+  {  // static warp split (segment_stream); the kernel for this tile height has NW warps
+    const int nw = (kR > 2048 ? 1024 : 512) / 32;
+    B.nw = nw;
+    B.split = static_cast<int32_t*>(csr_alloc(ctx, c, (nseg * (nw + 1) + 1) * sizeof(int32_t)));
+    k_warp_split<<<grid_for(nseg * (nw + 1), kBlock), kBlock, 0, st>>>(nseg, nw, B.seg_slice, B.slice_off, B.split);
+    GIFT_LAUNCH_CHECK(ctx);
+  }
   // 6. scatter entries into slices; padding = column kC (zero signal row), weight 0
   B.slice_rows = static_cast<uint16_t*>(csr_alloc(ctx, c, (nslices * 32 + 1) * sizeof(uint16_t)));
   DevBuf<uint16_t> colb(ctx, total + 8);
@@ -1083,7 +1238,7 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
   }
   BmtArgs b{c->n,         B.tile_rows,  B.data,      B.wide,      B.res_rowptr, B.res_col,     B.res_w,
             B.tile_seg,   B.seg_code,   B.seg_slice, B.slice_off, B.slice_rows, order,         ctr,
-            B.ntiles};
+            B.ntiles,     B.split};
   switch (fin) {
     case 1: launch_bmt_out<1>(ctx, a, b, B.ntiles, fout); break;
     case 2: launch_bmt_out<2>(ctx, a, b, B.ntiles, fout); break;
