@@ -1176,9 +1176,20 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
     std::vector<int64_t> hc(ntiles);
     GIFT_CUDA(cudaMemcpyAsync(hc.data(), cost.p, ntiles * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     GIFT_CUDA(cudaStreamSynchronize(st));
+    // heavy tiles (> 1.25 x the median cost) first, costliest first; the rest
+    // keep index order, so CTAs resident together work on neighbouring tiles
+    // and share the signal blocks they stage in L2 (a full cost sort scatters
+    // them: +12 % DRAM bytes on config 4, whose tiles are uniform)
+    std::vector<int64_t> sorted(hc);
+    std::nth_element(sorted.begin(), sorted.begin() + ntiles / 2, sorted.end());
+    const double heavy = 1.25 * (double)sorted[ntiles / 2];
     std::vector<int32_t> order(ntiles);
     for (int64_t t = 0; t < ntiles; ++t) order[t] = (int32_t)t;
-    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return hc[x] > hc[y]; });
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+      const bool hx = (double)hc[x] > heavy, hy = (double)hc[y] > heavy;
+      if (hx != hy) return hx;
+      return hx && hc[x] > hc[y];
+    });
     GIFT_CUDA(cudaMemcpyAsync(B.tile_order, order.data(), ntiles * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   }
   GIFT_CUDA(cudaStreamSynchronize(st));
