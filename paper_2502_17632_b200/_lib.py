@@ -21,7 +21,8 @@ from .errors import (
 )
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgiftb200.so")
+# GIFT_LIB: an alternative build of the same library (A/B of compile-time variants, tools/)
+LIB_PATH = os.environ.get("GIFT_LIB") or os.path.join(HERE, "libgiftb200.so")
 
 GIFT_OK = 0
 GIFT_ERR_VALUE = 1

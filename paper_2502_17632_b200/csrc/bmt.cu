@@ -8,8 +8,8 @@
 // are banded (nets live in +-W index windows): a tile of rows touches only a
 // few column blocks.  BMT stores a reordered copy of the matrix:
 //
-//   row tiles of kR = 2048 rows (8192 for short-row graphs, see tile_rows_for)
-//   x column blocks of kC = 4096 columns;
+//   row tiles of kR = 2048 rows x column blocks of kC = 4096 columns (4096 x
+//   8192 for short-row graphs, see bmt_shape_for);
 //   a SEGMENT = the entries of one (tile, block) pair; segments tile-major,
 //   blocks ascending;
 //   inside a segment, every row's run of entries goes to one lane of a
@@ -48,21 +48,42 @@
 #ifndef GIFT_BMT_STREAM
 #define GIFT_BMT_STREAM 0  // 1: static per-warp record streams per segment; 0: dynamic slice grabbing
 #endif
+// records in flight per warp (software-pipeline depth), per signal width
+#ifndef GIFT_BMT_DEPTH4
+#define GIFT_BMT_DEPTH4 3
+#endif
+#ifndef GIFT_BMT_DEPTH2
+#define GIFT_BMT_DEPTH2 5
+#endif
+template <int FIN>
+__host__ __device__ constexpr int bmt_depth() {
+  return FIN == 4 ? GIFT_BMT_DEPTH4 : GIFT_BMT_DEPTH2;
+}
 
 namespace gift {
 
 namespace {
 
-// rows per tile: 2048, or 8192 when rows are short (few entries per
-// (tile, block) segment would make the 64 KB block staging dominate)
-int tile_rows_for(double mean_row) {
-  const int forced = env_int("GIFT_BMT_TILE_ROWS", 0);  // 2048 / 4096 / 8192 (tuning)
-  if (forced == 2048 || forced == 4096 || forced == 8192) return forced;
-  return mean_row >= 160.0 ? 2048 : 8192;
+// Tile shape (rows per tile kR, columns per block kC = 2^cb), chosen per graph.
+// Long rows (c2/c3: ~400 entries) keep 2048 x 4096: runs of ~80 entries per
+// segment, 2 CTAs per SM at F = 4.  Short rows (c4: ~70 entries spread over a
+// +-40k-column band) get 4096 x 8192: a 4096-column block leaves ~6 entries per
+// run, so per-slice overhead and the round-up of runs to 4-entry steps (x1.32
+// stored slots) dominate; 8192 columns give ~11-entry runs and x1.20.  Both
+// shapes fit the F = 4 kernel: (kC + 16 + kR) x 16 B of shared memory.
+struct BmtShape {
+  int kR, cb;
+};
+BmtShape bmt_shape_for(double mean_row) {
+  BmtShape s = mean_row >= 160.0 ? BmtShape{2048, 12} : BmtShape{4096, 13};
+  const int fr = env_int("GIFT_BMT_TILE_ROWS", 0);  // 2048 / 4096 / 8192 (tuning)
+  if (fr == 2048 || fr == 4096 || fr == 8192) s.kR = fr;
+  const int fc = env_int("GIFT_BMT_COL_BITS", 0);  // 11..14 (tuning)
+  if (fc >= 11 && fc <= 14) s.cb = fc;
+  return s;
 }
-constexpr int kCbits = 12;
-constexpr int kC = 1 << kCbits;   // columns per block; columns kC .. kC+15 = zero padding rows
 constexpr int kPadRows = 16;      // one zero row per bank residue mod 16 (padding never conflicts)
+// columns kC .. kC + 15 of a staged block are its zero padding rows
 constexpr int kStage = 1024;      // a segment with >= kStage entries stages its block
 constexpr int kBlock = 256;
 constexpr int kWide = 8;          // rows touching > max(kWide, 3 x mean) blocks run on the row kernel
@@ -83,13 +104,13 @@ __global__ void k_iota64(int64_t n, int64_t* __restrict__ p) {
 // rows whose entries span many more column blocks than a typical row (pads /
 // macros wired all over the die): one CTA would walk every block for them, so
 // they stay on the row kernel.  Pass 1 counts blocks per row, pass 2 flags.
-__global__ void k_row_nblocks(int64_t n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ col,
+__global__ void k_row_nblocks(int64_t n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ col, int cb,
                               uint16_t* __restrict__ nb_out, unsigned long long* __restrict__ total) {
   unsigned long long acc = 0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
     int nb = 0, prev = -1;
     for (int64_t k = indptr[r]; k < indptr[r + 1] && nb < 65535; ++k) {
-      const int b = col[k] >> kCbits;
+      const int b = col[k] >> cb;
       nb += b != prev;
       prev = b;
     }
@@ -116,25 +137,25 @@ __global__ void k_wide_rows(int64_t n, const int64_t* __restrict__ indptr, const
 // sort key (tile, block) and payload (weight bits, row in tile, column in block);
 // wide rows get the sentinel key and sort past the kept entries
 __global__ void k_bmt_keys(int64_t nnz, const int32_t* __restrict__ row_of, const int32_t* __restrict__ col,
-                           const float* __restrict__ w, int bb, int kR, const uint8_t* __restrict__ wide,
+                           const float* __restrict__ w, int bb, int kR, int cb, const uint8_t* __restrict__ wide,
                            uint32_t sentinel,
                            uint32_t* __restrict__ key, uint64_t* __restrict__ payload) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t r = (uint32_t)row_of[k], c = (uint32_t)col[k];
-    key[k] = wide[r] ? sentinel : (((r / kR) << bb) | (c >> kCbits));
-    const uint32_t packed = ((r % kR) << kCbits) | (c & (kC - 1));
+    key[k] = wide[r] ? sentinel : (((r / kR) << bb) | (c >> cb));
+    const uint32_t packed = ((r % kR) << cb) | (c & ((1u << cb) - 1));
     payload[k] = ((uint64_t)__float_as_uint(w[k]) << 32) | packed;
   }
 }
 
 // segment heads (new (tile, block)) and run heads (new (segment, row)), counted
-__global__ void k_bmt_heads(int64_t nnz, const uint32_t* __restrict__ key, const uint64_t* __restrict__ pay,
+__global__ void k_bmt_heads(int64_t nnz, int cb, const uint32_t* __restrict__ key, const uint64_t* __restrict__ pay,
                             uint8_t* __restrict__ seg_head, uint8_t* __restrict__ run_head,
                             unsigned long long* __restrict__ counts) {
   unsigned long long ns = 0, nr = 0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
     const bool sh = k == 0 || key[k] != key[k - 1];
-    const bool rh = sh || ((uint32_t)pay[k] >> kCbits) != ((uint32_t)pay[k - 1] >> kCbits);
+    const bool rh = sh || ((uint32_t)pay[k] >> cb) != ((uint32_t)pay[k - 1] >> cb);
     seg_head[k] = sh;
     run_head[k] = rh;
     ns += sh;
@@ -152,7 +173,7 @@ __global__ void k_bmt_heads(int64_t nnz, const uint32_t* __restrict__ key, const
 
 // per run: sort key (segment, longest first); the stable sort keeps row order among equals
 __global__ void k_run_keys(int64_t nruns, const int64_t* __restrict__ run_start, int64_t nnz,
-                           const int64_t* __restrict__ seg_start, int64_t nseg, uint64_t* __restrict__ rkey) {
+                           const int64_t* __restrict__ seg_start, int64_t nseg, int cb, uint64_t* __restrict__ rkey) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nruns; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = run_start[i], b = i + 1 < nruns ? run_start[i + 1] : nnz;
     int64_t lo = 0, hi = nseg;  // segment = last seg_start <= a
@@ -162,16 +183,16 @@ __global__ void k_run_keys(int64_t nruns, const int64_t* __restrict__ run_start,
       else hi = mid;
     }
     const uint64_t len = (uint64_t)(b - a);  // <= kC distinct columns in a block
-    rkey[i] = ((uint64_t)lo << 13) | ((uint64_t)kC - len);
+    rkey[i] = ((uint64_t)lo << (cb + 1)) | ((1ull << cb) - len);
   }
 }
 
 // first sorted run of every segment
-__global__ void k_seg_runs(int64_t nruns, const uint64_t* __restrict__ rkey_s, int64_t nseg,
+__global__ void k_seg_runs(int64_t nruns, const uint64_t* __restrict__ rkey_s, int64_t nseg, int cb,
                            int64_t* __restrict__ seg_run) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= nruns; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = i < nruns ? (int64_t)(rkey_s[i] >> 13) : nseg;
-    const int64_t sp = i > 0 ? (int64_t)(rkey_s[i - 1] >> 13) : -1;
+    const int64_t s = i < nruns ? (int64_t)(rkey_s[i] >> (cb + 1)) : nseg;
+    const int64_t sp = i > 0 ? (int64_t)(rkey_s[i - 1] >> (cb + 1)) : -1;
     for (int64_t t = sp + 1; t <= s; ++t) seg_run[t] = i;
   }
 }
@@ -204,11 +225,11 @@ __global__ void k_warp_split(int64_t nseg, int nw, const int64_t* __restrict__ s
 }
 
 __global__ void k_slice_len(int64_t nseg, const int64_t* __restrict__ seg_run, const int64_t* __restrict__ seg_slice,
-                            const uint64_t* __restrict__ rkey_s, int64_t* __restrict__ slice_slots) {
+                            const uint64_t* __restrict__ rkey_s, int cb, int64_t* __restrict__ slice_slots) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r0 = seg_run[s], r1 = seg_run[s + 1];
     for (int64_t j = 0; r0 + 32 * j < r1; ++j) {
-      const int64_t len = kC - (int64_t)(rkey_s[r0 + 32 * j] & 0x1fff);
+      const int64_t len = (1ll << cb) - (int64_t)(rkey_s[r0 + 32 * j] & ((2ull << cb) - 1));
       slice_slots[seg_slice[s] + j] = ((len + 3) / 4) * 4 * 32;
     }
   }
@@ -217,7 +238,7 @@ __global__ void k_slice_len(int64_t nseg, const int64_t* __restrict__ seg_run, c
 // scatter every run's entries into its slice lane (CTA per segment, thread per run)
 __global__ void k_scatter_runs(int64_t nseg, const int64_t* __restrict__ seg_run, const int64_t* __restrict__ seg_slice,
                                const int64_t* __restrict__ run_perm, const int64_t* __restrict__ run_start,
-                               int64_t nruns, int64_t nnz, const uint64_t* __restrict__ pay,
+                               int64_t nruns, int64_t nnz, int cb, const uint64_t* __restrict__ pay,
                                const int64_t* __restrict__ slice_off, uint16_t* __restrict__ slice_rows,
                                uint16_t* __restrict__ col, float* __restrict__ w) {
   for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
@@ -229,11 +250,11 @@ __global__ void k_scatter_runs(int64_t nseg, const int64_t* __restrict__ seg_run
       const int64_t run = run_perm[q];
       const int64_t a = run_start[run], b = run + 1 < nruns ? run_start[run + 1] : nnz;
       const int64_t base = slice_off[slice] + 4 * lane;
-      slice_rows[slice * 32 + lane] = (uint16_t)((uint32_t)pay[a] >> kCbits);
+      slice_rows[slice * 32 + lane] = (uint16_t)((uint32_t)pay[a] >> cb);
       for (int64_t k = 0; k < b - a; ++k) {
         const uint64_t p = pay[a + k];
         const int64_t slot = base + (k / 4) * 128 + (k % 4);
-        col[slot] = (uint16_t)(p & (kC - 1));
+        col[slot] = (uint16_t)(p & ((1u << cb) - 1));
         w[slot] = __uint_as_float((uint32_t)(p >> 32));
       }
     }
@@ -253,7 +274,7 @@ __global__ void k_scatter_runs(int64_t nseg, const int64_t* __restrict__ seg_run
 // whose residue mod 8 is unused in its quarter, preferring its most plentiful
 // residue; failing that, one free mod 8 only; failing that, its most plentiful.
 // Thread per half warp; tmp holds the lanes' entries bucketed by residue.
-__global__ void k_slice_schedule(int64_t nslices, const int64_t* __restrict__ slice_off, uint16_t* __restrict__ col,
+__global__ void k_slice_schedule(int64_t nslices, int kC, const int64_t* __restrict__ slice_off, uint16_t* __restrict__ col,
                                  float* __restrict__ w, uint16_t* __restrict__ tcol, float* __restrict__ tw) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nslices * 2;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -354,14 +375,14 @@ __global__ void k_flag_sparse(int64_t nseg, const int64_t* __restrict__ seg_star
 
 // residual entry -> (global row key, payload with global column)
 __global__ void k_residual_keys(int64_t m, const uint32_t* __restrict__ key, const uint64_t* __restrict__ pay, int bb,
-                                int kR, uint32_t* __restrict__ rkey, uint64_t* __restrict__ rpay) {
+                                int kR, int cb, uint32_t* __restrict__ rkey, uint64_t* __restrict__ rpay) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t kk = key[k];
     const uint64_t p = pay[k];
     const uint32_t tile = kk >> bb, blk = kk & ((1u << bb) - 1);
-    const uint32_t rowl = (uint32_t)p >> kCbits, coll = (uint32_t)p & (kC - 1);
+    const uint32_t rowl = (uint32_t)p >> cb, coll = (uint32_t)p & ((1u << cb) - 1);
     rkey[k] = tile * (uint32_t)kR + rowl;
-    rpay[k] = (p & 0xffffffff00000000ULL) | (uint64_t)(blk * (uint32_t)kC + coll);
+    rpay[k] = (p & 0xffffffff00000000ULL) | (uint64_t)((blk << cb) + coll);
   }
 }
 
@@ -421,7 +442,7 @@ __global__ void k_bmt_tile_ptr(int64_t nseg, const uint32_t* __restrict__ seg_ti
 // estimated cost of a tile for the persistent scheduler: stored slots (6 B
 // each), one staged block per dense segment, residual entries (gathered from
 // L2) and the per-row epilogue
-__global__ void k_tile_cost(int64_t ntiles, int kR, int64_t n, const int64_t* __restrict__ tile_seg,
+__global__ void k_tile_cost(int64_t ntiles, int kR, int kC, int64_t n, const int64_t* __restrict__ tile_seg,
                             const int64_t* __restrict__ seg_slice, const int64_t* __restrict__ slice_off,
                             const int64_t* __restrict__ res_rowptr, int64_t* __restrict__ cost) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
@@ -429,13 +450,14 @@ __global__ void k_tile_cost(int64_t ntiles, int kR, int64_t n, const int64_t* __
     const int64_t slots = slice_off[seg_slice[s1]] - slice_off[seg_slice[s0]];
     const int64_t r0 = t * kR, r1 = min(n, r0 + kR);
     const int64_t res = res_rowptr[r1] - res_rowptr[r0];
-    cost[t] = 6 * slots + 32768 * (s1 - s0) + 32 * res + 16 * (r1 - r0);
+    cost[t] = 6 * slots + 8 * (int64_t)kC * (s1 - s0) + 32 * res + 16 * (r1 - r0);
   }
 }
 
 struct BmtArgs {
   int64_t ncols;
   int tile_rows;
+  int kC;               // columns per staged block
   const uint8_t* data;  // 768-byte step records (k_interleave)
   const uint8_t* wide;  // rows finished by the row kernel instead
   const int64_t* res_rowptr;  // [n + 1] residual (sparse-block) entries per row
@@ -460,54 +482,48 @@ __device__ __forceinline__ uint2 ld_stream_v2u32(const void* p, uint64_t pol) {
   return r;
 }
 
-template <int FIN, bool STAGED>
-__device__ __forceinline__ void gather_fma(float (&acc)[FIN], float w, int c, const float* zs, const float* zg,
-                                           uint64_t pol_z) {
-  if constexpr (STAGED) {
-    const float* zp = zs + c * FIN;  // c >= kC hits a zero row
-    if constexpr (FIN == 4) {
-      const float4 q = *reinterpret_cast<const float4*>(zp);
-      acc[0] = fmaf(w, q.x, acc[0]); acc[1] = fmaf(w, q.y, acc[1]);
-      acc[2] = fmaf(w, q.z, acc[2]); acc[3] = fmaf(w, q.w, acc[3]);
-    } else if constexpr (FIN == 2) {
-      const float2 q = *reinterpret_cast<const float2*>(zp);
-      acc[0] = fmaf(w, q.x, acc[0]); acc[1] = fmaf(w, q.y, acc[1]);
-    } else {
-      acc[0] = fmaf(w, zp[0], acc[0]);
-    }
+// entry (c, w) of a run: acc += w * z_c from the staged block (c >= kC hits a zero row)
+template <int FIN>
+__device__ __forceinline__ void gather_fma(float (&acc)[FIN], float w, int c, const float* zs) {
+  const float* zp = zs + c * FIN;
+  if constexpr (FIN == 4) {
+    const float4 q = *reinterpret_cast<const float4*>(zp);
+    acc[0] = fmaf(w, q.x, acc[0]); acc[1] = fmaf(w, q.y, acc[1]);
+    acc[2] = fmaf(w, q.z, acc[2]); acc[3] = fmaf(w, q.w, acc[3]);
+  } else if constexpr (FIN == 2) {
+    const float2 q = *reinterpret_cast<const float2*>(zp);
+    acc[0] = fmaf(w, q.x, acc[0]); acc[1] = fmaf(w, q.y, acc[1]);
   } else {
-    if (c < kC) {  // padding slots skip the gather
-      const VecF<FIN> q = ld_z<FIN>(zg + (int64_t)c * FIN, pol_z);
-#pragma unroll
-      for (int f = 0; f < FIN; ++f) acc[f] = fmaf(w, q.v[f], acc[f]);
-    }
+    acc[0] = fmaf(w, zp[0], acc[0]);
   }
 }
 
-// one slice: lane = one row's run, summed in its (conflict-scheduled) order
-// PF: steps of matrix records kept in flight per lane by an explicit software
-// pipeline (0: plain unrolled loop).  Measured on B200 (tools/ab: c3 / c4):
-// long runs (2048-row tiles) gain at F <= 2 with 3 (F = 4 spills and loses),
-// short runs (taller tiles, 1 CTA per SM) gain with 2.
-template <int FIN, int kThreads>
-__host__ __device__ constexpr int bmt_pf() {
-  return kThreads == 512 ? (FIN == 4 ? 0 : 3) : 2;
+// Record stream of one warp.  Step k of the stream is the 768-byte record at
+// base + k * 768: lane l reads its 4 columns (u16) at +8l and its 4 weights at
+// +256+16l.  D records are kept in flight by a software pipeline written so the
+// compiler needs no register copies: step k's registers are consumed (gathers
+// issued, FMAs issued) BEFORE the load of step k + D is issued into the same
+// registers.  (The first version issued the reload first; nvcc then renamed
+// the destination and copied it back at the loop end, which waited on the
+// load just issued -- one full memory latency per unrolled iteration, a third
+// of all stall samples in profiles/r02_base_c3.)
+template <int FIN>
+__device__ __forceinline__ void step_fma(float (&acc)[FIN], uint2 cv, float4 wv, const float* zs) {
+  gather_fma<FIN>(acc, wv.x, (int)(cv.x & 0xffffu), zs);
+  gather_fma<FIN>(acc, wv.y, (int)(cv.x >> 16), zs);
+  gather_fma<FIN>(acc, wv.z, (int)(cv.y & 0xffffu), zs);
+  gather_fma<FIN>(acc, wv.w, (int)(cv.y >> 16), zs);
 }
 
-template <int FIN, int PF>
-__device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int64_t steps, int row, const float* zs,
+// one slice (dynamic mode): lane = one row's run, summed in its (conflict-scheduled) order
+template <int FIN, int D>
+__device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int steps, int row, const float* zs,
                                           float* accs, int lane, uint64_t pol_s) {
   float acc[FIN];
 #pragma unroll
   for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
-  const uint8_t* rec = b.data + (off / 128) * 768;
-  const uint8_t* cp = rec + 8 * lane;
-  const uint8_t* wp = rec + 256 + 16 * lane;
-if constexpr (PF > 0) {
-  // software pipeline: the record of step k + D is requested as soon as step k's
-  // registers are consumed, so D steps of loads are always in flight (a plain
-  // unrolled loop restarts its loads every unroll block and exposes the latency)
-  constexpr int D = PF;
+  const uint8_t* cp = b.data + (off / 128) * 768 + 8 * lane;
+  const uint8_t* wp = cp + 256 + 8 * lane;
   uint2 cq[D];
   float4 wq[D];
 #pragma unroll
@@ -516,34 +532,34 @@ if constexpr (PF > 0) {
       cq[d] = ld_stream_v2u32(cp + d * 768, pol_s);
       wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + d * 768), pol_s);
     }
-  for (int64_t k = 0; k < steps; k += D) {
+  int rem = steps;
+  // steady state: D steps consumed, D reloaded, no predicates
+  while (rem >= 2 * D) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const uint2 cv = cq[d];
-      const float4 wv = wq[d];
-      if (k + d + D < steps) {
-        cq[d] = ld_stream_v2u32(cp + (k + d + D) * 768, pol_s);
-        wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + (k + d + D) * 768), pol_s);
-      }
-      if (k + d < steps) {
-        gather_fma<FIN, true>(acc, wv.x, (int)(cv.x & 0xffff), zs, nullptr, 0);
-        gather_fma<FIN, true>(acc, wv.y, (int)(cv.x >> 16), zs, nullptr, 0);
-        gather_fma<FIN, true>(acc, wv.z, (int)(cv.y & 0xffff), zs, nullptr, 0);
-        gather_fma<FIN, true>(acc, wv.w, (int)(cv.y >> 16), zs, nullptr, 0);
+      step_fma<FIN>(acc, cq[d], wq[d], zs);
+      cq[d] = ld_stream_v2u32(cp + (d + D) * 768, pol_s);
+      wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + (d + D) * 768), pol_s);
+    }
+    cp += D * 768;
+    wp += D * 768;
+    rem -= D;
+  }
+  // tail: fewer than 2D steps left
+  if (rem > D) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      step_fma<FIN>(acc, cq[d], wq[d], zs);
+      if (d + D < rem) {
+        cq[d] = ld_stream_v2u32(cp + (d + D) * 768, pol_s);
+        wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + (d + D) * 768), pol_s);
       }
     }
+    rem -= D;
   }
-} else {
-#pragma unroll 4
-  for (int64_t k = 0; k < steps; ++k) {
-    const uint2 cv = ld_stream_v2u32(cp + k * 768, pol_s);
-    const float4 wv = ld_stream_v4f32(reinterpret_cast<const float*>(wp + k * 768), pol_s);
-    gather_fma<FIN, true>(acc, wv.x, (int)(cv.x & 0xffff), zs, nullptr, 0);
-    gather_fma<FIN, true>(acc, wv.y, (int)(cv.x >> 16), zs, nullptr, 0);
-    gather_fma<FIN, true>(acc, wv.z, (int)(cv.y & 0xffff), zs, nullptr, 0);
-    gather_fma<FIN, true>(acc, wv.w, (int)(cv.y >> 16), zs, nullptr, 0);
-  }
-}
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+    if (d < rem) step_fma<FIN>(acc, cq[d], wq[d], zs);
   if (row != 0xffff) {
 #pragma unroll
     for (int f = 0; f < FIN; ++f) accs[row * FIN + f] += acc[f];
@@ -552,7 +568,7 @@ if constexpr (PF > 0) {
 
 // the slices of segment s: warps take them dynamically from *ctr (slices touch
 // distinct rows, so the assignment never changes a result)
-template <int FIN, int PF>
+template <int FIN, int D>
 __device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, const float* zs, float* accs, int* ctr,
                                                int lane, uint64_t pol_s) {
   const int64_t sl0 = b.seg_slice[s];
@@ -581,7 +597,7 @@ __device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, cons
       end_n = b.slice_off[sl0 + jn + 1];
       row_n = b.slice_rows[(sl0 + jn) * 32 + lane];
     }
-    run_slice<FIN, PF>(b, off, (end - off) / 128, row, zs, accs, lane, pol_s);
+    run_slice<FIN, D>(b, off, (int)((end - off) / 128), row, zs, accs, lane, pol_s);
     j = jn;
     off = off_n;
     end = end_n;
@@ -589,11 +605,12 @@ __device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, cons
   }
 }
 
-// the slices of segment s as ONE record stream per warp: the warp owns a
-// contiguous range of slices (static split, balanced by steps), so its loads
-// run ahead across slice boundaries; at a boundary each lane adds its run to
-// its row's accumulator and switches row (boundaries are warp-uniform)
-template <int FIN, int PF, int NW>
+// the slices of segment s as ONE record stream per warp (stream mode): the
+// warp owns a contiguous range of slices (static split balanced by steps,
+// k_warp_split), so its loads run ahead across slice boundaries; at a
+// boundary each lane adds its run to its row's accumulator and switches row
+// (boundaries are warp-uniform)
+template <int FIN, int D, int NW>
 __device__ __forceinline__ void segment_stream(const BmtArgs& b, int64_t s, const float* zs, float* accs, int warp,
                                                int lane, uint64_t pol_s) {
   const int64_t sl0 = b.seg_slice[s];
@@ -602,22 +619,20 @@ __device__ __forceinline__ void segment_stream(const BmtArgs& b, int64_t s, cons
   const int64_t j1 = sl0 + sp[warp + 1];
   if (j >= j1) return;
   const int64_t off0 = b.slice_off[j];
-  const int64_t total = (b.slice_off[j1] - off0) / 128;
-  const uint8_t* rec = b.data + (off0 / 128) * 768;
-  const uint8_t* cp = rec + 8 * lane;
-  const uint8_t* wp = rec + 256 + 16 * lane;
-  int64_t bound = (b.slice_off[j + 1] - off0) / 128;
+  const int total = (int)((b.slice_off[j1] - off0) / 128);
+  const uint8_t* cp = b.data + (off0 / 128) * 768 + 8 * lane;
+  const uint8_t* wp = cp + 256 + 8 * lane;
+  // slice boundaries (in steps from the stream start) and rows, one slice ahead
+  int bound = (int)((b.slice_off[j + 1] - off0) / 128);
   int row = b.slice_rows[j * 32 + lane];
-  int64_t bound_n = total;
-  int row_n = 0xffff;
+  int bound_n = total, row_n = 0xffff;
   if (j + 1 < j1) {
-    bound_n = (b.slice_off[j + 2] - off0) / 128;
+    bound_n = (int)((b.slice_off[j + 2] - off0) / 128);
     row_n = b.slice_rows[(j + 1) * 32 + lane];
   }
   float acc[FIN];
 #pragma unroll
   for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
-  constexpr int D = PF > 0 ? PF : 2;
   uint2 cq[D];
   float4 wq[D];
 #pragma unroll
@@ -626,38 +641,56 @@ __device__ __forceinline__ void segment_stream(const BmtArgs& b, int64_t s, cons
       cq[d] = ld_stream_v2u32(cp + d * 768, pol_s);
       wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + d * 768), pol_s);
     }
-  for (int64_t k = 0; k < total; k += D) {
+  auto boundary = [&](int k) {
+    if (k + 1 == bound) {  // end of this slice (same step for every lane)
+      if (row != 0xffff) {
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const uint2 cv = cq[d];
-      const float4 wv = wq[d];
-      if (k + d + D < total) {
-        cq[d] = ld_stream_v2u32(cp + (k + d + D) * 768, pol_s);
-        wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + (k + d + D) * 768), pol_s);
+        for (int f = 0; f < FIN; ++f) accs[row * FIN + f] += acc[f];
       }
-      if (k + d < total) {
-        gather_fma<FIN, true>(acc, wv.x, (int)(cv.x & 0xffff), zs, nullptr, 0);
-        gather_fma<FIN, true>(acc, wv.y, (int)(cv.x >> 16), zs, nullptr, 0);
-        gather_fma<FIN, true>(acc, wv.z, (int)(cv.y & 0xffff), zs, nullptr, 0);
-        gather_fma<FIN, true>(acc, wv.w, (int)(cv.y >> 16), zs, nullptr, 0);
-        if (k + d + 1 == bound) {  // end of this slice (same step for every lane)
-          if (row != 0xffff) {
 #pragma unroll
-            for (int f = 0; f < FIN; ++f) accs[row * FIN + f] += acc[f];
-          }
-#pragma unroll
-          for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
-          ++j;
-          row = row_n;
-          bound = bound_n;
-          if (j + 1 < j1) {
-            bound_n = (b.slice_off[j + 2] - off0) / 128;
-            row_n = b.slice_rows[(j + 1) * 32 + lane];
-          }
-        }
+      for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
+      ++j;
+      row = row_n;
+      bound = bound_n;
+      if (j + 1 < j1) {
+        bound_n = (int)((b.slice_off[j + 2] - off0) / 128);
+        row_n = b.slice_rows[(j + 1) * 32 + lane];
       }
     }
+  };
+  int k = 0;
+  while (k + 2 * D <= total) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      step_fma<FIN>(acc, cq[d], wq[d], zs);
+      cq[d] = ld_stream_v2u32(cp + (d + D) * 768, pol_s);
+      wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + (d + D) * 768), pol_s);
+      boundary(k + d);
+    }
+    cp += D * 768;
+    wp += D * 768;
+    k += D;
   }
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    if (k + d < total) {
+      step_fma<FIN>(acc, cq[d], wq[d], zs);
+      if (k + d + D < total) {
+        cq[d] = ld_stream_v2u32(cp + (d + D) * 768, pol_s);
+        wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + (d + D) * 768), pol_s);
+      }
+      boundary(k + d);
+    }
+  }
+  k += D;
+  cp += D * 768;
+  wp += D * 768;
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+    if (k + d < total) {
+      step_fma<FIN>(acc, cq[d], wq[d], zs);
+      boundary(k + d);
+    }
 }
 
 // after the segments: residual entries, then the fused row epilogue
@@ -707,6 +740,7 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
                                          uint64_t pol_s, uint64_t pol_z) {
   extern __shared__ float4 smem_f4[];
   __shared__ int slice_ctr;
+  const int kC = b.kC;
   float* zs = reinterpret_cast<float*>(smem_f4);  // [(kC + kPadRows) * FIN], rows >= kC stay zero
   float* accs = zs + (kC + kPadRows) * FIN;         // [kR * FIN]
   const int64_t r0 = tile * kR;
@@ -731,9 +765,9 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
     if (tid == 0) slice_ctr = 0;
     __syncthreads();
 #if GIFT_BMT_STREAM
-    segment_stream<FIN, bmt_pf<FIN, kThreads>(), kThreads / 32>(b, s, zs, accs, tid >> 5, lane, pol_s);
+    segment_stream<FIN, bmt_depth<FIN>(), kThreads / 32>(b, s, zs, accs, tid >> 5, lane, pol_s);
 #else
-    segment_slices<FIN, bmt_pf<FIN, kThreads>()>(b, s, zs, accs, &slice_ctr, lane, pol_s);
+    segment_slices<FIN, bmt_depth<FIN>()>(b, s, zs, accs, &slice_ctr, lane, pol_s);
 #endif
   }
   bmt_tile_finish<FIN, FOUT, kThreads>(a, b, r0, nrows, accs, tid, lane, pol_z);
@@ -744,8 +778,8 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
 template <int FIN, int kThreads>
 __device__ __forceinline__ void stage_async(const HopArgs& a, const BmtArgs& b, int64_t s, float* zs, int tid,
                                             uint64_t pol) {
-  const int64_t cbase = (int64_t)b.seg_code[s] * kC;
-  const int64_t cend = min(cbase + kC, b.ncols);
+  const int64_t cbase = (int64_t)b.seg_code[s] * b.kC;
+  const int64_t cend = min(cbase + b.kC, b.ncols);
   const int nf = (int)((cend - cbase) * FIN);
   const int nv = nf / 4;
   const float* zg = a.zin + cbase * FIN;
@@ -765,7 +799,8 @@ __device__ __forceinline__ void bmt_tile_db(const HopArgs& a, const BmtArgs& b, 
                                             int lane, uint64_t pol_s, uint64_t pol_z) {
   extern __shared__ float4 smem_f4[];
   __shared__ int slice_ctr2[2];
-  constexpr int zrows = (kC + kPadRows) * FIN;
+  const int kC = b.kC;
+  const int zrows = (kC + kPadRows) * FIN;
   float* zs0 = reinterpret_cast<float*>(smem_f4);
   float* zs1 = zs0 + zrows;
   float* accs = zs1 + zrows;  // [kR * FIN]
@@ -790,10 +825,9 @@ __device__ __forceinline__ void bmt_tile_db(const HopArgs& a, const BmtArgs& b, 
       if (tid == 0) slice_ctr2[buf ^ 1] = 0;
     }
 #if GIFT_BMT_STREAM
-    segment_stream<FIN, bmt_pf<FIN, kThreads>(), kThreads / 32>(b, s, buf ? zs1 : zs0, accs, tid >> 5, lane,
-                                                                pol_s);
+    segment_stream<FIN, bmt_depth<FIN>(), kThreads / 32>(b, s, buf ? zs1 : zs0, accs, tid >> 5, lane, pol_s);
 #else
-    segment_slices<FIN, bmt_pf<FIN, kThreads>()>(b, s, buf ? zs1 : zs0, accs, &slice_ctr2[buf], lane, pol_s);
+    segment_slices<FIN, bmt_depth<FIN>()>(b, s, buf ? zs1 : zs0, accs, &slice_ctr2[buf], lane, pol_s);
 #endif
   }
   bmt_tile_finish<FIN, FOUT, kThreads>(a, b, r0, nrows, accs, tid, lane, pol_z);
@@ -842,9 +876,137 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a
   }
 }
 
-size_t bmt_smem(int fin, int kR) { return (size_t)(kC + kPadRows) * fin * 4 + (size_t)kR * fin * 4; }
+// ---------------------------------------------------------------------------
+// Barrier-free segment pipeline (default where it fits in shared memory).
+//
+// The kernels above end every segment with a CTA barrier: the next block is
+// staged into the buffer the slowest warp may still read, and two segments of
+// a tile may touch the same row's accumulator.  ncu (profiles/r02_base_c3)
+// put 18 % of the F = 2 pass's stall samples on that barrier.  Here:
+//   * two signal buffers, filled by one bulk async copy each
+//     (cp.async.bulk global -> shared, completion on an mbarrier);
+//   * two accumulator banks: segment i adds into bank i % 2;
+//   * a warp that finishes segment i bumps done[i % 2]; the LAST warp to do so
+//     (every warp has left segment i, so nobody reads buffer i % 2 or adds to
+//     bank i % 2 any more) issues the copy of segment i + 2 into that buffer.
+// A warp may thus run one segment ahead of the slowest warp; it waits only if
+// it gets two ahead.  A row's sum is (bank 0 + bank 1) + residual: fixed
+// order, so the result stays deterministic (it is a different, equally valid
+// fp32 association than the single-bank kernels).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-size_t bmt_smem_db(int fin, int kR) { return bmt_smem(fin, kR) + (size_t)(kC + kPadRows) * fin * 4; }
+__device__ __forceinline__ void mbar_init(uint64_t* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(m)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* m, unsigned bytes) {
+  uint64_t state;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+               : "=l"(state)
+               : "r"(smem_addr(m)), "r"(bytes)
+               : "memory");
+  (void)state;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_addr(m)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+// segment s's signal block -> dst: one bulk copy of the 16-byte-aligned part,
+// the ragged tail (last block of an odd-sized signal) by this thread's own
+// stores, which the arrive (release) publishes together with the copy
+template <int FIN>
+__device__ __forceinline__ void stage_bulk(const HopArgs& a, const BmtArgs& b, int64_t s, float* dst, uint64_t* full,
+                                           uint64_t pol) {
+  const int64_t cbase = (int64_t)b.seg_code[s] * b.kC;
+  const int64_t cend = min(cbase + b.kC, b.ncols);
+  const unsigned nf = (unsigned)((cend - cbase) * FIN);
+  const unsigned bytes = (nf * 4u) & ~15u;
+  const float* src = a.zin + cbase * FIN;
+  for (unsigned i = bytes / 4; i < nf; ++i) dst[i] = src[i];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of dst before the async write
+  mbar_arrive_expect_tx(full, bytes);
+  if (bytes)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(full)), "l"(pol)
+        : "memory");
+}
+
+template <int FIN, int FOUT, int kThreads>
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt_nb(HopArgs a, BmtArgs b) {
+  extern __shared__ float4 smem_f4[];
+  __shared__ uint64_t full[2];
+  __shared__ int slice_ctr[2];
+  __shared__ int done[2];
+  constexpr int NW = kThreads / 32;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int kR = b.tile_rows, kC = b.kC;
+  const uint64_t pol_s = policy_evict_first();
+  const uint64_t pol_z = policy_evict_last();
+  const int zrows = (kC + kPadRows) * FIN;
+  float* zs[2];
+  zs[0] = reinterpret_cast<float*>(smem_f4);
+  zs[1] = zs[0] + zrows;
+  float* acc[2];
+  acc[0] = zs[1] + zrows;
+  acc[1] = acc[0] + kR * FIN;
+  const int64_t tile = b.tile_order ? b.tile_order[blockIdx.x] : blockIdx.x;
+  const int64_t r0 = tile * kR;
+  const int nrows = (int)min((int64_t)kR, a.n - r0);
+  for (int i = tid; i < nrows * FIN; i += kThreads) {
+    acc[0][i] = 0.f;
+    acc[1][i] = 0.f;
+  }
+  for (int i = kC * FIN + tid; i < zrows; i += kThreads) {  // zero padding rows of both buffers
+    zs[0][i] = 0.f;
+    zs[1][i] = 0.f;
+  }
+  const int64_t s0 = b.tile_seg[tile];
+  const int nseg = (int)(b.tile_seg[tile + 1] - s0);
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    slice_ctr[0] = slice_ctr[1] = 0;
+    done[0] = done[1] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int i = 0; i < 2 && i < nseg; ++i) stage_bulk<FIN>(a, b, s0 + i, zs[i], &full[i], pol_z);
+  for (int i = 0; i < nseg; ++i) {
+    const int buf = i & 1;
+    mbar_wait(&full[buf], (unsigned)(i >> 1) & 1u);
+    segment_slices<FIN, bmt_depth<FIN>()>(b, s0 + i, zs[buf], acc[buf], &slice_ctr[buf], lane, pol_s);
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&done[buf], 1) == NW - 1) {  // every warp has left segment i
+        __threadfence_block();
+        done[buf] = 0;
+        slice_ctr[buf] = 0;
+        if (i + 2 < nseg) stage_bulk<FIN>(a, b, s0 + i + 2, zs[buf], &full[buf], pol_z);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < nrows * FIN; i += kThreads) acc[0][i] += acc[1][i];
+  bmt_tile_finish<FIN, FOUT, kThreads>(a, b, r0, nrows, acc[0], tid, lane, pol_z);
+}
+
+size_t bmt_smem_nb(int fin, int kR, int kC) { return 2 * ((size_t)(kC + kPadRows) * fin * 4 + (size_t)kR * fin * 4); }
+
+size_t bmt_smem(int fin, int kR, int kC) { return (size_t)(kC + kPadRows) * fin * 4 + (size_t)kR * fin * 4; }
+
+size_t bmt_smem_db(int fin, int kR, int kC) { return bmt_smem(fin, kR, kC) + (size_t)(kC + kPadRows) * fin * 4; }
 
 template <int FIN, int FOUT, bool DB>
 void launch_bmt_k(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, int tpb, size_t smem) {
@@ -874,13 +1036,44 @@ void launch_bmt_k(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, 
   GIFT_LAUNCH_CHECK(ctx);
 }
 
+template <int FIN, int FOUT, int kThreads>
+void launch_bmt_nb(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, size_t smem) {
+  auto kern = k_hop_bmt_nb<FIN, FOUT, kThreads>;
+  static std::once_flag once;
+  std::call_once(once, [&]() {
+    int optin = 0;
+    GIFT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    cudaFuncAttributes fa{};
+    GIFT_CUDA(cudaFuncGetAttributes(&fa, kern));
+    GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+  });
+  kern<<<(unsigned)ntiles, kThreads, smem, ctx->stream>>>(a, b);
+  GIFT_LAUNCH_CHECK(ctx);
+}
+
 template <int FIN, int FOUT>
 void launch_bmt(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles) {
+  // barrier-free pipeline where it keeps the barrier kernel's occupancy:
+  // 2 CTAs x 512 threads per SM for 2048-row tiles, 1 x 1024 for taller ones
+  // (A/B on B200: c4 F=2 pass 1.83 -> 1.63 ms at 1 x 1024; c3 F=4 pass 1.16 ->
+  // 1.25 ms when its 197 KB footprint drops it from 2 x 512 to 1 x 1024).  The
+  // bulk copies need a 16-byte aligned signal.
+  if (env_int("GIFT_BMT_NB", 1) && !b.ctr && ((uintptr_t)a.zin & 15) == 0) {
+    const size_t nb = bmt_smem_nb(FIN, b.tile_rows, b.kC), fixed = 3 * 1024;
+    if (b.tile_rows <= 2048 && 2 * (nb + fixed) <= 228 * 1024) {
+      launch_bmt_nb<FIN, FOUT, 512>(ctx, a, b, ntiles, nb);
+      return;
+    }
+    if (b.tile_rows > 2048 && nb + fixed <= 228 * 1024) {
+      launch_bmt_nb<FIN, FOUT, 1024>(ctx, a, b, ntiles, nb);
+      return;
+    }
+  }
   // 2048-row tiles: 2 CTAs x 512 threads per SM; taller tiles: 1 CTA x 1024.
   // Double-buffered staging when both buffers fit at that occupancy.
   const int tpb = b.tile_rows > 2048 ? 1024 : 512;
   const int per_sm = tpb == 512 ? 2 : 1;
-  const size_t smem1 = bmt_smem(FIN, b.tile_rows), smem2 = bmt_smem_db(FIN, b.tile_rows);
+  const size_t smem1 = bmt_smem(FIN, b.tile_rows, b.kC), smem2 = bmt_smem_db(FIN, b.tile_rows, b.kC);
   const bool db = env_int("GIFT_BMT_DB", 1) && ((uintptr_t)a.zin & 15) == 0 &&
                   (size_t)per_sm * (smem2 + 3 * 1024) <= 228 * 1024;
   if (db)
@@ -929,7 +1122,8 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   Csr::Bmt& B = c->bmt;
   cudaStream_t st = ctx->stream;
   const int64_t n = c->n, nnz_all = c->nnz;
-  const int kR = tile_rows_for(c->mean_row);
+  const BmtShape shape = bmt_shape_for(c->mean_row);
+  const int kR = shape.kR, cb = shape.cb, kC = 1 << cb;
   const int64_t ntiles = (n + kR - 1) / kR;
   const int64_t nblocks = (n + kC - 1) / kC;
   const int bb = bit_length((uint64_t)(nblocks > 1 ? nblocks - 1 : 1));
@@ -943,7 +1137,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
     DevBuf<unsigned long long> wc(ctx, 3);
     GIFT_CUDA(cudaMemsetAsync(wc.p, 0, 3 * sizeof(unsigned long long), st));
     DevBuf<uint16_t> nb(ctx, n);
-    k_row_nblocks<<<grid_for(n, kBlock), kBlock, 0, st>>>(n, c->indptr, c->indices, nb.p, wc.p + 2);
+    k_row_nblocks<<<grid_for(n, kBlock), kBlock, 0, st>>>(n, c->indptr, c->indices, cb, nb.p, wc.p + 2);
     GIFT_LAUNCH_CHECK(ctx);
     const double mean_nb = (double)fetch(ctx, wc.p + 2) / (double)(n > 0 ? n : 1);
     const int limit = std::max(kWide, (int)(3.0 * mean_nb + 0.5));
@@ -985,7 +1179,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   {
     DevBuf<uint32_t> key(ctx, nnz_all);
     DevBuf<uint64_t> pay(ctx, nnz_all);
-    k_bmt_keys<<<grid_for(nnz_all, kBlock), kBlock, 0, st>>>(nnz_all, row_of.p, c->indices, w32, bb, kR, B.wide, sentinel,
+    k_bmt_keys<<<grid_for(nnz_all, kBlock), kBlock, 0, st>>>(nnz_all, row_of.p, c->indices, w32, bb, kR, cb, B.wide, sentinel,
                                                              key.p, pay.p);
     GIFT_LAUNCH_CHECK(ctx);
     row_of.reset();
@@ -1005,7 +1199,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
     DevBuf<unsigned long long> cnt0(ctx, 2);
     DevBuf<int64_t> nsel0(ctx, 2);
     GIFT_CUDA(cudaMemsetAsync(cnt0.p, 0, 2 * sizeof(unsigned long long), st));
-    k_bmt_heads<<<grid_for(nnz, kBlock), kBlock, 0, st>>>(nnz, key_s.p, pay_s.p, seg_head.p, run_head.p, cnt0.p);
+    k_bmt_heads<<<grid_for(nnz, kBlock), kBlock, 0, st>>>(nnz, cb, key_s.p, pay_s.p, seg_head.p, run_head.p, cnt0.p);
     GIFT_LAUNCH_CHECK(ctx);
     const int64_t nseg0 = (int64_t)fetch(ctx, cnt0.p);
     DevBuf<int64_t> seg0(ctx, nseg0 + 1);
@@ -1034,7 +1228,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
     if (nres > 0) {
       DevBuf<uint32_t> rkey(ctx, nres), rkey_s2(ctx, nres);
       DevBuf<uint64_t> rpay(ctx, nres), rpay_s2(ctx, nres);
-      k_residual_keys<<<grid_for(nres, kBlock), kBlock, 0, st>>>(nres, rk.p, rp.p, bb, kR, rkey.p, rpay.p);
+      k_residual_keys<<<grid_for(nres, kBlock), kBlock, 0, st>>>(nres, rk.p, rp.p, bb, kR, cb, rkey.p, rpay.p);
       GIFT_LAUNCH_CHECK(ctx);
       const int row_bits = bit_length((uint64_t)(n > 1 ? n - 1 : 1));
       GIFT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, rkey.p, rkey_s2.p, rpay.p, rpay_s2.p, nres, 0,
@@ -1075,7 +1269,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   {
     DevBuf<uint8_t> seg_head(ctx, nnz), run_head(ctx, nnz);
     GIFT_CUDA(cudaMemsetAsync(counts.p, 0, 2 * sizeof(unsigned long long), st));
-    k_bmt_heads<<<grid_for(nnz, kBlock), kBlock, 0, st>>>(nnz, key_s.p, pay_s.p, seg_head.p, run_head.p, counts.p);
+    k_bmt_heads<<<grid_for(nnz, kBlock), kBlock, 0, st>>>(nnz, cb, key_s.p, pay_s.p, seg_head.p, run_head.p, counts.p);
     GIFT_LAUNCH_CHECK(ctx);
     unsigned long long h[2];
     GIFT_CUDA(cudaMemcpyAsync(h, counts.p, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -1094,11 +1288,11 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   {
     DevBuf<uint64_t> rkey(ctx, nruns);
     DevBuf<int64_t> iota(ctx, nruns);
-    k_run_keys<<<grid_for(nruns, kBlock), kBlock, 0, st>>>(nruns, run_start.p, nnz, seg_start.p, nseg, rkey.p);
+    k_run_keys<<<grid_for(nruns, kBlock), kBlock, 0, st>>>(nruns, run_start.p, nnz, seg_start.p, nseg, cb, rkey.p);
     GIFT_LAUNCH_CHECK(ctx);
     k_iota64<<<grid_for(nruns, kBlock), kBlock, 0, st>>>(nruns, iota.p);
     GIFT_LAUNCH_CHECK(ctx);
-    const int rbits = 13 + bit_length((uint64_t)nseg);
+    const int rbits = cb + 1 + bit_length((uint64_t)nseg);
     size_t bytes = 0;
     GIFT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, rkey.p, rkey_s.p, iota.p, run_perm.p, nruns, 0, rbits,
                                               st));
@@ -1109,7 +1303,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   }
   // 5. slices: ceil(runs / 32) per segment; slots from each slice's longest run
   DevBuf<int64_t> seg_run(ctx, nseg + 1), nsl(ctx, nseg + 1);
-  k_seg_runs<<<grid_for(nruns + 1, kBlock), kBlock, 0, st>>>(nruns, rkey_s.p, nseg, seg_run.p);
+  k_seg_runs<<<grid_for(nruns + 1, kBlock), kBlock, 0, st>>>(nruns, rkey_s.p, nseg, cb, seg_run.p);
   GIFT_LAUNCH_CHECK(ctx);
   k_seg_slices<<<grid_for(nseg, kBlock), kBlock, 0, st>>>(nseg, seg_run.p, nsl.p);
   GIFT_LAUNCH_CHECK(ctx);
@@ -1119,7 +1313,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   const int64_t nslices = fetch(ctx, B.seg_slice + nseg);
   DevBuf<int64_t> slots(ctx, nslices + 1);
   GIFT_CUDA(cudaMemsetAsync(slots.p + nslices, 0, sizeof(int64_t), st));
-  k_slice_len<<<grid_for(nseg, kBlock), kBlock, 0, st>>>(nseg, seg_run.p, B.seg_slice, rkey_s.p, slots.p);
+  k_slice_len<<<grid_for(nseg, kBlock), kBlock, 0, st>>>(nseg, seg_run.p, B.seg_slice, rkey_s.p, cb, slots.p);
   GIFT_LAUNCH_CHECK(ctx);
   B.slice_off = static_cast<int64_t*>(csr_alloc(ctx, c, (nslices + 1) * sizeof(int64_t)));
   exclusive_sum(ctx, slots.p, B.slice_off, nslices + 1);
@@ -1143,13 +1337,13 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   GIFT_LAUNCH_CHECK(ctx);
   GIFT_CUDA(cudaMemsetAsync(bw, 0, total * sizeof(float), st));
   k_scatter_runs<<<(unsigned)std::min<int64_t>(nseg, 65535), 256, 0, st>>>(
-      nseg, seg_run.p, B.seg_slice, run_perm.p, run_start.p, nruns, nnz, pay_s.p, B.slice_off, B.slice_rows, bcol,
+      nseg, seg_run.p, B.seg_slice, run_perm.p, run_start.p, nruns, nnz, cb, pay_s.p, B.slice_off, B.slice_rows, bcol,
       bw);
   GIFT_LAUNCH_CHECK(ctx);
   if (env_int("GIFT_BMT_SCHEDULE", 1)) {
     DevBuf<uint16_t> tcol(ctx, total + 8);
     DevBuf<float> tw(ctx, total + 8);
-    k_slice_schedule<<<grid_for(nslices * 2, 128, 1LL << 30), 128, 0, st>>>(nslices, B.slice_off, bcol, bw, tcol.p,
+    k_slice_schedule<<<grid_for(nslices * 2, 128, 1LL << 30), 128, 0, st>>>(nslices, kC, B.slice_off, bcol, bw, tcol.p,
                                                                            tw.p);
     GIFT_LAUNCH_CHECK(ctx);
   }
@@ -1170,7 +1364,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   B.tile_order = static_cast<int32_t*>(csr_alloc(ctx, c, (ntiles + 1) * sizeof(int32_t)));
   {
     DevBuf<int64_t> cost(ctx, ntiles);
-    k_tile_cost<<<grid_for(ntiles, kBlock), kBlock, 0, st>>>(ntiles, kR, n, B.tile_seg, B.seg_slice, B.slice_off,
+    k_tile_cost<<<grid_for(ntiles, kBlock), kBlock, 0, st>>>(ntiles, kR, kC, n, B.tile_seg, B.seg_slice, B.slice_off,
                                                             B.res_rowptr, cost.p);
     GIFT_LAUNCH_CHECK(ctx);
     std::vector<int64_t> hc(ntiles);
@@ -1195,6 +1389,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   GIFT_CUDA(cudaStreamSynchronize(st));
   B.ntiles = ntiles;
   B.tile_rows = kR;
+  B.kC = kC;
   B.nwide = nwide;
   B.nseg = nseg;
   B.nslices = nslices;
@@ -1219,6 +1414,11 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
     B.ok = bmt_build(ctx, c, csr_w32_public(ctx, c));
   }
   if (!B.ok) return false;
+  {  // a tuning shape may not fit this signal width's shared-memory footprint
+    static int optin = 0;
+    if (!optin) GIFT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    if (bmt_smem(fin, B.tile_rows, B.kC) + 1024 > (size_t)optin) return false;
+  }
   // the wide rows (pads / macros, long rows) run concurrently on a side stream:
   // disjoint output rows, same input signal
   const bool fork = B.nwide > 0;
@@ -1247,7 +1447,7 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
     }
     ctr = slot;
   }
-  BmtArgs b{c->n,         B.tile_rows,  B.data,      B.wide,      B.res_rowptr, B.res_col,     B.res_w,
+  BmtArgs b{c->n,         B.tile_rows,  B.kC,         B.data,      B.wide,      B.res_rowptr, B.res_col,     B.res_w,
             B.tile_seg,   B.seg_code,   B.seg_slice, B.slice_off, B.slice_rows, order,         ctr,
             B.ntiles,     B.split};
   switch (fin) {

@@ -146,6 +146,7 @@ struct Csr {
     bool ready = false, ok = false;
     int64_t ntiles = 0, nseg = 0, nslices = 0, slots = 0, nwide = 0;
     int tile_rows = 2048;
+    int kC = 4096;                  // columns per staged block
     uint8_t* wide = nullptr;        // [n] rows left to the row kernel (span > kWide blocks)
     int32_t* wide_rows = nullptr;   // [nwide]
     int64_t nres = 0;               // entries in sparse (tile, block) segments

@@ -404,19 +404,26 @@ def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, monkeypatch, world,
     assert rel_l2(full, single) <= FP32_TOL
 
 
-@pytest.mark.parametrize("config,scale,cap,tile_rows,db", [
-    ("c2", 0.05, 200, 0, 1), ("c3", 0.03, 200, 0, 1), ("c1", 0.2, None, 0, 1), ("c0", 1.0, None, 0, 1),
-    ("c2", 0.01, None, 0, 1), ("c2", 0.05, 200, 4096, 1), ("c1", 0.2, None, 4096, 1), ("c3", 0.03, 200, 2048, 0),
-    ("c1", 0.2, None, 8192, 0)])
-def test_bmt_hop_matches_oracle_and_row_kernel(gb, orc, monkeypatch, config, scale, cap, tile_rows, db):
+@pytest.mark.parametrize("config,scale,cap,tile_rows,db,col_bits,nb", [
+    ("c2", 0.05, 200, 0, 1, 0, 1), ("c3", 0.03, 200, 0, 1, 0, 1), ("c1", 0.2, None, 0, 1, 0, 1),
+    ("c0", 1.0, None, 0, 1, 0, 1), ("c2", 0.01, None, 0, 1, 0, 1), ("c2", 0.05, 200, 4096, 1, 0, 1),
+    ("c1", 0.2, None, 4096, 1, 0, 1), ("c3", 0.03, 200, 2048, 0, 0, 0), ("c1", 0.2, None, 8192, 0, 0, 0),
+    ("c2", 0.05, 200, 2048, 1, 12, 0), ("c1", 0.2, None, 4096, 1, 13, 0), ("c1", 0.2, None, 8192, 1, 12, 0),
+    ("c4", 0.02, 100, 4096, 1, 13, 1), ("c4", 0.02, 100, 2048, 1, 11, 1), ("c2", 0.05, 200, 2048, 1, 14, 1)])
+def test_bmt_hop_matches_oracle_and_row_kernel(gb, orc, monkeypatch, config, scale, cap, tile_rows, db, col_bits,
+                                               nb):
     """Force the block-major tiled hop (bmt.cu) on small graphs (it is normally
     reserved for >= 256k rows) and check it against the oracle and the
-    row-parallel kernel; tile heights 2048 / 4096 / 8192, single- and
-    double-buffered block staging."""
+    row-parallel kernel; tile heights 2048 / 4096 / 8192, column blocks of
+    2048 .. 16384 (a shape too large for F = 4 falls back to the row kernel for
+    that pass), the barrier-free pipeline (nb) and the barrier kernels with
+    single- and double-buffered block staging."""
     from paper_2502_17632_b200 import synth
 
     monkeypatch.setenv("GIFT_BMT_TILE_ROWS", str(tile_rows))
+    monkeypatch.setenv("GIFT_BMT_COL_BITS", str(col_bits))
     monkeypatch.setenv("GIFT_BMT_DB", str(db))
+    monkeypatch.setenv("GIFT_BMT_NB", str(nb))
 
     fd = synth.generate(config, seed=6, scale=scale, window=900)
     ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, cap)

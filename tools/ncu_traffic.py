@@ -33,7 +33,7 @@ def main() -> None:
     acc = collections.defaultdict(lambda: [0.0, 0.0, 0])
     for r in rows[2:]:
         name = r[ix["Kernel Name"]]
-        m = re.search(r"(k_hop_bmt|k_hop)<(\d+), (\d+)", name)
+        m = re.search(r"(k_hop_bmt_nb|k_hop_bmt|k_hop)<(\d+), (\d+)", name)
         if not m:
             continue
         key = f"{m.group(1)}<{m.group(2)}, {m.group(3)}>"
