@@ -45,9 +45,6 @@
 #include "hop.cuh"
 
 
-#ifndef GIFT_BMT_STREAM
-#define GIFT_BMT_STREAM 0  // 1: static per-warp record streams per segment; 0: dynamic slice grabbing
-#endif
 // records in flight per warp (software-pipeline depth), per signal width
 #ifndef GIFT_BMT_DEPTH4
 #define GIFT_BMT_DEPTH4 3
@@ -76,8 +73,8 @@ struct BmtShape {
 };
 BmtShape bmt_shape_for(double mean_row) {
   BmtShape s = mean_row >= 160.0 ? BmtShape{2048, 12} : BmtShape{4096, 13};
-  const int fr = env_int("GIFT_BMT_TILE_ROWS", 0);  // 2048 / 4096 / 8192 (tuning)
-  if (fr == 2048 || fr == 4096 || fr == 8192) s.kR = fr;
+  const int fr = env_int("GIFT_BMT_TILE_ROWS", 0);  // 1024 / 2048 / 4096 / 8192 (tuning)
+  if (fr == 1024 || fr == 2048 || fr == 4096 || fr == 8192) s.kR = fr;
   const int fc = env_int("GIFT_BMT_COL_BITS", 0);  // 11..14 (tuning)
   if (fc >= 11 && fc <= 14) s.cb = fc;
   return s;
@@ -203,27 +200,6 @@ __global__ void k_seg_slices(int64_t nseg, const int64_t* __restrict__ seg_run, 
 }
 
 // slot count of each slice: its longest (first) run rounded up to 4, x 32 lanes
-// static split of a segment's slices over the NW warps of a CTA, balanced by
-// steps: warp w takes the slices whose first step lies in [w T / NW, (w+1) T / NW)
-__global__ void k_warp_split(int64_t nseg, int nw, const int64_t* __restrict__ seg_slice,
-                             const int64_t* __restrict__ slice_off, int32_t* __restrict__ split) {
-  const int64_t total = nseg * (nw + 1);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t sg = i / (nw + 1);
-    const int w = (int)(i % (nw + 1));
-    const int64_t sl0 = seg_slice[sg], sl1 = seg_slice[sg + 1];
-    const int64_t base = slice_off[sl0], T = (slice_off[sl1] - base) / 128;
-    const int64_t target = (T * w) / nw;
-    int64_t lo = sl0, hi = sl1;  // first slice with start step >= target
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) / 2;
-      if ((slice_off[mid] - base) / 128 < target) lo = mid + 1;
-      else hi = mid;
-    }
-    split[i] = (int32_t)(w == nw ? sl1 - sl0 : lo - sl0);
-  }
-}
-
 __global__ void k_slice_len(int64_t nseg, const int64_t* __restrict__ seg_run, const int64_t* __restrict__ seg_slice,
                             const uint64_t* __restrict__ rkey_s, int cb, int64_t* __restrict__ slice_slots) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
@@ -400,6 +376,26 @@ __global__ void k_residual_split(int64_t m, const uint32_t* __restrict__ rkey, c
   }
 }
 
+// rows with residual entries, and each tile's range of that list
+__global__ void k_has_res(int64_t n, const int64_t* __restrict__ rowptr, uint8_t* __restrict__ flag) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    flag[r] = rowptr[r + 1] > rowptr[r];
+}
+
+__global__ void k_tile_res(int64_t ntiles, int kR, const int64_t* __restrict__ rows, int64_t m,
+                           int64_t* __restrict__ tile_res) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= ntiles; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t key = t * kR;
+    int64_t lo = 0, hi = m;  // first row >= key
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (rows[mid] < key) lo = mid + 1;
+      else hi = mid;
+    }
+    tile_res[t] = lo;
+  }
+}
+
 // final layout: one 768-byte record per (slice, step of 4): 32 lanes x 4 u16
 // columns, then 32 lanes x 4 f32 weights -- a warp step reads one contiguous
 // record (one DRAM stream per warp instead of two)
@@ -471,7 +467,8 @@ struct BmtArgs {
   const int32_t* tile_order;  // persistent mode: tiles by decreasing cost
   unsigned* ctr;              // persistent mode: [next tile, finished CTAs]; null = one CTA per tile
   int64_t ntiles;
-  const int32_t* split;       // [nseg * (NW + 1)] static warp split of each segment's slices; null = dynamic
+  const int64_t* res_rows;    // rows with residual entries, ascending
+  const int64_t* tile_res;    // [ntiles + 1] range of res_rows per tile
 };
 
 __device__ __forceinline__ uint2 ld_stream_v2u32(const void* p, uint64_t pol) {
@@ -573,13 +570,13 @@ __device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, cons
                                                int lane, uint64_t pol_s) {
   const int64_t sl0 = b.seg_slice[s];
   const int nsl = (int)(b.seg_slice[s + 1] - sl0);
-  // the next slice's index and metadata are fetched before the current one
-  // runs, so their latency hides behind its stream
   auto grab = [&]() {
     int j = 0;
     if (lane == 0) j = atomicAdd(ctr, 1);
     return __shfl_sync(0xffffffffu, j, 0);
   };
+  // the next slice's index and metadata are fetched before the current one
+  // runs, so their latency hides behind its stream
   int j = grab();
   int64_t off = 0, end = 0;
   int row = 0xffff;
@@ -605,115 +602,30 @@ __device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, cons
   }
 }
 
-// the slices of segment s as ONE record stream per warp (stream mode): the
-// warp owns a contiguous range of slices (static split balanced by steps,
-// k_warp_split), so its loads run ahead across slice boundaries; at a
-// boundary each lane adds its run to its row's accumulator and switches row
-// (boundaries are warp-uniform)
-template <int FIN, int D, int NW>
-__device__ __forceinline__ void segment_stream(const BmtArgs& b, int64_t s, const float* zs, float* accs, int warp,
-                                               int lane, uint64_t pol_s) {
-  const int64_t sl0 = b.seg_slice[s];
-  const int32_t* sp = b.split + s * (NW + 1);
-  int64_t j = sl0 + sp[warp];
-  const int64_t j1 = sl0 + sp[warp + 1];
-  if (j >= j1) return;
-  const int64_t off0 = b.slice_off[j];
-  const int total = (int)((b.slice_off[j1] - off0) / 128);
-  const uint8_t* cp = b.data + (off0 / 128) * 768 + 8 * lane;
-  const uint8_t* wp = cp + 256 + 8 * lane;
-  // slice boundaries (in steps from the stream start) and rows, one slice ahead
-  int bound = (int)((b.slice_off[j + 1] - off0) / 128);
-  int row = b.slice_rows[j * 32 + lane];
-  int bound_n = total, row_n = 0xffff;
-  if (j + 1 < j1) {
-    bound_n = (int)((b.slice_off[j + 2] - off0) / 128);
-    row_n = b.slice_rows[(j + 1) * 32 + lane];
-  }
-  float acc[FIN];
-#pragma unroll
-  for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
-  uint2 cq[D];
-  float4 wq[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d)
-    if (d < total) {
-      cq[d] = ld_stream_v2u32(cp + d * 768, pol_s);
-      wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + d * 768), pol_s);
-    }
-  auto boundary = [&](int k) {
-    if (k + 1 == bound) {  // end of this slice (same step for every lane)
-      if (row != 0xffff) {
-#pragma unroll
-        for (int f = 0; f < FIN; ++f) accs[row * FIN + f] += acc[f];
-      }
-#pragma unroll
-      for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
-      ++j;
-      row = row_n;
-      bound = bound_n;
-      if (j + 1 < j1) {
-        bound_n = (int)((b.slice_off[j + 2] - off0) / 128);
-        row_n = b.slice_rows[(j + 1) * 32 + lane];
-      }
-    }
-  };
-  int k = 0;
-  while (k + 2 * D <= total) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      step_fma<FIN>(acc, cq[d], wq[d], zs);
-      cq[d] = ld_stream_v2u32(cp + (d + D) * 768, pol_s);
-      wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + (d + D) * 768), pol_s);
-      boundary(k + d);
-    }
-    cp += D * 768;
-    wp += D * 768;
-    k += D;
-  }
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    if (k + d < total) {
-      step_fma<FIN>(acc, cq[d], wq[d], zs);
-      if (k + d + D < total) {
-        cq[d] = ld_stream_v2u32(cp + (d + D) * 768, pol_s);
-        wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + (d + D) * 768), pol_s);
-      }
-      boundary(k + d);
-    }
-  }
-  k += D;
-  cp += D * 768;
-  wp += D * 768;
-#pragma unroll
-  for (int d = 0; d < D; ++d)
-    if (k + d < total) {
-      step_fma<FIN>(acc, cq[d], wq[d], zs);
-      boundary(k + d);
-    }
-}
-
 // after the segments: residual entries, then the fused row epilogue
 template <int FIN, int FOUT, int kThreads>
-__device__ __forceinline__ void bmt_tile_finish(const HopArgs& a, const BmtArgs& b, int64_t r0, int nrows,
-                                                float* accs, int tid, int lane, uint64_t pol_z) {
+__device__ __forceinline__ void bmt_tile_finish(const HopArgs& a, const BmtArgs& b, int64_t tile, int64_t r0,
+                                                int nrows, float* accs, int tid, int lane, uint64_t pol_z) {
   __syncthreads();
-  // residual entries (sparse blocks: pad / macro columns), 8 lanes per row, from L2
+  // residual entries (sparse blocks: pad / macro columns), 8 lanes per row, from
+  // L2; only the tile's rows that have any (a precomputed list)
   {
     constexpr int G = 8;
     const int sub = lane & (G - 1);
     const unsigned gmask = 0xffu << (lane & ~(G - 1));
-    for (int rr = tid / G; rr < nrows; rr += kThreads / G) {
-      const int64_t beg = b.res_rowptr[r0 + rr], end = b.res_rowptr[r0 + rr + 1];
-      if (beg == end) continue;  // uniform in the group
+    const int64_t q1 = b.tile_res[tile + 1];
+    for (int64_t q = b.tile_res[tile] + tid / G; q < q1; q += kThreads / G) {
+      const int64_t r = b.res_rows[q];
+      const int rr = (int)(r - r0);
+      const int64_t beg = b.res_rowptr[r], end = b.res_rowptr[r + 1];
       float acc[FIN];
 #pragma unroll
       for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
       for (int64_t k = beg + sub; k < end; k += G) {
-        const VecF<FIN> q = ld_z<FIN>(a.zin + (int64_t)b.res_col[k] * FIN, pol_z);
+        const VecF<FIN> zq = ld_z<FIN>(a.zin + (int64_t)b.res_col[k] * FIN, pol_z);
         const float wk = b.res_w[k];
 #pragma unroll
-        for (int f = 0; f < FIN; ++f) acc[f] = fmaf(wk, q.v[f], acc[f]);
+        for (int f = 0; f < FIN; ++f) acc[f] = fmaf(wk, zq.v[f], acc[f]);
       }
 #pragma unroll
       for (int off = G / 2; off > 0; off >>= 1)
@@ -764,13 +676,9 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
     for (int i = nf + tid; i < (kC + kPadRows) * FIN; i += kThreads) zs[i] = 0.f;  // short block + padding rows
     if (tid == 0) slice_ctr = 0;
     __syncthreads();
-#if GIFT_BMT_STREAM
-    segment_stream<FIN, bmt_depth<FIN>(), kThreads / 32>(b, s, zs, accs, tid >> 5, lane, pol_s);
-#else
     segment_slices<FIN, bmt_depth<FIN>()>(b, s, zs, accs, &slice_ctr, lane, pol_s);
-#endif
   }
-  bmt_tile_finish<FIN, FOUT, kThreads>(a, b, r0, nrows, accs, tid, lane, pol_z);
+  bmt_tile_finish<FIN, FOUT, kThreads>(a, b, tile, r0, nrows, accs, tid, lane, pol_z);
 }
 
 // cp.async (16 B, L2 hint) of segment s's signal block into zs; a ragged tail
@@ -824,13 +732,9 @@ __device__ __forceinline__ void bmt_tile_db(const HopArgs& a, const BmtArgs& b, 
       stage_async<FIN, kThreads>(a, b, s + 1, buf ? zs0 : zs1, tid, pol_z);
       if (tid == 0) slice_ctr2[buf ^ 1] = 0;
     }
-#if GIFT_BMT_STREAM
-    segment_stream<FIN, bmt_depth<FIN>(), kThreads / 32>(b, s, buf ? zs1 : zs0, accs, tid >> 5, lane, pol_s);
-#else
     segment_slices<FIN, bmt_depth<FIN>()>(b, s, buf ? zs1 : zs0, accs, &slice_ctr2[buf], lane, pol_s);
-#endif
   }
-  bmt_tile_finish<FIN, FOUT, kThreads>(a, b, r0, nrows, accs, tid, lane, pol_z);
+  bmt_tile_finish<FIN, FOUT, kThreads>(a, b, tile, r0, nrows, accs, tid, lane, pol_z);
 }
 
 template <int FIN, int FOUT, int kThreads, bool DB>
@@ -906,7 +810,7 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* m, unsigned byte
                : "=l"(state)
                : "r"(smem_addr(m)), "r"(bytes)
                : "memory");
-  (void)state;
+  asm volatile("" ::"l"(state));  // the phase token is not needed
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
@@ -999,7 +903,7 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt_nb(HopArg
   }
   __syncthreads();
   for (int i = tid; i < nrows * FIN; i += kThreads) acc[0][i] += acc[1][i];
-  bmt_tile_finish<FIN, FOUT, kThreads>(a, b, r0, nrows, acc[0], tid, lane, pol_z);
+  bmt_tile_finish<FIN, FOUT, kThreads>(a, b, tile, r0, nrows, acc[0], tid, lane, pol_z);
 }
 
 size_t bmt_smem_nb(int fin, int kR, int kC) { return 2 * ((size_t)(kC + kPadRows) * fin * 4 + (size_t)kR * fin * 4); }
@@ -1244,6 +1148,21 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
       GIFT_CUDA(cudaMemsetAsync(B.res_rowptr, 0, (n + 1) * sizeof(int64_t), st));
     }
     B.nres = nres;
+    {  // rows with residual entries per tile (the tile epilogue visits only those)
+      DevBuf<uint8_t> flag(ctx, n);
+      k_has_res<<<grid_for(n, kBlock), kBlock, 0, st>>>(n, B.res_rowptr, flag.p);
+      GIFT_LAUNCH_CHECK(ctx);
+      const int64_t cap = std::min<int64_t>(n, nres);
+      B.res_rows = static_cast<int64_t*>(csr_alloc(ctx, c, (cap + 1) * sizeof(int64_t)));
+      int64_t m = 0;
+      if (cap > 0) {
+        select_positions(ctx, flag.p, n, B.res_rows, nsel0.p);
+        m = fetch(ctx, nsel0.p);
+      }
+      B.tile_res = static_cast<int64_t*>(csr_alloc(ctx, c, (ntiles + 1) * sizeof(int64_t)));
+      k_tile_res<<<grid_for(ntiles + 1, kBlock), kBlock, 0, st>>>(ntiles, kR, B.res_rows, m, B.tile_res);
+      GIFT_LAUNCH_CHECK(ctx);
+    }
     // compact the dense entries (order preserved)
     DevBuf<uint32_t> k2(ctx, nnz - nres + 1);
     DevBuf<uint64_t> p2(ctx, nnz - nres + 1);
@@ -1318,13 +1237,6 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
   B.slice_off = static_cast<int64_t*>(csr_alloc(ctx, c, (nslices + 1) * sizeof(int64_t)));
   exclusive_sum(ctx, slots.p, B.slice_off, nslices + 1);
   const int64_t total = fetch(ctx, B.slice_off + nslices);
-  {  // static warp split (segment_stream); the kernel for this tile height has NW warps
-    const int nw = (kR > 2048 ? 1024 : 512) / 32;
-    B.nw = nw;
-    B.split = static_cast<int32_t*>(csr_alloc(ctx, c, (nseg * (nw + 1) + 1) * sizeof(int32_t)));
-    k_warp_split<<<grid_for(nseg * (nw + 1), kBlock), kBlock, 0, st>>>(nseg, nw, B.seg_slice, B.slice_off, B.split);
-    GIFT_LAUNCH_CHECK(ctx);
-  }
   // 6. scatter entries into slices; padding = column kC (zero signal row), weight 0
   B.slice_rows = static_cast<uint16_t*>(csr_alloc(ctx, c, (nslices * 32 + 1) * sizeof(uint16_t)));
   DevBuf<uint16_t> colb(ctx, total + 8);
@@ -1449,7 +1361,7 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
   }
   BmtArgs b{c->n,         B.tile_rows,  B.kC,         B.data,      B.wide,      B.res_rowptr, B.res_col,     B.res_w,
             B.tile_seg,   B.seg_code,   B.seg_slice, B.slice_off, B.slice_rows, order,         ctr,
-            B.ntiles,     B.split};
+            B.ntiles,     B.res_rows,   B.tile_res};
   switch (fin) {
     case 1: launch_bmt_out<1>(ctx, a, b, B.ntiles, fout); break;
     case 2: launch_bmt_out<2>(ctx, a, b, B.ntiles, fout); break;

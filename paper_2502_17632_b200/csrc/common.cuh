@@ -155,8 +155,8 @@ struct Csr {
     float* res_w = nullptr;
     int64_t* tile_seg = nullptr;    // [ntiles + 1] segment range of each row tile
     int32_t* tile_order = nullptr;  // [ntiles] tiles by decreasing estimated cost (persistent CTAs take them in order)
-    int nw = 16;                    // warps per CTA of this tile height's kernel
-    int32_t* split = nullptr;       // [nseg * (nw + 1)] static split of each segment's slices over the warps
+    int64_t* res_rows = nullptr;    // rows with residual entries
+    int64_t* tile_res = nullptr;    // [ntiles + 1] range of res_rows per tile
     int32_t* seg_code = nullptr;    // [nseg] staged column block, or -(block + 1): gather from L2
     int64_t* seg_slice = nullptr;   // [nseg + 1] slice range of each segment
     int64_t* slice_off = nullptr;   // [nslices + 1] first slot of each slice

@@ -537,3 +537,4 @@ def test_filter_host_pinned_in_place_matches_staged(gb, config, scale):
         assert_bits_equal(h_o.numpy(), out_pg, "pinned in-place output vs staged")
     fixed = mask.astype(bool)
     assert np.array_equal(h_o.numpy()[fixed], pos[fixed])
+
