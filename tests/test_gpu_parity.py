@@ -539,33 +539,3 @@ def test_filter_host_pinned_in_place_matches_staged(gb, config, scale):
     assert np.array_equal(h_o.numpy()[fixed], pos[fixed])
 
 
-
-@pytest.mark.parametrize("cover", [None, 0.5])
-def test_bmt_weight_codes_and_escapes(gb, orc, monkeypatch, cover):
-    """The tiled copy stores a u8 code per entry (the graph's 255 most frequent
-    fp32 weights); entries with other weights are summed from the residual CSR.
-    A banded graph whose weights are spread over many values exercises the
-    escapes (coverage ~72 %, accepted with GIFT_BMT_MIN_COVER=0.5); with the
-    default 90 % floor the graph is left to the row kernel.  Both must match
-    the oracle and each other within the fp32 tolerance."""
-    rng = np.random.default_rng(11)
-    n, per_row, band = 4096, 48, 700
-    rows = np.repeat(np.arange(n), per_row)
-    cols = np.clip(rows + rng.integers(-band, band + 1, size=rows.size), 0, n - 1)
-    keep = rows < cols
-    r, c = rows[keep], cols[keep]
-    vals = 1.0 / (1 + rng.geometric(0.005, size=r.size))  # top-255 weights cover ~72 % of the entries
-    rr, cc, vv = np.concatenate([r, c]), np.concatenate([c, r]), np.concatenate([vals, vals])
-    g = rng.standard_normal((n, 2)).astype(np.float32)
-    ref = orc.coo_to_csr(n, rr, cc, vv)
-    want = orc.gift_filter(ref, g.astype(np.float64), DEFAULT)
-    monkeypatch.setenv("GIFT_BMT", "0")
-    row_kernel = gb.gift_filter(gb.from_coo(n, rr, cc, vv), g)
-    monkeypatch.setenv("GIFT_BMT", "1")
-    monkeypatch.setenv("GIFT_BMT_MIN_ROWS", "1")
-    monkeypatch.setenv("GIFT_BMT_MIN_MEAN", "1")
-    if cover is not None:
-        monkeypatch.setenv("GIFT_BMT_MIN_COVER", str(cover))
-    out = gb.gift_filter(gb.from_coo(n, rr, cc, vv), g)
-    assert rel_l2(out, want) <= FP32_TOL
-    assert rel_l2(out, row_kernel) <= 1e-6
