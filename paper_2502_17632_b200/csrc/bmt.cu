@@ -45,16 +45,21 @@
 #include "hop.cuh"
 
 
-// records in flight per warp (software-pipeline depth), per signal width
+// records in flight per warp (software-pipeline depth), per signal width; at
+// F = 4, 4 on 512-thread CTAs (c3 F=4 pass 1.138 -> 1.117 ms) and 3 on
+// 1024-thread ones (c4: 4 was 1.5 % slower)
 #ifndef GIFT_BMT_DEPTH4
 #define GIFT_BMT_DEPTH4 3
+#endif
+#ifndef GIFT_BMT_DEPTH4_512
+#define GIFT_BMT_DEPTH4_512 4
 #endif
 #ifndef GIFT_BMT_DEPTH2
 #define GIFT_BMT_DEPTH2 5
 #endif
-template <int FIN>
+template <int FIN, int kThreads>
 __host__ __device__ constexpr int bmt_depth() {
-  return FIN == 4 ? GIFT_BMT_DEPTH4 : GIFT_BMT_DEPTH2;
+  return FIN == 4 ? (kThreads == 512 ? GIFT_BMT_DEPTH4_512 : GIFT_BMT_DEPTH4) : GIFT_BMT_DEPTH2;
 }
 
 namespace gift {
@@ -676,7 +681,7 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
     for (int i = nf + tid; i < (kC + kPadRows) * FIN; i += kThreads) zs[i] = 0.f;  // short block + padding rows
     if (tid == 0) slice_ctr = 0;
     __syncthreads();
-    segment_slices<FIN, bmt_depth<FIN>()>(b, s, zs, accs, &slice_ctr, lane, pol_s);
+    segment_slices<FIN, bmt_depth<FIN, kThreads>()>(b, s, zs, accs, &slice_ctr, lane, pol_s);
   }
   bmt_tile_finish<FIN, FOUT, kThreads>(a, b, tile, r0, nrows, accs, tid, lane, pol_z);
 }
@@ -732,7 +737,7 @@ __device__ __forceinline__ void bmt_tile_db(const HopArgs& a, const BmtArgs& b, 
       stage_async<FIN, kThreads>(a, b, s + 1, buf ? zs0 : zs1, tid, pol_z);
       if (tid == 0) slice_ctr2[buf ^ 1] = 0;
     }
-    segment_slices<FIN, bmt_depth<FIN>()>(b, s, buf ? zs1 : zs0, accs, &slice_ctr2[buf], lane, pol_s);
+    segment_slices<FIN, bmt_depth<FIN, kThreads>()>(b, s, buf ? zs1 : zs0, accs, &slice_ctr2[buf], lane, pol_s);
   }
   bmt_tile_finish<FIN, FOUT, kThreads>(a, b, tile, r0, nrows, accs, tid, lane, pol_z);
 }
@@ -889,7 +894,7 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt_nb(HopArg
   for (int i = 0; i < nseg; ++i) {
     const int buf = i & 1;
     mbar_wait(&full[buf], (unsigned)(i >> 1) & 1u);
-    segment_slices<FIN, bmt_depth<FIN>()>(b, s0 + i, zs[buf], acc[buf], &slice_ctr[buf], lane, pol_s);
+    segment_slices<FIN, bmt_depth<FIN, kThreads>()>(b, s0 + i, zs[buf], acc[buf], &slice_ctr[buf], lane, pol_s);
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
