@@ -539,3 +539,4 @@ def test_filter_host_pinned_in_place_matches_staged(gb, config, scale):
     assert np.array_equal(h_o.numpy()[fixed], pos[fixed])
 
 
+
