@@ -30,6 +30,8 @@ for c in c2 c4; do
   timeout 900 python bench.py --config $c --steps 10 --no-cpu-baseline > gpurun_out/bench_$c.log 2>&1
   echo "bench $c exit $?"; tail -1 gpurun_out/bench_$c.log | cut -c1-300
 done
+timeout 1500 python tools/full_parity.py c0 c1 c2 c3 c4 > gpurun_out/full_parity.jsonl 2>gpurun_out/full_parity.err
+echo "full parity exit $?"; cut -c1-160 gpurun_out/full_parity.jsonl
 timeout 900 python tools/depth_sweep.py --config c4 > gpurun_out/depth_sweep_c4.jsonl 2>gpurun_out/depth_sweep_c4.err
 echo "depth sweep exit $?"; tail -2 gpurun_out/depth_sweep_c4.jsonl | cut -c1-300
 ls -la gpurun_out | head -40
