@@ -66,18 +66,23 @@ namespace gift {
 
 namespace {
 
-// Tile shape (rows per tile kR, columns per block kC = 2^cb), chosen per graph.
-// Long rows (c2/c3: ~400 entries) keep 2048 x 4096: runs of ~80 entries per
-// segment, 2 CTAs per SM at F = 4.  Short rows (c4: ~70 entries spread over a
-// +-40k-column band) get 4096 x 8192: a 4096-column block leaves ~6 entries per
-// run, so per-slice overhead and the round-up of runs to 4-entry steps (x1.32
-// stored slots) dominate; 8192 columns give ~11-entry runs and x1.20.  Both
-// shapes fit the F = 4 kernel: (kC + 16 + kR) x 16 B of shared memory.
+// Tile shape (rows per tile kR, columns per block kC = 2^cb), chosen per graph
+// and signal width.  Long rows (c2/c3: ~400 entries) keep 2048 x 4096 for every
+// width: runs of ~80 entries per segment, 2 CTAs per SM at F = 4.  Short rows
+// (c4: ~70 entries spread over a +-40k-column band) are bound by the little
+// work per segment: a 4096-column block leaves ~6 entries per run (and x1.32
+// stored slots after the round-up of runs to 4-entry steps), 8192 columns
+// ~11 entries (x1.20); F = 4 gets 4096 x 8192 (the largest shape whose F = 4
+// footprint, (kC + 16 + kR) x 16 B, fits), F <= 2 a second copy of 8192 x
+// 16384 (measured per hop on c4, tools/shape_sweep.sh: 4096x4096 1.87 ms,
+// 4096x8192 1.45, 8192x8192 1.48, 4096x16384 1.36, 8192x16384 1.22).
 struct BmtShape {
   int kR, cb;
 };
-BmtShape bmt_shape_for(double mean_row) {
-  BmtShape s = mean_row >= 160.0 ? BmtShape{2048, 12} : BmtShape{4096, 13};
+bool bmt_short_rows(double mean_row) { return mean_row < 160.0; }
+
+BmtShape bmt_shape_for(double mean_row, bool wide_blocks) {
+  BmtShape s = !bmt_short_rows(mean_row) ? BmtShape{2048, 12} : (wide_blocks ? BmtShape{8192, 14} : BmtShape{4096, 13});
   const int fr = env_int("GIFT_BMT_TILE_ROWS", 0);  // 1024 / 2048 / 4096 / 8192 (tuning)
   if (fr == 1024 || fr == 2048 || fr == 4096 || fr == 8192) s.kR = fr;
   const int fc = env_int("GIFT_BMT_COL_BITS", 0);  // 11..14 (tuning)
@@ -1027,11 +1032,10 @@ void exclusive_sum(Ctx* ctx, const int64_t* in, int64_t* out, int64_t n) {
 }
 
 // Build the sliced block-major copy (once per graph; cached on the csr).
-bool bmt_build(Ctx* ctx, Csr* c, const float* w32) {
-  Csr::Bmt& B = c->bmt;
+bool bmt_build(Ctx* ctx, Csr* c, const float* w32, Csr::Bmt& B, bool wide_blocks) {
   cudaStream_t st = ctx->stream;
   const int64_t n = c->n, nnz_all = c->nnz;
-  const BmtShape shape = bmt_shape_for(c->mean_row);
+  const BmtShape shape = bmt_shape_for(c->mean_row, wide_blocks);
   const int kR = shape.kR, cb = shape.cb, kC = 1 << cb;
   const int64_t ntiles = (n + kR - 1) / kR;
   const int64_t nblocks = (n + kC - 1) / kC;
@@ -1322,13 +1326,17 @@ void launch_row_list(Ctx* ctx, const HopArgs& base, const int32_t* rows, int64_t
 bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
   if (env_int("GIFT_BMT", 1) == 0 || !c->sorted_rows || !c->square) return false;
   // building the tiled copy costs ~a few hops; only resident graphs amortise it
-  if (!ctx->bmt_enabled && !c->bmt.ok) return false;
+  // short-row graphs keep a second, wide-block copy for signal widths <= 2
+  // (unless a tuning shape is forced); long-row graphs use one copy
+  const bool wide_blocks = fin <= 2 && bmt_short_rows(c->mean_row) && env_int("GIFT_BMT_TILE_ROWS", 0) == 0 &&
+                           env_int("GIFT_BMT_COL_BITS", 0) == 0 && env_int("GIFT_BMT_WIDE", 1);
+  Csr::Bmt& B = wide_blocks ? c->bmt_wide : c->bmt;
+  if (!ctx->bmt_enabled && !B.ok) return false;
   if (c->n < env_int("GIFT_BMT_MIN_ROWS", 262144) || c->mean_row < env_int("GIFT_BMT_MIN_MEAN", 32)) return false;
   if (a.row_begin != 0 || a.n != c->n || a.part_in) return false;  // part_out: the epilogue writes partials
-  Csr::Bmt& B = c->bmt;
   if (!B.ready) {
     B.ready = true;
-    B.ok = bmt_build(ctx, c, csr_w32_public(ctx, c));
+    B.ok = bmt_build(ctx, c, csr_w32_public(ctx, c), B, wide_blocks);
   }
   if (!B.ok) return false;
   {  // a tuning shape may not fit this signal width's shared-memory footprint
