@@ -67,22 +67,23 @@ namespace gift {
 namespace {
 
 // Tile shape (rows per tile kR, columns per block kC = 2^cb), chosen per graph
-// and signal width.  Long rows (c2/c3: ~400 entries) keep 2048 x 4096 for every
-// width: runs of ~80 entries per segment, 2 CTAs per SM at F = 4.  Short rows
-// (c4: ~70 entries spread over a +-40k-column band) are bound by the little
-// work per segment: a 4096-column block leaves ~6 entries per run (and x1.32
-// stored slots after the round-up of runs to 4-entry steps), 8192 columns
-// ~11 entries (x1.20); F = 4 gets 4096 x 8192 (the largest shape whose F = 4
-// footprint, (kC + 16 + kR) x 16 B, fits), F <= 2 a second copy of 8192 x
-// 16384 (measured per hop on c4, tools/shape_sweep.sh: 4096x4096 1.87 ms,
-// 4096x8192 1.45, 8192x8192 1.48, 4096x16384 1.36, 8192x16384 1.22).
+// and signal width.  Fewer, larger segments win (per-segment hand-offs and the
+// round-up of runs to 4-entry steps cost more than the larger staged block):
+// signal widths <= 2 use 8192 x 16384 -- the largest F = 2 footprint,
+// (kC + 16) x 8 B + kR x 8 B -- on every graph (per hop, tools/shape_sweep.sh:
+// c4 4096x4096 1.87 ms, 4096x8192 1.45, 8192x8192 1.48, 4096x16384 1.36,
+// 8192x16384 1.22; c3 2048x4096 0.98, 2048x8192 0.93, 4096x16384 0.89,
+// 8192x16384 0.87).  F = 4 (kC + 16 + kR) x 16 B must fit too, so it gets a
+// second copy: 2048 x 4096 for long rows (c2/c3, ~400 entries: runs of ~80
+// entries per segment, 2 CTAs per SM), 4096 x 8192 for short rows (c4, ~70
+// entries over a +-40k-column band: 4096-column blocks left ~6-entry runs).
 struct BmtShape {
   int kR, cb;
 };
 bool bmt_short_rows(double mean_row) { return mean_row < 160.0; }
 
 BmtShape bmt_shape_for(double mean_row, bool wide_blocks) {
-  BmtShape s = !bmt_short_rows(mean_row) ? BmtShape{2048, 12} : (wide_blocks ? BmtShape{8192, 14} : BmtShape{4096, 13});
+  BmtShape s = wide_blocks ? BmtShape{8192, 14} : (!bmt_short_rows(mean_row) ? BmtShape{2048, 12} : BmtShape{4096, 13});
   const int fr = env_int("GIFT_BMT_TILE_ROWS", 0);  // 1024 / 2048 / 4096 / 8192 (tuning)
   if (fr == 1024 || fr == 2048 || fr == 4096 || fr == 8192) s.kR = fr;
   const int fc = env_int("GIFT_BMT_COL_BITS", 0);  // 11..14 (tuning)
@@ -1326,10 +1327,10 @@ void launch_row_list(Ctx* ctx, const HopArgs& base, const int32_t* rows, int64_t
 bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
   if (env_int("GIFT_BMT", 1) == 0 || !c->sorted_rows || !c->square) return false;
   // building the tiled copy costs ~a few hops; only resident graphs amortise it
-  // short-row graphs keep a second, wide-block copy for signal widths <= 2
-  // (unless a tuning shape is forced); long-row graphs use one copy
-  const bool wide_blocks = fin <= 2 && bmt_short_rows(c->mean_row) && env_int("GIFT_BMT_TILE_ROWS", 0) == 0 &&
-                           env_int("GIFT_BMT_COL_BITS", 0) == 0 && env_int("GIFT_BMT_WIDE", 1);
+  // signal widths <= 2 use the wide-block copy, F = 4 its own (unless a
+  // tuning shape is forced: then one copy serves every width)
+  const bool wide_blocks = fin <= 2 && env_int("GIFT_BMT_TILE_ROWS", 0) == 0 && env_int("GIFT_BMT_COL_BITS", 0) == 0 &&
+                           env_int("GIFT_BMT_WIDE", 1);
   Csr::Bmt& B = wide_blocks ? c->bmt_wide : c->bmt;
   if (!ctx->bmt_enabled && !B.ok) return false;
   if (c->n < env_int("GIFT_BMT_MIN_ROWS", 262144) || c->mean_row < env_int("GIFT_BMT_MIN_MEAN", 32)) return false;

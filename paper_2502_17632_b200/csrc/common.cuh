@@ -163,7 +163,7 @@ struct Csr {
     uint16_t* slice_rows = nullptr; // [nslices * 32] row in tile per lane (0xffff: none)
     uint8_t* data = nullptr;        // [slots / 128] 768-byte records: 32x4 u16 columns (kC = padding),
                                     // then 32x4 f32 weights
-  } bmt, bmt_wide;  // bmt_wide: short-row graphs, signal widths <= 2 (bmt.cu bmt_shape_for)
+  } bmt, bmt_wide;  // bmt_wide: signal widths <= 2; bmt: F = 4 (bmt.cu bmt_shape_for)
   std::vector<void*> owned;       // everything above, freed on destroy
 };
 
