@@ -73,17 +73,15 @@ namespace {
 // (kC + 16) x 8 B + kR x 8 B -- on every graph (per hop, tools/shape_sweep.sh:
 // c4 4096x4096 1.87 ms, 4096x8192 1.45, 8192x8192 1.48, 4096x16384 1.36,
 // 8192x16384 1.22; c3 2048x4096 0.98, 2048x8192 0.93, 4096x16384 0.89,
-// 8192x16384 0.87).  F = 4 (kC + 16 + kR) x 16 B must fit too, so it gets a
-// second copy: 2048 x 4096 for long rows (c2/c3, ~400 entries: runs of ~80
-// entries per segment, 2 CTAs per SM), 4096 x 8192 for short rows (c4, ~70
-// entries over a +-40k-column band: 4096-column blocks left ~6-entry runs).
+// 8192x16384 0.87).  F = 4 needs (kC + 16 + kR) x 16 B and gets a second copy
+// of 4096 x 8192, the largest shape that fits (F = 4 pass, c3: 2048x4096 at
+// 2 CTAs per SM 1.12 ms, 4096x4096 1.23, 2048x8192 1.41, 4096x8192 1.10;
+// c4: 4096-column blocks left ~6-entry runs and x1.32 stored slots).
 struct BmtShape {
   int kR, cb;
 };
-bool bmt_short_rows(double mean_row) { return mean_row < 160.0; }
-
-BmtShape bmt_shape_for(double mean_row, bool wide_blocks) {
-  BmtShape s = wide_blocks ? BmtShape{8192, 14} : (!bmt_short_rows(mean_row) ? BmtShape{2048, 12} : BmtShape{4096, 13});
+BmtShape bmt_shape_for(bool wide_blocks) {
+  BmtShape s = wide_blocks ? BmtShape{8192, 14} : BmtShape{4096, 13};
   const int fr = env_int("GIFT_BMT_TILE_ROWS", 0);  // 1024 / 2048 / 4096 / 8192 (tuning)
   if (fr == 1024 || fr == 2048 || fr == 4096 || fr == 8192) s.kR = fr;
   const int fc = env_int("GIFT_BMT_COL_BITS", 0);  // 11..14 (tuning)
@@ -984,11 +982,12 @@ void launch_bmt(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles) {
       return;
     }
   }
-  // 2048-row tiles: 2 CTAs x 512 threads per SM; taller tiles: 1 CTA x 1024.
-  // Double-buffered staging when both buffers fit at that occupancy.
-  const int tpb = b.tile_rows > 2048 ? 1024 : 512;
-  const int per_sm = tpb == 512 ? 2 : 1;
+  // 2048-row tiles: 2 CTAs x 512 threads per SM when two fit; taller tiles
+  // (or a footprint only one CTA fits): 1 CTA x 1024.  Double-buffered staging
+  // when both buffers fit at that occupancy.
   const size_t smem1 = bmt_smem(FIN, b.tile_rows, b.kC), smem2 = bmt_smem_db(FIN, b.tile_rows, b.kC);
+  const int tpb = (b.tile_rows > 2048 || 2 * (smem1 + 3 * 1024) > 228 * 1024) ? 1024 : 512;
+  const int per_sm = tpb == 512 ? 2 : 1;
   const bool db = env_int("GIFT_BMT_DB", 1) && ((uintptr_t)a.zin & 15) == 0 &&
                   (size_t)per_sm * (smem2 + 3 * 1024) <= 228 * 1024;
   if (db)
@@ -1036,7 +1035,7 @@ void exclusive_sum(Ctx* ctx, const int64_t* in, int64_t* out, int64_t n) {
 bool bmt_build(Ctx* ctx, Csr* c, const float* w32, Csr::Bmt& B, bool wide_blocks) {
   cudaStream_t st = ctx->stream;
   const int64_t n = c->n, nnz_all = c->nnz;
-  const BmtShape shape = bmt_shape_for(c->mean_row, wide_blocks);
+  const BmtShape shape = bmt_shape_for(wide_blocks);
   const int kR = shape.kR, cb = shape.cb, kC = 1 << cb;
   const int64_t ntiles = (n + kR - 1) / kR;
   const int64_t nblocks = (n + kC - 1) / kC;
