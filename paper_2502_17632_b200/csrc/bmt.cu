@@ -73,15 +73,18 @@ namespace {
 // (kC + 16) x 8 B + kR x 8 B -- on every graph (per hop, tools/shape_sweep.sh:
 // c4 4096x4096 1.87 ms, 4096x8192 1.45, 8192x8192 1.48, 4096x16384 1.36,
 // 8192x16384 1.22; c3 2048x4096 0.98, 2048x8192 0.93, 4096x16384 0.89,
-// 8192x16384 0.87).  F = 4 needs (kC + 16 + kR) x 16 B and gets a second copy
-// of 4096 x 8192, the largest shape that fits (F = 4 pass, c3: 2048x4096 at
-// 2 CTAs per SM 1.12 ms, 4096x4096 1.23, 2048x8192 1.41, 4096x8192 1.10;
-// c4: 4096-column blocks left ~6-entry runs and x1.32 stored slots).
+// 8192x16384 0.87).  F = 4 needs (kC + 16 + kR) x 16 B and gets a second
+// copy: 8192 x 4096 for long rows (c2/c3, ~400 entries: ~80-entry runs even in
+// 4096-column blocks, and more rows per segment; F = 4 pass on c3: 2048x4096
+// at 2 CTAs per SM 1.12 ms, 4096x4096 1.23, 2048x8192 1.41, 4096x8192 1.10,
+// 8192x2048 1.18, 8192x4096 1.04), 4096 x 8192 for short rows (c4, ~70
+// entries over a +-40k band: 4096-column blocks left ~6-entry runs and x1.32
+// stored slots).
 struct BmtShape {
   int kR, cb;
 };
-BmtShape bmt_shape_for(bool wide_blocks) {
-  BmtShape s = wide_blocks ? BmtShape{8192, 14} : BmtShape{4096, 13};
+BmtShape bmt_shape_for(double mean_row, bool wide_blocks) {
+  BmtShape s = wide_blocks ? BmtShape{8192, 14} : (mean_row >= 160.0 ? BmtShape{8192, 12} : BmtShape{4096, 13});
   const int fr = env_int("GIFT_BMT_TILE_ROWS", 0);  // 1024 / 2048 / 4096 / 8192 (tuning)
   if (fr == 1024 || fr == 2048 || fr == 4096 || fr == 8192) s.kR = fr;
   const int fc = env_int("GIFT_BMT_COL_BITS", 0);  // 11..14 (tuning)
@@ -1035,7 +1038,7 @@ void exclusive_sum(Ctx* ctx, const int64_t* in, int64_t* out, int64_t n) {
 bool bmt_build(Ctx* ctx, Csr* c, const float* w32, Csr::Bmt& B, bool wide_blocks) {
   cudaStream_t st = ctx->stream;
   const int64_t n = c->n, nnz_all = c->nnz;
-  const BmtShape shape = bmt_shape_for(wide_blocks);
+  const BmtShape shape = bmt_shape_for(c->mean_row, wide_blocks);
   const int kR = shape.kR, cb = shape.cb, kC = 1 << cb;
   const int64_t ntiles = (n + kR - 1) / kR;
   const int64_t nblocks = (n + kC - 1) / kC;
