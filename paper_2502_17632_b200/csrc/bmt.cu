@@ -1339,7 +1339,20 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
   if (a.row_begin != 0 || a.n != c->n || a.part_in) return false;  // part_out: the epilogue writes partials
   if (!B.ready) {
     B.ready = true;
-    B.ok = bmt_build(ctx, c, csr_w32_public(ctx, c), B, wide_blocks);
+    // the tiled copy is an optimisation: if device memory runs out while it is
+    // built (its temporaries take ~3x the matrix), free what it got and let
+    // the row kernel serve this graph
+    const size_t mark = c->owned.size();
+    try {
+      B.ok = bmt_build(ctx, c, csr_w32_public(ctx, c), B, wide_blocks);
+    } catch (const GiftException& e) {
+      if (e.code != GIFT_ERR_OOM) throw;
+      for (size_t i = mark; i < c->owned.size(); ++i) dev_free(ctx, c->owned[i]);
+      c->owned.resize(mark);
+      B = Csr::Bmt{};
+      B.ready = true;
+      B.ok = false;
+    }
   }
   if (!B.ok) return false;
   {  // a tuning shape may not fit this signal width's shared-memory footprint
