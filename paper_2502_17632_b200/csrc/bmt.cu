@@ -85,8 +85,8 @@ struct BmtShape {
 };
 BmtShape bmt_shape_for(double mean_row, bool wide_blocks) {
   BmtShape s = wide_blocks ? BmtShape{8192, 14} : (mean_row >= 160.0 ? BmtShape{8192, 12} : BmtShape{4096, 13});
-  const int fr = env_int("GIFT_BMT_TILE_ROWS", 0);  // 1024 / 2048 / 4096 / 8192 (tuning)
-  if (fr == 1024 || fr == 2048 || fr == 4096 || fr == 8192) s.kR = fr;
+  const int fr = env_int("GIFT_BMT_TILE_ROWS", 0);  // 1024 .. 16384 (tuning)
+  if (fr == 1024 || fr == 2048 || fr == 4096 || fr == 8192 || fr == 16384) s.kR = fr;
   const int fc = env_int("GIFT_BMT_COL_BITS", 0);  // 11..14 (tuning)
   if (fc >= 11 && fc <= 14) s.cb = fc;
   return s;
