@@ -55,6 +55,13 @@ extern "C" {
 #define GIFT_DTYPE_F32 0
 #define GIFT_DTYPE_F64 1
 
+/* When the fp32 bank builds the tiled (block-major, BMT) copy of a graph --
+ * a one-time reordering (~ a few hops of work) that makes later hops faster: */
+#define GIFT_TILED_NEVER 0     /* row kernel only */
+#define GIFT_TILED_ON_REUSE 1  /* default: the first bank on a graph runs the row kernel;
+                                  the copy is built when the graph is filtered again */
+#define GIFT_TILED_ALWAYS 2    /* build on the first fp32 hop */
+
 typedef struct gift_ctx gift_ctx; /* device + stream + workspace */
 typedef struct gift_csr gift_csr; /* immutable symmetric CSR (SparseSymMatrix, graph.py:48-111) */
 typedef struct gift_bookshelf gift_bookshelf; /* a parsed design (parse_design, netlist.py:418-458) */
@@ -67,6 +74,8 @@ int gift_ctx_set_stream(gift_ctx* ctx, void* stream);
 const char* gift_last_error(void);
 int64_t gift_last_error_arg(void);
 const char* gift_version(void);
+/* Tiled-copy policy of this context (GIFT_TILED_*). */
+int gift_ctx_set_tiled_policy(gift_ctx* ctx, int policy);
 /* Number of kernels this library launched on ctx since creation (for the bench's gpu_launches). */
 int64_t gift_ctx_launch_count(const gift_ctx* ctx);
 /* Launch timing: when on, every filter-bank kernel is bracketed by CUDA
@@ -82,7 +91,8 @@ int gift_ctx_profile_drain(gift_ctx* ctx, int max_records, int* h_kind, int* h_u
 /* build_clique_graph(design, max_clique_pins)  graph.py:120-158.
  * d_net_start: int64[n_nets+1] (Design.pin_table net_start, netlist.py:142-166),
  * d_pin_cell:  int32[n_pins] cell ids in [0, n_cells).
- * max_clique_pins <= 0 means None (no cap).  *n_skipped (host, nullable)
+ * max_clique_pins < 0 means None (no cap); a cap >= 0 skips every net with
+ * more pins than it (cap 0 or 1 skips all nets, as the reference does).  *n_skipped (host, nullable)
  * receives the number of nets skipped by the cap (graph.py:150-151). */
 int gift_build_clique_graph(gift_ctx* ctx, int64_t n_cells, int64_t n_nets,
                             const int64_t* d_net_start, const int32_t* d_pin_cell,
@@ -95,7 +105,13 @@ int gift_csr_from_coo(gift_ctx* ctx, int64_t n, int64_t nnz, const int64_t* d_ro
                       const int64_t* d_cols, const double* d_vals, int check_symmetric,
                       gift_csr** out);
 
+/* Frees csr once the work already enqueued on it has finished (no host wait,
+ * no device-wide synchronisation). */
 int gift_csr_destroy(gift_csr* csr);
+/* State of the tiled copies of csr (which: 0 = the F = 4 copy, 1 = the copy for
+ * signal widths <= 2): h_info[8] = {built, usable, tile_rows, block_cols,
+ * segments, slices, stored slots, rows left to the row kernel}. */
+int gift_csr_tiled_info(const gift_csr* csr, int which, int64_t* h_info);
 int gift_csr_shape(const gift_csr* csr, int64_t* n, int64_t* nnz);
 /* Device views (owned by csr): indptr int64[n+1], indices int32[nnz], values fp64[nnz]
  * (SparseSymMatrix.indptr/.indices/.values, graph.py:77-87). */
@@ -190,6 +206,16 @@ int gift_hop_fp32(gift_ctx* ctx, gift_csr* csr, const gift_hop_desc* desc);
 /* z[i, j*wcols + c] = s_j[i] * g[i*ld + c0 + c] for j < nch, c < wcols; F floats per row. */
 int gift_pack_fp32(gift_ctx* ctx, int64_t n, int wcols, int nch, const float* const* h_s, int in_dtype,
                    const void* d_g, int64_t ld, int64_t c0, int F, float* d_z);
+/* Row sharding of a resident graph (shard.py), all on the device:
+ * nnz-balanced contiguous row bounds for `world` ranks (h_bounds[world + 1],
+ * host), and the split of rows [r0, r1) into a LOCAL block (columns in
+ * [r0, r1), renumbered col - r0) and a GHOST block (other columns, renumbered
+ * (r1 - r0) + rank among the block's distinct ghost columns; their global ids
+ * from gift_csr_ext_ids).  Entry order and fp64 values are kept bit for bit. */
+int gift_csr_row_bounds(gift_ctx* ctx, const gift_csr* csr, int world, int64_t* h_bounds);
+int gift_csr_split_rows(gift_ctx* ctx, const gift_csr* csr, int64_t r0, int64_t r1, gift_csr** local,
+                        gift_csr** ghost);
+int gift_csr_ext_ids(const gift_csr* ghost, const int64_t** d_ids, int64_t* n_ids);
 /* dst[r, :] = src[idx[r], :] for F floats per row (halo send buffers). */
 int gift_gather_rows_f32(gift_ctx* ctx, int64_t n_idx, int F, const int64_t* d_idx, const float* d_src,
                          float* d_dst);

@@ -31,8 +31,42 @@ _probe = None
 
 
 def build() -> None:
-    """Compile the oracle (gcc) into oracle/_build/."""
+    """Compile the oracle (gcc) into oracle/_build/, and stage the reference."""
     subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    stage_reference()
+
+
+REF_SRC = "/root/reference/pkg/src/giftplace"
+REF_DIR = os.path.join(_HERE, "_ref")
+
+
+def stage_reference(src: str = REF_SRC) -> bool:
+    """Copy the reference package (pure Python) into oracle/_ref/ -- git-ignored,
+    it travels to the GPU box with the built libraries -- so bench.py's
+    cpu_baseline leg can time the reference's own gift_filter (gift.py:73-95)
+    where /root/reference does not exist.  No-op when the source is absent
+    (the GPU box uses the staged copy)."""
+    import shutil
+
+    if not os.path.isdir(src):
+        return os.path.isdir(os.path.join(REF_DIR, "giftplace"))
+    dst = os.path.join(REF_DIR, "giftplace")
+    if os.path.isdir(dst):
+        shutil.rmtree(dst)
+    shutil.copytree(src, dst, ignore=shutil.ignore_patterns("__pycache__", "*.pyc"))
+    return True
+
+
+def reference_module():
+    """The staged reference package (`giftplace`), or None."""
+    import importlib
+    import sys
+
+    if not os.path.isdir(os.path.join(REF_DIR, "giftplace")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    return importlib.import_module("giftplace")
 
 
 def _load():
@@ -122,7 +156,8 @@ def build_clique_graph(n: int, net_start, pin_cell, max_clique_pins: int | None 
     net_start = _i64(net_start)
     pin_cell = _i64(pin_cell)
     n_nets = len(net_start) - 1
-    cap = int(max_clique_pins) if max_clique_pins is not None else -1
+    # None = no cap; any cap < 2 skips every net with >= 2 pins (m > cap), as the reference
+    cap = max(int(max_clique_pins), 0) if max_clique_pins is not None else -1
     T = int(lib.orc_count_clique_pairs(n_nets, _p(net_start, _i64p), cap))
     indptr = np.zeros(n + 1, dtype=np.int64)
     indices = np.empty(max(2 * T, 1), dtype=np.int64)

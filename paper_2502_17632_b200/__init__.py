@@ -43,6 +43,7 @@ from .graph import (
 from .metrics import hpwl, laplacian, quadratic_wirelength, rayleigh_smoothness
 from .netlist import Cell, Design, FlatDesign, Net, Pin, Region, Row
 from .plio import PL_PRECISION, format_placement, write_placement
+from ._lib import set_tiled_policy
 
 __version__ = "0.1.0"
 
@@ -54,5 +55,5 @@ __all__ = [
     "Net", "NonSymmetricError", "Pin", "Region", "Row", "SparseSymMatrix", "TooLargeForDenseError",
     "apply_operator_power", "as_device_matrix", "build_clique_graph", "from_coo", "gift_filter", "gift_place",
     "gift_place_arrays", "hpwl", "initial_signal", "laplacian", "normalized_augmented_adjacency",
-    "quadratic_wirelength", "rayleigh_smoothness", "ZeroSignalError",
+    "quadratic_wirelength", "rayleigh_smoothness", "ZeroSignalError", "set_tiled_policy",
 ]

@@ -39,6 +39,10 @@ GIFT_PREC_FP64_EXACT = 1
 GIFT_DTYPE_F32 = 0
 GIFT_DTYPE_F64 = 1
 
+GIFT_TILED_NEVER = 0
+GIFT_TILED_ON_REUSE = 1
+GIFT_TILED_ALWAYS = 2
+
 c_i64 = ctypes.c_int64
 c_int = ctypes.c_int
 c_vp = ctypes.c_void_p
@@ -53,6 +57,8 @@ SIGNATURES = [
     ("gift_last_error", ctypes.c_char_p, []),
     ("gift_last_error_arg", c_i64, []),
     ("gift_version", ctypes.c_char_p, []),
+    ("gift_ctx_set_tiled_policy", c_int, [c_vp, c_int]),
+    ("gift_csr_tiled_info", c_int, [c_vp, c_int, c_i64p]),
     ("gift_ctx_launch_count", c_i64, [c_vp]),
     ("gift_ctx_set_profiling", c_int, [c_vp, c_int]),
     ("gift_ctx_profile_drain", c_int, [c_vp, c_int, c_vp, c_vp, c_vp, ctypes.POINTER(c_int)]),
@@ -78,6 +84,9 @@ SIGNATURES = [
     ("gift_hop_fp32", c_int, [c_vp, c_vp, c_vp]),
     ("gift_pack_fp32", c_int, [c_vp, c_i64, c_int, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_int, c_vp]),
     ("gift_gather_rows_f32", c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp]),
+    ("gift_csr_row_bounds", c_int, [c_vp, c_vp, c_int, c_i64p]),
+    ("gift_csr_split_rows", c_int, [c_vp, c_vp, c_i64, c_i64, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
+    ("gift_csr_ext_ids", c_int, [c_vp, ctypes.POINTER(c_vp), c_i64p]),
     # placement metrics (metrics.py)
     ("gift_quadratic_wirelength", c_int, [c_vp, c_vp, c_vp, c_dp]),
     ("gift_laplacian", c_int, [c_vp, c_vp, ctypes.POINTER(c_vp)]),
@@ -95,7 +104,8 @@ SIGNATURES = [
 
 _lib = None
 _lock = threading.Lock()
-_ctxs: dict[int, int] = {}
+_ctxs: dict[tuple[int, int], int] = {}  # (thread id, device) -> gift_ctx*
+_policy = GIFT_TILED_ON_REUSE
 
 
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
@@ -144,25 +154,46 @@ def torch_cuda():
 
 
 def context(device: int | None = None) -> int:
-    """Per-device library context bound to torch's current stream."""
+    """Library context of (this thread, device), bound to torch's current
+    stream.  A gift_ctx holds per-call scratch and a stream, so threads get
+    their own (the library also serialises entry points on a context)."""
     torch = torch_cuda()
     lib = load_library()
     dev = torch.cuda.current_device() if device is None else int(device)
-    ctx = _ctxs.get(dev)
+    key = (threading.get_ident(), dev)
+    ctx = _ctxs.get(key)
     if ctx is None:
         h = c_vp()
         check(lib.gift_ctx_create(dev, ctypes.byref(h)))
         ctx = h.value
-        _ctxs[dev] = ctx
+        check(lib.gift_ctx_set_tiled_policy(ctx, _policy))
+        with _lock:
+            _ctxs[key] = ctx
     stream = torch.cuda.current_stream(dev).cuda_stream
     check(lib.gift_ctx_set_stream(ctx, c_vp(stream)))
     return ctx
 
 
+def set_tiled_policy(policy: str) -> None:
+    """When the fp32 bank builds a graph's tiled copy: "on_reuse" (default:
+    the first bank on a graph runs the row kernel, later ones build and use
+    the copy), "always" (first hop) or "never"."""
+    global _policy
+    codes = {"never": GIFT_TILED_NEVER, "on_reuse": GIFT_TILED_ON_REUSE, "always": GIFT_TILED_ALWAYS}
+    if policy not in codes:
+        raise ValueError(f"tiled policy must be one of {sorted(codes)}, got {policy!r}")
+    _policy = codes[policy]
+    lib = load_library()
+    with _lock:
+        ctxs = list(_ctxs.values())
+    for ctx in ctxs:
+        check(lib.gift_ctx_set_tiled_policy(ctx, _policy))
+
+
 def launch_count(device: int | None = None) -> int:
     torch = torch_cuda()
     dev = torch.cuda.current_device() if device is None else int(device)
-    ctx = _ctxs.get(dev)
+    ctx = _ctxs.get((threading.get_ident(), dev))
     return int(load_library().gift_ctx_launch_count(ctx)) if ctx else 0
 
 

@@ -4,6 +4,8 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "common.cuh"
@@ -30,6 +32,8 @@ void pack_fp32(Ctx* ctx, int64_t n, int wcols, int nch, const float* const* s, i
 void gather_rows_f32(Ctx* ctx, int64_t n_idx, int F, const int64_t* idx, const float* src, float* dst);
 Csr* csr_from_arrays(Ctx* ctx, int64_t n_rows, int64_t nnz, const int64_t* d_indptr, const int32_t* d_indices,
                      const double* d_values);
+void csr_row_bounds(Ctx* ctx, const Csr* c, int world, int64_t* h_bounds);
+void csr_split_rows(Ctx* ctx, const Csr* c, int64_t r0, int64_t r1, Csr** local, Csr** ghost);
 
 double quadratic_wirelength(Ctx* ctx, const Csr* c, const double* g);
 double hpwl(Ctx* ctx, int64_t n_nets, const int64_t* net_start, const int32_t* pin_cell, const double* pdx,
@@ -75,8 +79,14 @@ void dev_free(Ctx* ctx, void* p) {
 
 void* scratch(Ctx* ctx, int slot, size_t bytes) {
   if (ctx->scratch_bytes[slot] < bytes) {
-    if (ctx->scratch[slot]) dev_free(ctx, ctx->scratch[slot]);
-    ctx->scratch[slot] = dev_alloc(ctx, bytes);
+    // forget the old arena before allocating: if the allocation throws, the
+    // context must not keep a pointer it already freed
+    void* old = ctx->scratch[slot];
+    ctx->scratch[slot] = nullptr;
+    ctx->scratch_bytes[slot] = 0;
+    dev_free(ctx, old);
+    void* p = dev_alloc(ctx, bytes);
+    ctx->scratch[slot] = p;
     ctx->scratch_bytes[slot] = bytes;
   }
   return ctx->scratch[slot];
@@ -84,9 +94,13 @@ void* scratch(Ctx* ctx, int slot, size_t bytes) {
 
 void* pinned(Ctx* ctx, size_t bytes) {
   if (ctx->pinned_bytes < bytes) {
-    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    void* old = ctx->pinned;
     ctx->pinned = nullptr;
-    check_cuda(cudaMallocHost(&ctx->pinned, bytes), "cudaMallocHost", __FILE__, __LINE__);
+    ctx->pinned_bytes = 0;
+    if (old) cudaFreeHost(old);
+    void* p = nullptr;
+    check_cuda(cudaMallocHost(&p, bytes), "cudaMallocHost", __FILE__, __LINE__);
+    ctx->pinned = p;
     ctx->pinned_bytes = bytes;
   }
   return ctx->pinned;
@@ -98,15 +112,41 @@ void* csr_alloc(Ctx* ctx, Csr* c, size_t bytes) {
   return p;
 }
 
+// one non-blocking stream per device that returns freed graphs to the pool
+static cudaStream_t free_stream(int device) {
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> streams;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = streams.find(device);
+  if (it != streams.end()) return it->second;
+  cudaStream_t s = nullptr;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  streams[device] = s;
+  return s;
+}
+
+// The arrays are freed in stream order after the last entry point that used
+// them (its stream recorded c->last_use): no host wait, no device-wide sync.
 void csr_destroy(Csr* c) {
   if (!c) return;
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(c->device);
-  cudaDeviceSynchronize();  // outstanding work on any stream may still read the arrays
-  for (void* p : c->owned) cudaFreeAsync(p, 0);  // device idle: returns blocks to the pool
+  cudaStream_t fs = free_stream(c->device);
+  if (c->last_use) {
+    cudaStreamWaitEvent(fs, c->last_use, 0);
+    cudaEventDestroy(c->last_use);
+  }
+  for (void* p : c->owned) cudaFreeAsync(p, fs);
   cudaSetDevice(prev);
   delete static_cast<gift_csr*>(c);
+}
+
+// marks c as used by work enqueued on ctx->stream (see csr_destroy)
+void csr_touch(Ctx* ctx, Csr* c) {
+  if (!c) return;
+  if (!c->last_use) GIFT_CUDA(cudaEventCreateWithFlags(&c->last_use, cudaEventDisableTiming));
+  GIFT_CUDA(cudaEventRecord(c->last_use, ctx->stream));
 }
 
 }  // namespace gift
@@ -140,6 +180,27 @@ struct DeviceGuard {
 void require(bool ok, int code, const char* msg) {
   if (!ok) gift::throw_error(code, msg);
 }
+
+// An entry point that works on (ctx, csr): switches to the context's device,
+// serialises on the context and the graph (lock order ctx -> csr), and on
+// exit records that csr was used on ctx->stream (csr_destroy orders its
+// frees after that).
+struct ApiScope {
+  DeviceGuard dev;
+  std::unique_lock<std::recursive_mutex> lc, lg;
+  gift::Ctx* ctx;
+  gift::Csr* csr;
+  ApiScope(gift::Ctx* c, const gift::Csr* g)
+      : dev(c->device), lc(c->mu), ctx(c), csr(const_cast<gift::Csr*>(g)) {
+    if (csr) lg = std::unique_lock<std::recursive_mutex>(csr->mu);
+  }
+  ~ApiScope() {
+    try {
+      gift::csr_touch(ctx, csr);
+    } catch (...) {
+    }
+  }
+};
 }  // namespace
 
 extern "C" {
@@ -163,6 +224,7 @@ int gift_ctx_create(int device, gift_ctx** out) {
   auto* c = new gift_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&c->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   *out = c;
   GIFT_API_END
 }
@@ -170,7 +232,7 @@ int gift_ctx_create(int device, gift_ctx** out) {
 int gift_ctx_destroy(gift_ctx* ctx) {
   GIFT_API_BEGIN
   if (!ctx) return GIFT_OK;
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, nullptr);
   cudaStreamSynchronize(ctx->stream);
   for (int i = 0; i < 4; ++i)
     if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
@@ -205,7 +267,7 @@ int gift_ctx_set_profiling(gift_ctx* ctx, int on) {
 int gift_ctx_profile_drain(gift_ctx* ctx, int max_records, int* h_kind, int* h_units, float* h_ms, int* n_records) {
   GIFT_API_BEGIN
   require(ctx != nullptr, GIFT_ERR_VALUE, "null context");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, nullptr);
   GIFT_CUDA(cudaStreamSynchronize(ctx->stream));
   int k = 0;
   for (auto& r : ctx->recs) {
@@ -230,7 +292,7 @@ int gift_build_clique_graph(gift_ctx* ctx, int64_t n_cells, int64_t n_nets, cons
                             int64_t* n_skipped) {
   GIFT_API_BEGIN
   require(ctx && out, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, nullptr);
   *out = static_cast<gift_csr*>(
       gift::build_clique_graph(ctx, n_cells, n_nets, d_net_start, d_pin_cell, max_clique_pins, n_skipped));
   GIFT_API_END
@@ -240,7 +302,7 @@ int gift_csr_from_coo(gift_ctx* ctx, int64_t n, int64_t nnz, const int64_t* d_ro
                       const double* d_vals, int check_symmetric, gift_csr** out) {
   GIFT_API_BEGIN
   require(ctx && out, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, nullptr);
   *out = static_cast<gift_csr*>(gift::csr_from_coo(ctx, n, nnz, d_rows, d_cols, d_vals, check_symmetric != 0));
   GIFT_API_END
 }
@@ -273,7 +335,7 @@ int gift_csr_download(gift_ctx* ctx, const gift_csr* csr, int64_t* h_indptr, int
                       double* h_values) {
   GIFT_API_BEGIN
   require(ctx && csr, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, csr);
   if (h_indptr)
     GIFT_CUDA(cudaMemcpyAsync(h_indptr, csr->indptr, (csr->n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost,
                               ctx->stream));
@@ -290,7 +352,7 @@ int gift_csr_download(gift_ctx* ctx, const gift_csr* csr, int64_t* h_indptr, int
 int gift_csr_degrees(gift_ctx* ctx, gift_csr* csr, const double** d_degrees) {
   GIFT_API_BEGIN
   require(ctx && csr && d_degrees, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, csr);
   *d_degrees = gift::csr_degrees(ctx, csr);
   GIFT_API_END
 }
@@ -298,7 +360,7 @@ int gift_csr_degrees(gift_ctx* ctx, gift_csr* csr, const double** d_degrees) {
 int gift_normalized_augmented_adjacency(gift_ctx* ctx, gift_csr* adj, double sigma, gift_csr** out) {
   GIFT_API_BEGIN
   require(ctx && adj && out, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, adj);
   *out = static_cast<gift_csr*>(gift::normalized_augmented_adjacency(ctx, adj, sigma));
   GIFT_API_END
 }
@@ -307,7 +369,7 @@ int gift_csr_matmul(gift_ctx* ctx, const gift_csr* csr, int64_t ncols, const dou
   GIFT_API_BEGIN
   require(ctx && csr, GIFT_ERR_VALUE, "null argument");
   require(ncols >= 0, GIFT_ERR_DIMENSION, "negative column count");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, csr);
   gift::csr_matmul(ctx, csr, ncols, d_x, d_y);
   GIFT_API_END
 }
@@ -317,7 +379,7 @@ int gift_filter(gift_ctx* ctx, gift_csr* adj, int n_terms, const double* h_sigma
                 const uint8_t* d_fixed_mask, const double* d_fixed_pos, const double* h_region, int precision) {
   GIFT_API_BEGIN
   require(ctx && adj, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, adj);
   gift::filter(ctx, adj, n_terms, h_sigma, h_k, h_alpha, ncols, in_dtype, d_g, out_dtype, d_out, d_fixed_mask,
                d_fixed_pos, h_region, precision);
   GIFT_API_END
@@ -339,7 +401,7 @@ int gift_filter_host(gift_ctx* ctx, gift_csr* adj, int n_terms, const double* h_
                      const uint8_t* h_fixed_mask, const double* h_fixed_pos, const double* h_region, int precision) {
   GIFT_API_BEGIN
   require(ctx && adj, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, adj);
   cudaStream_t st = ctx->stream;
   const int64_t n = adj->n;
   const size_t in_b = (size_t)(n * ncols) * (in_dtype == GIFT_DTYPE_F64 ? 8 : 4);
@@ -375,7 +437,7 @@ int gift_place_host(gift_ctx* ctx, int64_t n_cells, int64_t n_nets, const int64_
                     int64_t* nnz_out) {
   GIFT_API_BEGIN
   require(ctx && h_net_start, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, nullptr);
   cudaStream_t st = ctx->stream;
   int64_t n_pins = h_net_start[n_nets];
   gift::DevBuf<int64_t> dns(ctx, n_nets + 1);
@@ -402,21 +464,16 @@ int gift_place_host(gift_ctx* ctx, int64_t n_cells, int64_t n_nets, const int64_
       GIFT_CUDA(cudaMemcpyAsync(dmask.p, h_fixed_mask, n, cudaMemcpyHostToDevice, st));
       if (!z_pos) GIFT_CUDA(cudaMemcpyAsync(dpos.p, h_fixed_pos, 2 * n * sizeof(double), cudaMemcpyHostToDevice, st));
     }
-    const bool bmt = ctx->bmt_enabled;
-    ctx->bmt_enabled = false;  // one-shot graph: the row kernel, no tiled copy
-    try {
-      gift::filter(ctx, c, n_terms, h_sigma, h_k, h_alpha, 2, GIFT_DTYPE_F32, dg.p, out_dtype,
-                   z_out ? z_out : dout.p, h_fixed_mask ? dmask.p : nullptr,
-                   h_fixed_mask ? (z_pos ? z_pos : dpos.p) : nullptr, h_region, precision);
-    } catch (...) {
-      ctx->bmt_enabled = bmt;
-      throw;
-    }
-    ctx->bmt_enabled = bmt;
+    // a one-shot graph: under the default policy (GIFT_TILED_ON_REUSE) its
+    // single bank runs the row kernel and no tiled copy is built
+    gift::filter(ctx, c, n_terms, h_sigma, h_k, h_alpha, 2, GIFT_DTYPE_F32, dg.p, out_dtype,
+                 z_out ? z_out : dout.p, h_fixed_mask ? dmask.p : nullptr,
+                 h_fixed_mask ? (z_pos ? z_pos : dpos.p) : nullptr, h_region, precision);
     if (!z_out) GIFT_CUDA(cudaMemcpyAsync(h_out, dout.p, out_b, cudaMemcpyDeviceToHost, st));
     GIFT_CUDA(cudaStreamSynchronize(st));
     if (nnz_out) *nnz_out = c->nnz;
   } catch (...) {
+    gift::csr_touch(ctx, c);
     gift::csr_destroy(c);
     throw;
   }
@@ -427,7 +484,7 @@ int gift_place_host(gift_ctx* ctx, int64_t n_cells, int64_t n_nets, const int64_
 int gift_csr_scale(gift_ctx* ctx, gift_csr* csr, double sigma, const double** d_s64, const float** d_s32) {
   GIFT_API_BEGIN
   require(ctx && csr, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, csr);
   gift::scale_vectors(ctx, csr, sigma, d_s64, d_s32);
   GIFT_API_END
 }
@@ -435,7 +492,7 @@ int gift_csr_scale(gift_ctx* ctx, gift_csr* csr, double sigma, const double** d_
 int gift_csr_weights32(gift_ctx* ctx, gift_csr* csr, const float** d_w32) {
   GIFT_API_BEGIN
   require(ctx && csr && d_w32, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, csr);
   *d_w32 = gift::weights32(ctx, csr);
   GIFT_API_END
 }
@@ -445,7 +502,7 @@ int gift_csr_from_arrays(gift_ctx* ctx, int64_t n_rows, int64_t nnz, const int64
   GIFT_API_BEGIN
   require(ctx && out && d_indptr, GIFT_ERR_VALUE, "null argument");
   require(n_rows >= 0 && nnz >= 0, GIFT_ERR_VALUE, "negative size");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, nullptr);
   *out = static_cast<gift_csr*>(gift::csr_from_arrays(ctx, n_rows, nnz, d_indptr, d_indices, d_values));
   GIFT_API_END
 }
@@ -453,7 +510,7 @@ int gift_csr_from_arrays(gift_ctx* ctx, int64_t n_rows, int64_t nnz, const int64
 int gift_hop_fp32(gift_ctx* ctx, gift_csr* csr, const gift_hop_desc* desc) {
   GIFT_API_BEGIN
   require(ctx && csr && desc, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, csr);
   gift::hop_fp32(ctx, csr, desc);
   GIFT_API_END
 }
@@ -463,7 +520,7 @@ int gift_pack_fp32(gift_ctx* ctx, int64_t n, int wcols, int nch, const float* co
   GIFT_API_BEGIN
   require(ctx && h_s, GIFT_ERR_VALUE, "null argument");
   require(nch >= 1 && nch <= 4 && wcols * nch <= F, GIFT_ERR_VALUE, "bad packing");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, nullptr);
   gift::pack_fp32(ctx, n, wcols, nch, h_s, in_dtype, d_g, ld, c0, F, d_z);
   GIFT_API_END
 }
@@ -472,7 +529,7 @@ int gift_gather_rows_f32(gift_ctx* ctx, int64_t n_idx, int F, const int64_t* d_i
                          float* d_dst) {
   GIFT_API_BEGIN
   require(ctx, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, nullptr);
   gift::gather_rows_f32(ctx, n_idx, F, d_idx, d_src, d_dst);
   GIFT_API_END
 }
@@ -480,7 +537,7 @@ int gift_gather_rows_f32(gift_ctx* ctx, int64_t n_idx, int F, const int64_t* d_i
 int gift_quadratic_wirelength(gift_ctx* ctx, const gift_csr* adj, const double* d_g, double* h_out) {
   GIFT_API_BEGIN
   require(ctx && adj && h_out, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, adj);
   *h_out = gift::quadratic_wirelength(ctx, adj, d_g);
   GIFT_API_END
 }
@@ -488,7 +545,7 @@ int gift_quadratic_wirelength(gift_ctx* ctx, const gift_csr* adj, const double* 
 int gift_laplacian(gift_ctx* ctx, gift_csr* adj, gift_csr** out) {
   GIFT_API_BEGIN
   require(ctx && adj && out, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, adj);
   *out = static_cast<gift_csr*>(gift::laplacian(ctx, adj));
   GIFT_API_END
 }
@@ -497,7 +554,7 @@ int gift_rayleigh_parts(gift_ctx* ctx, const gift_csr* lap, const double* d_col,
                         double* h_den) {
   GIFT_API_BEGIN
   require(ctx && lap && h_num && h_den, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, lap);
   gift::rayleigh_parts(ctx, lap, d_col, center != 0, h_num, h_den);
   GIFT_API_END
 }
@@ -506,7 +563,7 @@ int gift_hpwl(gift_ctx* ctx, int64_t n_nets, const int64_t* d_net_start, const i
               const double* d_pin_dx, const double* d_pin_dy, const double* d_g, double* h_out) {
   GIFT_API_BEGIN
   require(ctx && h_out, GIFT_ERR_VALUE, "null argument");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, nullptr);
   *h_out = gift::hpwl(ctx, n_nets, d_net_start, d_pin_cell, d_pin_dx, d_pin_dy, d_g);
   GIFT_API_END
 }
@@ -518,7 +575,7 @@ int gift_format_placement(gift_ctx* ctx, int64_t n, const double* d_pos, const d
   GIFT_API_BEGIN
   require(ctx && h_len && n >= 0, GIFT_ERR_VALUE, "null argument");
   require(n == 0 || d_pos, GIFT_ERR_VALUE, "null positions");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, nullptr);
   *h_len = gift::format_placement(ctx, n, d_pos, d_width, d_height, d_fixed, d_names, d_name_off, h_name_prefix,
                                   d_out, cap);
   GIFT_API_END
@@ -528,6 +585,56 @@ struct gift_bookshelf {
   gift::Bookshelf* b;
 };
 
+int gift_ctx_set_tiled_policy(gift_ctx* ctx, int policy) {
+  GIFT_API_BEGIN
+  require(ctx != nullptr, GIFT_ERR_VALUE, "null context");
+  require(policy == GIFT_TILED_NEVER || policy == GIFT_TILED_ON_REUSE || policy == GIFT_TILED_ALWAYS, GIFT_ERR_VALUE,
+          "unknown tiled policy");
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+  ctx->tiled_policy = policy;
+  GIFT_API_END
+}
+
+int gift_csr_row_bounds(gift_ctx* ctx, const gift_csr* csr, int world, int64_t* h_bounds) {
+  GIFT_API_BEGIN
+  require(ctx && csr && h_bounds, GIFT_ERR_VALUE, "null argument");
+  ApiScope g(ctx, csr);
+  gift::csr_row_bounds(ctx, csr, world, h_bounds);
+  GIFT_API_END
+}
+
+int gift_csr_split_rows(gift_ctx* ctx, const gift_csr* csr, int64_t r0, int64_t r1, gift_csr** local,
+                        gift_csr** ghost) {
+  GIFT_API_BEGIN
+  require(ctx && csr && local && ghost, GIFT_ERR_VALUE, "null argument");
+  ApiScope g(ctx, csr);
+  gift::Csr *L = nullptr, *G = nullptr;
+  gift::csr_split_rows(ctx, csr, r0, r1, &L, &G);
+  *local = static_cast<gift_csr*>(L);
+  *ghost = static_cast<gift_csr*>(G);
+  GIFT_API_END
+}
+
+int gift_csr_ext_ids(const gift_csr* ghost, const int64_t** d_ids, int64_t* n_ids) {
+  GIFT_API_BEGIN
+  require(ghost && d_ids && n_ids, GIFT_ERR_VALUE, "null argument");
+  *d_ids = ghost->ext_ids;
+  *n_ids = ghost->ext_n;
+  GIFT_API_END
+}
+
+int gift_csr_tiled_info(const gift_csr* csr, int which, int64_t* h_info) {
+  GIFT_API_BEGIN
+  require(csr && h_info, GIFT_ERR_VALUE, "null argument");
+  require(which == 0 || which == 1, GIFT_ERR_VALUE, "which must be 0 (F = 4 copy) or 1 (F <= 2 copy)");
+  gift::Csr* c = const_cast<gift_csr*>(csr);
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
+  const gift::Csr::Bmt& B = which == 0 ? c->bmt : c->bmt_wide;
+  const int64_t v[8] = {B.ready, B.ok, B.tile_rows, B.kC, B.nseg, B.nslices, B.slots, B.nwide};
+  for (int i = 0; i < 8; ++i) h_info[i] = v[i];
+  GIFT_API_END
+}
+
 int gift_bookshelf_parse(gift_ctx* ctx, const char* h_nodes, int64_t nodes_len, const char* h_nets,
                          int64_t nets_len, const char* h_pl, int64_t pl_len, gift_bookshelf** out) {
   GIFT_API_BEGIN
@@ -535,7 +642,7 @@ int gift_bookshelf_parse(gift_ctx* ctx, const char* h_nodes, int64_t nodes_len, 
   require(nodes_len >= 0 && nets_len >= 0 && pl_len >= 0, GIFT_ERR_VALUE, "negative length");
   require((h_nodes || !nodes_len) && (h_nets || !nets_len) && (h_pl || !pl_len), GIFT_ERR_VALUE, "null text");
   *out = nullptr;
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, nullptr);
   gift::Bookshelf* b = gift::bookshelf_parse(ctx, h_nodes, nodes_len, h_nets, nets_len, h_pl, pl_len);
   *out = new gift_bookshelf{b};
   GIFT_API_END
@@ -578,7 +685,7 @@ int gift_bookshelf_copy(gift_ctx* ctx, const gift_bookshelf* bs, int64_t* h_net_
                         int64_t* h_net_name_off) {
   GIFT_API_BEGIN
   require(ctx && bs && bs->b, GIFT_ERR_VALUE, "null handle");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, nullptr);
   const gift::Bookshelf& B = *bs->b;
   cudaStream_t st = ctx->stream;
   auto cp = [&](void* dst, const void* src, int64_t bytes) {
@@ -604,7 +711,7 @@ int gift_bookshelf_destroy(gift_ctx* ctx, gift_bookshelf* bs) {
   GIFT_API_BEGIN
   if (!bs) return GIFT_OK;
   require(ctx, GIFT_ERR_VALUE, "null context");
-  DeviceGuard g(ctx->device);
+  ApiScope g(ctx, nullptr);
   cudaStreamSynchronize(ctx->stream);
   gift::bookshelf_destroy(ctx, bs->b);
   delete bs;

@@ -96,6 +96,7 @@ constexpr int kPadRows = 16;      // one zero row per bank residue mod 16 (paddi
 constexpr int kStage = 1024;      // a segment with >= kStage entries stages its block
 constexpr int kBlock = 256;
 constexpr int kWide = 8;          // rows touching > max(kWide, 3 x mean) blocks run on the row kernel
+constexpr int kReuseHops = 4;     // GIFT_TILED_ON_REUSE: build once a graph has served this many fp32 hops
 
 __global__ void k_mark_rows(int64_t n, const int64_t* __restrict__ indptr, int32_t* __restrict__ mark) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
@@ -261,88 +262,122 @@ __global__ void k_scatter_runs(int64_t nseg, const int64_t* __restrict__ seg_run
 // step each lane takes an entry whose residue mod 16 is unused in its half and
 // whose residue mod 8 is unused in its quarter, preferring its most plentiful
 // residue; failing that, one free mod 8 only; failing that, its most plentiful.
-// Thread per half warp; tmp holds the lanes' entries bucketed by residue.
-__global__ void k_slice_schedule(int64_t nslices, int kC, const int64_t* __restrict__ slice_off, uint16_t* __restrict__ col,
-                                 float* __restrict__ w, uint16_t* __restrict__ tcol, float* __restrict__ tw) {
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nslices * 2;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t sl = g / 2;
-    const int lane0 = (int)(g % 2) * 16;
+// Padding (column kC, residue 0, after the lane's real entries) is a
+// wildcard: it can sit on any zero row kC + r, so it takes a residue no other
+// lane of its half / quarter uses.
+//
+// One warp per slice, lane = the slice's lane: each lane buckets its own run by
+// residue (counting sort into tmp), then the two halves decide step by step,
+// lane after lane, with the half's used-residue masks kept warp-uniform
+// through shuffles.  (The first version ran one thread per half slice over
+// [16][16] count tables: local-memory bound, 560 ms of the c3 build.)
+__global__ void __launch_bounds__(256) k_slice_schedule(int64_t nslices, int kC, const int64_t* __restrict__ slice_off,
+                                                        uint16_t* __restrict__ col, float* __restrict__ w,
+                                                        uint16_t* __restrict__ tcol, float* __restrict__ tw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t sl = warp0; sl < nslices; sl += nwarps) {
     const int64_t off = slice_off[sl];
     const int64_t L = (slice_off[sl + 1] - off) / 32;  // slots per lane
-    int cnt[16][16], cnt_real0[16];
-    int64_t next[16][16];
-    for (int l = 0; l < 16; ++l) {
-      cnt_real0[l] = 0;
-      for (int r = 0; r < 16; ++r) cnt[l][r] = 0;
+    int cnt[16];
+    int next[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) cnt[r] = 0;
+    int real0 = 0;
+    for (int64_t k = 0; k < L; ++k) {
+      const int cv = col[off + (k / 4) * 128 + lane * 4 + (k % 4)];
+      cnt[cv & 15]++;
+      real0 += ((cv & 15) == 0 && cv < kC);
     }
-    for (int l = 0; l < 16; ++l)
-      for (int64_t k = 0; k < L; ++k) {
-        const int cv = col[off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4)];
-        cnt[l][cv & 15]++;
-        cnt_real0[l] += ((cv & 15) == 0 && cv < kC);
-      }
-    for (int l = 0; l < 16; ++l) {
-      int64_t base = off + (int64_t)(lane0 + l) * L;
-      int64_t pos[16];
+    {
+      int acc = 0;
+#pragma unroll
       for (int r = 0; r < 16; ++r) {
-        next[l][r] = base;
-        pos[r] = base;
-        base += cnt[l][r];
+        next[r] = acc;
+        acc += cnt[r];
       }
+    }
+    const int64_t base = off + (int64_t)lane * L;
+    {
+      int pos[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) pos[r] = next[r];
       for (int64_t k = 0; k < L; ++k) {
-        const int64_t slot = off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4);
-        const int r = col[slot] & 15;
-        tcol[pos[r]] = col[slot];
-        tw[pos[r]] = w[slot];
+        const int64_t slot = off + (k / 4) * 128 + lane * 4 + (k % 4);
+        const uint16_t cv = col[slot];
+        const int r = cv & 15;
+        tcol[base + pos[r]] = cv;
+        tw[base + pos[r]] = w[slot];
         pos[r]++;
       }
     }
+    const int pad_first = next[0] + real0;  // first padding entry of bucket 0
+    int pads = cnt[0] - real0;
+    int reals0 = real0;
+    const int hl = lane & 15;        // position in the half
+    const int q = hl >> 3;           // quarter within the half
     for (int64_t k = 0; k < L; ++k) {
-      unsigned used16 = 0, used8[2] = {0, 0};
+      unsigned used16 = 0, used8 = 0;  // this lane's half: residues mod 16 / mod 8 (bits 0-7 quarter 0, 8-15 quarter 1)
       for (int l = 0; l < 16; ++l) {
-        const int q = l >> 3;
-        // padding (column kC, bucket 0, sorted after real residue-0 entries since
-        // kC is the largest value) is a wildcard: it can sit on any zero row
-        // kC + r, so it takes a residue no other lane of its half / quarter uses
-        const int64_t pad_first = next[l][0] + cnt_real0[l];
-        int best = -1, bestc = 0, ok8 = -1, ok8c = 0, any = -1, anyc = 0;
-        for (int r = 0; r < 16; ++r) {
-          const int c = (r == 0) ? cnt_real0[l] : cnt[l][r];
-          if (c <= 0) continue;
-          if (c > anyc) { anyc = c; any = r; }
-          if (!(used8[q] & (1u << (r & 7)))) {
-            if (c > ok8c) { ok8c = c; ok8 = r; }
-            if (!(used16 & (1u << r)) && c > bestc) { bestc = c; best = r; }
+        int choice = 0;  // residue | 16 if a padding wildcard
+        if (hl == l) {
+          unsigned avail = 0;
+#pragma unroll
+          for (int r = 0; r < 16; ++r) avail |= ((r == 0 ? reals0 : cnt[r]) > 0 ? 1u : 0u) << r;
+          const unsigned q8 = (used8 >> (8 * q)) & 0xffu;
+          const unsigned blocked = q8 | (q8 << 8);
+          const unsigned c_best = avail & ~used16 & ~blocked, c_ok8 = avail & ~blocked;
+          auto pick = [&](unsigned m) {
+            int best = -1, bc = 0;
+            while (m) {
+              const int r = __ffs(m) - 1;
+              m &= m - 1;
+              const int c = r == 0 ? reals0 : cnt[r];
+              if (c > bc) {
+                bc = c;
+                best = r;
+              }
+            }
+            return best;
+          };
+          int r = pick(c_best);
+          if (r < 0 && pads > 0) {
+            // no conflict-free real entry: a padding slot on a free zero row
+            const unsigned f16 = ~used16 & ~blocked & 0xffffu, f8 = ~blocked & 0xffffu;
+            r = f16 ? __ffs(f16) - 1 : (f8 ? __ffs(f8) - 1 : 0);
+            choice = r | 16;
+          } else {
+            if (r < 0) r = pick(c_ok8);
+            if (r < 0) r = pick(avail);
+            if (r < 0) r = 0;  // only padding left
+            choice = r;
           }
         }
-        const int64_t slot = off + (k / 4) * 128 + (lane0 + l) * 4 + (k % 4);
-        const int pads = cnt[l][0] - cnt_real0[l];
-        if (best < 0 && pads > 0) {
-          // no conflict-free real entry: place a padding slot on a free zero row
-          int r = -1;
-          for (int t = 0; t < 16 && r < 0; ++t)
-            if (!(used16 & (1u << t)) && !(used8[q] & (1u << (t & 7)))) r = t;
-          if (r < 0)
-            for (int t = 0; t < 16 && r < 0; ++t)
-              if (!(used8[q] & (1u << (t & 7)))) r = t;
-          if (r < 0) r = 0;
-          used16 |= 1u << r;
-          used8[q] |= 1u << (r & 7);
-          const int64_t src = pad_first + (pads - 1);
-          cnt[l][0]--;
-          col[slot] = (uint16_t)(kC + r);
-          w[slot] = tw[src];
-          continue;
+        const int got = __shfl_sync(0xffffffffu, choice, (lane & 16) | l);
+        const int rr = got & 15;
+        used16 |= 1u << rr;
+        used8 |= 1u << ((rr & 7) + 8 * (l >> 3));
+        if (hl == l) {
+          const int64_t slot = off + (k / 4) * 128 + lane * 4 + (k % 4);
+          if (got & 16) {  // padding wildcard (weight 0)
+            pads--;
+            cnt[0]--;
+            col[slot] = (uint16_t)(kC + rr);
+            w[slot] = tw[base + pad_first + pads];
+          } else if (rr == 0 && reals0 == 0) {  // residue 0 with only padding left: a plain padding slot
+            pads--;
+            cnt[0]--;
+            col[slot] = (uint16_t)kC;
+            w[slot] = tw[base + pad_first + pads];
+          } else {
+            const int src = next[rr]++;
+            cnt[rr]--;
+            if (rr == 0) reals0--;
+            col[slot] = tcol[base + src];
+            w[slot] = tw[base + src];
+          }
         }
-        const int r = best >= 0 ? best : (ok8 >= 0 ? ok8 : (any >= 0 ? any : 0));
-        used16 |= 1u << r;
-        used8[q] |= 1u << (r & 7);
-        const int64_t src = next[l][r]++;
-        cnt[l][r]--;
-        if (r == 0) cnt_real0[l]--;
-        col[slot] = tcol[src];
-        w[slot] = tw[src];
       }
     }
   }
@@ -928,20 +963,20 @@ template <int FIN, int FOUT, bool DB>
 void launch_bmt_k(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, int tpb, size_t smem) {
   auto kern = tpb == 1024 ? k_hop_bmt<FIN, FOUT, 1024, DB> : k_hop_bmt<FIN, FOUT, 512, DB>;
   static std::mutex mu;
-  static std::map<const void*, int> occ;  // resident CTAs per SM per instance (after the smem opt-in)
+  static std::map<std::pair<const void*, int>, int> occ;  // resident CTAs per SM per (instance, device)
   int per_sm = 0;
   {
     std::lock_guard<std::mutex> lk(mu);
-    auto it = occ.find((const void*)kern);
+    const auto key = std::make_pair((const void*)kern, ctx->device);
+    auto it = occ.find(key);
     if (it == occ.end()) {
-      int optin = 0;
-      GIFT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+      const int optin = ctx->smem_optin;
       cudaFuncAttributes fa{};
       GIFT_CUDA(cudaFuncGetAttributes(&fa, kern));
       GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      optin - (int)fa.sharedSizeBytes));
       GIFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tpb, smem));
-      occ[(const void*)kern] = per_sm;
+      occ[key] = per_sm;
     } else {
       per_sm = it->second;
     }
@@ -955,14 +990,19 @@ void launch_bmt_k(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, 
 template <int FIN, int FOUT, int kThreads>
 void launch_bmt_nb(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, size_t smem) {
   auto kern = k_hop_bmt_nb<FIN, FOUT, kThreads>;
-  static std::once_flag once;
-  std::call_once(once, [&]() {
-    int optin = 0;
-    GIFT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-    cudaFuncAttributes fa{};
-    GIFT_CUDA(cudaFuncGetAttributes(&fa, kern));
-    GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
-  });
+  // the smem opt-in is a per-device function attribute: set it once per device
+  static std::mutex mu;
+  static std::set<int> done;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done.count(ctx->device)) {
+      cudaFuncAttributes fa{};
+      GIFT_CUDA(cudaFuncGetAttributes(&fa, kern));
+      GIFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     ctx->smem_optin - (int)fa.sharedSizeBytes));
+      done.insert(ctx->device);
+    }
+  }
   kern<<<(unsigned)ntiles, kThreads, smem, ctx->stream>>>(a, b);
   GIFT_LAUNCH_CHECK(ctx);
 }
@@ -1267,8 +1307,8 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32, Csr::Bmt& B, bool wide_blocks
   if (env_int("GIFT_BMT_SCHEDULE", 1)) {
     DevBuf<uint16_t> tcol(ctx, total + 8);
     DevBuf<float> tw(ctx, total + 8);
-    k_slice_schedule<<<grid_for(nslices * 2, 128, 1LL << 30), 128, 0, st>>>(nslices, kC, B.slice_off, bcol, bw, tcol.p,
-                                                                           tw.p);
+    k_slice_schedule<<<grid_for(nslices * 32, 256, 1LL << 30), 256, 0, st>>>(nslices, kC, B.slice_off, bcol, bw,
+                                                                            tcol.p, tw.p);
     GIFT_LAUNCH_CHECK(ctx);
   }
   B.data = static_cast<uint8_t*>(csr_alloc(ctx, c, (total / 128 + 1) * 768));
@@ -1324,7 +1364,8 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32, Csr::Bmt& B, bool wide_blocks
 }  // namespace
 
 const float* csr_w32_public(Ctx* ctx, Csr* c);
-void launch_row_list(Ctx* ctx, const HopArgs& base, const int32_t* rows, int64_t nrows, int fin, int fout, int G);
+void launch_row_list(Ctx* ctx, cudaStream_t st, const HopArgs& base, const int32_t* rows, int64_t nrows, int fin,
+                     int fout, int G);
 
 bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
   if (env_int("GIFT_BMT", 1) == 0 || !c->sorted_rows || !c->square) return false;
@@ -1334,7 +1375,11 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
   const bool wide_blocks = fin <= 2 && env_int("GIFT_BMT_TILE_ROWS", 0) == 0 && env_int("GIFT_BMT_COL_BITS", 0) == 0 &&
                            env_int("GIFT_BMT_WIDE", 1);
   Csr::Bmt& B = wide_blocks ? c->bmt_wide : c->bmt;
-  if (!ctx->bmt_enabled && !B.ok) return false;
+  // build policy (GIFT_TILED_*): a graph filtered once (gift_place on a fresh
+  // design, cli.py:203-220) never pays for the copy; one filtered again gets it
+  if (!B.ready && (ctx->tiled_policy == GIFT_TILED_NEVER ||
+                   (ctx->tiled_policy == GIFT_TILED_ON_REUSE && c->fp32_hops < kReuseHops)))
+    return false;
   if (c->n < env_int("GIFT_BMT_MIN_ROWS", 262144) || c->mean_row < env_int("GIFT_BMT_MIN_MEAN", 32)) return false;
   if (a.row_begin != 0 || a.n != c->n || a.part_in) return false;  // part_out: the epilogue writes partials
   if (!B.ready) {
@@ -1355,11 +1400,8 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
     }
   }
   if (!B.ok) return false;
-  {  // a tuning shape may not fit this signal width's shared-memory footprint
-    static int optin = 0;
-    if (!optin) GIFT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-    if (bmt_smem(fin, B.tile_rows, B.kC) + 1024 > (size_t)optin) return false;
-  }
+  // a tuning shape may not fit this signal width's shared-memory footprint
+  if (bmt_smem(fin, B.tile_rows, B.kC) + 1024 > (size_t)ctx->smem_optin) return false;
   // the wide rows (pads / macros, long rows) run concurrently on a side stream:
   // disjoint output rows, same input signal
   const bool fork = B.nwide > 0;
@@ -1371,10 +1413,7 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
     }
     GIFT_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
     GIFT_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
-    cudaStream_t main = ctx->stream;
-    ctx->stream = ctx->side;
-    launch_row_list(ctx, a, B.wide_rows, B.nwide, fin, fout, 32);
-    ctx->stream = main;
+    launch_row_list(ctx, ctx->side, a, B.wide_rows, B.nwide, fin, fout, 32);
     GIFT_CUDA(cudaEventRecord(ctx->join_ev, ctx->side));
   }
   unsigned* ctr = nullptr;

@@ -38,7 +38,7 @@ __global__ void k_pair_counts(int64_t n_nets, const int64_t* __restrict__ net_st
     int64_t m = net_start[e + 1] - net_start[e];
     int64_t c = 0;
     if (m >= 2) {
-      if (cap > 0 && m > cap) atomicAdd(skipped, 1ULL);
+      if (cap >= 0 && m > cap) atomicAdd(skipped, 1ULL);  // graph.py:136-138; cap < 0 = None
       else c = m * (m - 1) / 2;
     }
     counts[e] = c;

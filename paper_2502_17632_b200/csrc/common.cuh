@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -49,7 +50,9 @@ struct Ctx {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   int64_t launches = 0;
   int num_sms = 148;
-  bool bmt_enabled = true;        // false: one-shot calls skip building the tiled copy
+  int smem_optin = 0;             // max dynamic shared memory per block (opt-in), this device
+  int tiled_policy = GIFT_TILED_ON_REUSE;  // when the fp32 hop builds the tiled (BMT) copy of a graph
+  std::recursive_mutex mu;        // entry points serialise on the context (scratch, stream, logs)
   // persistent BMT tile scheduler counters [next tile, finished CTAs], one
   // pair per stream (launches on one stream never overlap; self-resetting)
   std::map<cudaStream_t, unsigned*> tile_ctr;
@@ -164,7 +167,12 @@ struct Csr {
     uint8_t* data = nullptr;        // [slots / 128] 768-byte records: 32x4 u16 columns (kC = padding),
                                     // then 32x4 f32 weights
   } bmt, bmt_wide;  // bmt_wide: signal widths <= 2; bmt: F = 4 (bmt.cu bmt_shape_for)
+  int64_t fp32_hops = 0;          // fp32 hop launches served (tiled-copy policy: build on reuse)
+  int64_t ext_n = 0;              // ghost block of a row shard: its columns >= n index these
+  int64_t* ext_ids = nullptr;     // [ext_n] global ids of the ghost columns, ascending
   std::vector<void*> owned;       // everything above, freed on destroy
+  std::recursive_mutex mu;        // lazy derived state (degrees, w32, s_sigma, tiled copies)
+  cudaEvent_t last_use = nullptr; // recorded on the using stream by every entry point; destroy waits on it
 };
 
 // a parsed Bookshelf design (bookshelf.cu): device arrays owned by the handle
@@ -183,6 +191,7 @@ struct Bookshelf {
 
 void* csr_alloc(Ctx* ctx, Csr* c, size_t bytes);
 void csr_destroy(Csr* c);
+void csr_touch(Ctx* ctx, Csr* c);
 
 // ---- launch helpers --------------------------------------------------------
 inline unsigned grid_for(int64_t work, int block, int64_t cap = 148LL * 64) {

@@ -361,13 +361,12 @@ int pow2_ceil(int v) {
 }
 
 template <int FIN, int FOUT>
-void launch_hop_g(Ctx* ctx, const HopArgs& a, int G) {
+void launch_hop_g(Ctx* ctx, cudaStream_t st, const HopArgs& a, int G) {
   if (a.n <= a.row_begin) return;
   G = env_int("GIFT_HOP_G", G);
   const int U = env_int("GIFT_HOP_U", 1);
   const int64_t threads = (a.n - a.row_begin) * (int64_t)G;
   const unsigned grid = (unsigned)((threads + kBlock - 1) / kBlock);
-  cudaStream_t st = ctx->stream;
   if (U >= 2) {
     switch (G) {
       case 8: k_hop<FIN, FOUT, 8, 2><<<grid, kBlock, 0, st>>>(a); break;
@@ -385,27 +384,29 @@ void launch_hop_g(Ctx* ctx, const HopArgs& a, int G) {
 }
 
 template <int FIN>
-void launch_hop_out(Ctx* ctx, const HopArgs& a, int fout, int G) {
+void launch_hop_out(Ctx* ctx, cudaStream_t st, const HopArgs& a, int fout, int G) {
   switch (fout) {
-    case 0: launch_hop_g<FIN, 0>(ctx, a, G); break;
-    case 1: launch_hop_g<FIN, 1>(ctx, a, G); break;
-    case 2: launch_hop_g<FIN, 2>(ctx, a, G); break;
-    default: launch_hop_g<FIN, 4>(ctx, a, G); break;
+    case 0: launch_hop_g<FIN, 0>(ctx, st, a, G); break;
+    case 1: launch_hop_g<FIN, 1>(ctx, st, a, G); break;
+    case 2: launch_hop_g<FIN, 2>(ctx, st, a, G); break;
+    default: launch_hop_g<FIN, 4>(ctx, st, a, G); break;
   }
 }
 
 }  // namespace
 
-// row kernel over an explicit row list (bmt.cu: the wide rows it leaves out)
-void launch_row_list(Ctx* ctx, const HopArgs& base, const int32_t* rows, int64_t nrows, int fin, int fout, int G) {
+// row kernel over an explicit row list on stream st (bmt.cu: the wide rows
+// it leaves out, on the context's side stream)
+void launch_row_list(Ctx* ctx, cudaStream_t st, const HopArgs& base, const int32_t* rows, int64_t nrows, int fin,
+                     int fout, int G) {
   HopArgs a = base;
   a.row_list = rows;
   a.row_begin = 0;
   a.n = nrows;
   switch (fin) {
-    case 1: launch_hop_out<1>(ctx, a, fout, G); break;
-    case 2: launch_hop_out<2>(ctx, a, fout, G); break;
-    default: launch_hop_out<4>(ctx, a, fout, G); break;
+    case 1: launch_hop_out<1>(ctx, st, a, fout, G); break;
+    case 2: launch_hop_out<2>(ctx, st, a, fout, G); break;
+    default: launch_hop_out<4>(ctx, st, a, fout, G); break;
   }
 }
 
@@ -413,11 +414,13 @@ namespace {
 
 void launch_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout, int G, bool allow_bmt) {
   ProfScope prof(ctx, fin, a.nch);
-  if (allow_bmt && bmt_hop(ctx, c, a, fin, fout)) return;
+  const bool tiled = allow_bmt && bmt_hop(ctx, c, a, fin, fout);
+  c->fp32_hops++;
+  if (tiled) return;
   switch (fin) {
-    case 1: launch_hop_out<1>(ctx, a, fout, G); break;
-    case 2: launch_hop_out<2>(ctx, a, fout, G); break;
-    default: launch_hop_out<4>(ctx, a, fout, G); break;
+    case 1: launch_hop_out<1>(ctx, ctx->stream, a, fout, G); break;
+    case 2: launch_hop_out<2>(ctx, ctx->stream, a, fout, G); break;
+    default: launch_hop_out<4>(ctx, ctx->stream, a, fout, G); break;
   }
 }
 

@@ -169,7 +169,7 @@ def gift_place_arrays(net_start, pin_cell, g0, fixed_mask, fixed_pos, region, te
     sig, kk, al = _term_arrays(terms)
     out = np.empty((n, 2), dtype=out_dtype)
     nnz = ctypes.c_int64(0)
-    cap = int(max_clique_pins) if max_clique_pins is not None else -1
+    cap = max(int(max_clique_pins), 0) if max_clique_pins is not None else -1  # -1 = None
     _lib.check(lib.gift_place_host(
         ctx, n, len(net_start) - 1, net_start.ctypes.data_as(ctypes.c_void_p),
         pin_cell.ctypes.data_as(ctypes.c_void_p), cap, len(sig), sig.ctypes.data_as(_lib.c_dp),

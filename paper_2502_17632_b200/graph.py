@@ -165,6 +165,19 @@ class SparseSymMatrix:
             raise DimensionMismatchError(f"signal has {g.shape[0]} rows, operator expects {self.n}")
         return _matmul_power(self, g, 1)
 
+    def tiled_info(self) -> dict:
+        """State of the graph's tiled (block-major) copies used by the fp32
+        bank: {"f4": {...}, "f2": {...}} with built / usable flags, tile shape
+        (rows x block columns), segments, slices, stored slots and the number
+        of rows left to the row kernel."""
+        out = {}
+        for which, name in ((0, "f4"), (1, "f2")):
+            info = (ctypes.c_int64 * 8)()
+            _lib.check(self._lib.gift_csr_tiled_info(self._h, which, info))
+            keys = ("built", "usable", "tile_rows", "block_cols", "segments", "slices", "slots", "wide_rows")
+            out[name] = dict(zip(keys, [int(v) for v in info]))
+        return out
+
     def to_dense(self, limit: int = DENSE_LIMIT) -> np.ndarray:
         if self.n > limit:
             raise TooLargeForDenseError(self.n, limit)
@@ -236,7 +249,7 @@ def build_clique_graph(design, max_clique_pins: int | None = None) -> SparseSymM
     ctx = _lib.context()
     d_ns = torch.from_numpy(np.ascontiguousarray(net_start, dtype=np.int64)).cuda()
     d_pc = torch.from_numpy(np.ascontiguousarray(pin_cell, dtype=np.int32)).cuda()
-    cap = int(max_clique_pins) if max_clique_pins is not None else -1
+    cap = max(int(max_clique_pins), 0) if max_clique_pins is not None else -1  # -1 = None
     h = ctypes.c_void_p()
     skipped = ctypes.c_int64(0)
     _lib.check(lib.gift_build_clique_graph(ctx, n, len(net_start) - 1, _lib.dptr(d_ns), _lib.dptr(d_pc), cap,

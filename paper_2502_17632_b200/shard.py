@@ -148,8 +148,10 @@ def nnz_balanced_bounds(indptr: np.ndarray, world: int) -> np.ndarray:
 
 @dataclass
 class ShardPlan:
-    """Rank-local view: local/ghost CSR blocks (remapped columns) and the
-    exchange lists.  Column ids index z_ext = [owned rows | ghost rows]."""
+    """This rank's exchange lists.  Column ids of its blocks index
+    z_ext = [owned rows | ghost rows]; `ghosts` are the global ids of the
+    ghost rows, ascending (grouped by owner, since owners hold contiguous
+    row ranges)."""
 
     world: int
     rank: int
@@ -160,12 +162,6 @@ class ShardPlan:
     recv_counts: list[int]      # ghosts owned by each rank (grouped, ascending)
     send_counts: list[int]      # rows each rank asked this rank for
     send_rows: np.ndarray       # local row ids to pack, grouped by destination rank
-    local_indptr: np.ndarray    # entries with owned columns
-    local_indices: np.ndarray
-    local_pos: np.ndarray       # positions of those entries in the global value array
-    ghost_indptr: np.ndarray    # entries with ghost columns
-    ghost_indices: np.ndarray
-    ghost_pos: np.ndarray
 
     @property
     def n_local(self) -> int:
@@ -176,7 +172,11 @@ class ShardPlan:
         return len(self.ghosts)
 
 
-def _split_block(indptr, indices, r0, r1):
+def split_block(indptr, indices, r0, r1):
+    """Host restatement of gift_csr_split_rows (csrc/shard.cu), used by the CPU
+    tests: rows [r0, r1) -> (ghosts, local block, ghost block); a block is
+    (indptr, remapped int32 columns, positions of its entries in the full
+    value array), entry order kept."""
     lo, hi = int(indptr[r0]), int(indptr[r1])
     cols = np.asarray(indices[lo:hi], dtype=np.int64)
     rowlen = np.diff(np.asarray(indptr[r0:r1 + 1], dtype=np.int64))
@@ -191,26 +191,26 @@ def _split_block(indptr, indices, r0, r1):
         np.cumsum(cnt, out=ptr[1:])
         return ptr, remap.astype(np.int32), pos[mask]
 
-    l_ptr, l_idx, l_pos = block(owned, cols[owned] - r0)
-    g_ptr, g_idx, g_pos = block(~owned, (r1 - r0) + np.searchsorted(ghosts, cols[~owned]))
-    return ghosts, (l_ptr, l_idx, l_pos), (g_ptr, g_idx, g_pos)
+    loc = block(owned, cols[owned] - r0)
+    gh = block(~owned, (r1 - r0) + np.searchsorted(ghosts, cols[~owned]))
+    return ghosts, loc, gh
 
 
-def make_shard_plan(indptr, indices, world: int, rank: int, exchange_ids) -> ShardPlan:
-    """Build this rank's plan.  `exchange_ids(send_lists) -> recv_lists` is an
-    all-to-all of int64 id lists (setup only): rank p tells each owner which
-    of its rows it needs."""
-    bounds = nnz_balanced_bounds(indptr, world)
+def exchange_plan(bounds, rank: int, ghosts, exchange_ids) -> ShardPlan:
+    """This rank's plan from the row bounds and its ghost ids.
+    `exchange_ids(send_lists) -> recv_lists` is an all-to-all of int64 id lists
+    (setup only): rank p tells each owner which of its rows it needs."""
+    bounds = np.asarray(bounds, dtype=np.int64)
+    world = len(bounds) - 1
     r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
-    ghosts, loc, gh = _split_block(indptr, indices, r0, r1)
+    ghosts = np.asarray(ghosts, dtype=np.int64)
     owner = np.searchsorted(bounds, ghosts, side="right") - 1
     requests = [ghosts[owner == q] for q in range(world)]
     recv_counts = [len(x) for x in requests]
     asked = exchange_ids(requests)  # asked[q] = my rows rank q needs (global ids)
     send_counts = [len(x) for x in asked]
     send_rows = (np.concatenate(asked) - r0).astype(np.int64) if asked else np.zeros(0, np.int64)
-    return ShardPlan(world, rank, bounds, r0, r1, ghosts, recv_counts, send_counts, send_rows,
-                     loc[0], loc[1], loc[2], gh[0], gh[1], gh[2])
+    return ShardPlan(world, rank, bounds, r0, r1, ghosts, recv_counts, send_counts, send_rows)
 
 
 # ------------------------------------------------------------------ exchange
@@ -322,17 +322,6 @@ class CudaBackend:
     def upload(self, arr):
         return self.torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{self.device}")
 
-    def block(self, indptr, indices, values):
-        """Local row block -> gift_csr handle (values fp64; fp32 copy made lazily)."""
-        d_ptr = self.upload(np.asarray(indptr, np.int64))
-        d_idx = self.upload(np.asarray(indices, np.int32))
-        d_val = self.upload(np.asarray(values, np.float64))
-        h = ctypes.c_void_p()
-        self._lib.check(self.lib.gift_csr_from_arrays(self.ctx(), len(indptr) - 1, len(indices),
-                                                      self._lib.dptr(d_ptr), self._lib.dptr(d_idx),
-                                                      self._lib.dptr(d_val), ctypes.byref(h)))
-        return _Handle(self.lib, h.value)
-
     def pack(self, n, wcols, groups_s, g, ld, c0, F, z):
         arr = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(p) for p in groups_s] + [None] * (4 - len(groups_s)))
         in_dtype = self._lib.GIFT_DTYPE_F32 if g.dtype == self.torch.float32 else self._lib.GIFT_DTYPE_F64
@@ -405,20 +394,20 @@ def _hop_desc(d: dict) -> _HopDesc:
 class ShardedFilter:
     """Runs the bank on this rank's row block with per-hop ghost exchange.
 
-    plan      : ShardPlan
-    values    : global fp64 CSR values (host) -- only this block's are used
-    s_by_sigma: {sigma: handle-to-local s32} backend-specific (device pointers
-                for CudaBackend, numpy arrays for tests)
+    plan        : ShardPlan
+    local, ghost: this rank's two CSR blocks (backend handles: gift_csr for
+                  CudaBackend, scipy matrices for the CPU tests)
+    s_of        : sigma -> this block's s32 (backend handle)
     """
 
-    def __init__(self, plan: ShardPlan, values: np.ndarray, backend, exchange, s_of):
+    def __init__(self, plan: ShardPlan, local, ghost, backend, exchange, s_of):
         self.plan = plan
         self.be = backend
         self.ex = exchange
         self.ex.plan = plan
-        self.s_of = s_of  # sigma -> this block's s32 (backend handle)
-        self.local = backend.block(plan.local_indptr, plan.local_indices, values[plan.local_pos])
-        self.ghost = backend.block(plan.ghost_indptr, plan.ghost_indices, values[plan.ghost_pos])
+        self.s_of = s_of
+        self.local = local
+        self.ghost = ghost
         n, ng = plan.n_local, plan.n_ghost
         self.zA = backend.empty(n + ng, 4)
         self.zB = backend.empty(n + ng, 4)
@@ -477,15 +466,32 @@ class ShardedFilter:
 
 def cuda_sharded_filter(adj, world: int, rank: int, device: int, exchange=None, group=None) -> ShardedFilter:
     """Set up this rank's share of `adj` (a full SparseSymMatrix resident on
-    `device`, built replicated on every rank).  s_sigma comes from the full
-    graph's degrees, sliced to the block, so it is the single-GPU vector."""
+    `device`, built on every rank) without a host copy of the graph: row
+    bounds and the local / ghost split run on the device
+    (gift_csr_row_bounds / gift_csr_split_rows); only the ghost id list
+    (halo + fixed objects, ~1e5 ids at c4) comes to the host for the exchange
+    plan.  s_sigma comes from the full graph's degrees, sliced to the block,
+    so it is the single-GPU vector."""
     from . import _lib
 
     be = CudaBackend(device)
     ex = exchange or TorchExchange(group=group, device=f"cuda:{device}")
-    indptr = np.asarray(adj.indptr, dtype=np.int64)
-    plan = make_shard_plan(indptr, adj.indices, world, rank, ex.ids)
     lib = _lib.load_library()
+    ctx = _lib.context(device)
+    bounds = np.zeros(world + 1, dtype=np.int64)
+    _lib.check(lib.gift_csr_row_bounds(ctx, adj.handle, world, bounds.ctypes.data_as(_lib.c_i64p)))
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    hl, hg = ctypes.c_void_p(), ctypes.c_void_p()
+    _lib.check(lib.gift_csr_split_rows(ctx, adj.handle, r0, r1, ctypes.byref(hl), ctypes.byref(hg)))
+    local, ghost = _Handle(lib, hl.value), _Handle(lib, hg.value)
+    ids_p, n_ids = ctypes.c_void_p(), ctypes.c_int64()
+    _lib.check(lib.gift_csr_ext_ids(ghost.h, ctypes.byref(ids_p), ctypes.byref(n_ids)))
+    ghosts = np.empty(n_ids.value, dtype=np.int64)
+    if n_ids.value:
+        from .graph import _memcpy_d2h
+
+        _memcpy_d2h(ghosts, ids_p.value)
+    plan = exchange_plan(bounds, rank, ghosts, ex.ids)
     cache: dict = {}
 
     def s_of(sigma):
@@ -497,4 +503,14 @@ def cuda_sharded_filter(adj, world: int, rank: int, device: int, exchange=None, 
             cache[sigma] = (s32.value or 0) + 4 * plan.r0
         return cache[sigma]
 
-    return ShardedFilter(plan, np.asarray(adj.values), be, ex, s_of)
+    for sigma in {t.sigma for t in _default_terms()}:  # the usual bank's vectors, before any rank thread runs
+        s_of(sigma)
+    sf = ShardedFilter(plan, local, ghost, be, ex, s_of)
+    sf._adj = adj  # s_sigma slices point into the full graph's arrays
+    return sf
+
+
+def _default_terms():
+    from .gift import DEFAULT_TERMS
+
+    return DEFAULT_TERMS

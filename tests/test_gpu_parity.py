@@ -32,6 +32,14 @@ def gb():
     return gb
 
 
+@pytest.fixture
+def tiled_always(gb):
+    """Build the tiled copy on a graph's first fp32 hop (default: on reuse)."""
+    gb.set_tiled_policy("always")
+    yield
+    gb.set_tiled_policy("on_reuse")
+
+
 def sha(a) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
@@ -178,20 +186,107 @@ def _oracle_parity(gb, orc, fd, cap, seed=0, check_place=True):
     return adj, ref
 
 
+def _configs_meta():
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "configs_meta.json")) as f:
+        return json.load(f)["samples"]
+
+
+def _reference_hashes(gb, adj, fd, meta, name):
+    """The CUDA path against hashes the reference itself produced
+    (tests/golden/make_golden_configs.py): CSR, degrees, the fp64 filter of
+    the fp32-rounded seed and the fp64 placement, bit for bit."""
+    assert adj.nnz == meta["nnz"], name
+    assert sha(np.asarray(adj.indptr, np.int64)) == meta["indptr_sha"], f"{name}: indptr"
+    assert sha(np.asarray(adj.indices, np.int64)) == meta["indices_sha"], f"{name}: indices"
+    assert sha(np.asarray(adj.values, np.float64)) == meta["values_sha"], f"{name}: values"
+    assert sha(np.asarray(adj.degrees, np.float64)) == meta["degrees_sha"], f"{name}: degrees"
+    cfg = gb.GiftConfig(seed=0, jitter_scale=10.0, precision="fp64")
+    g0 = gb.initial_signal(fd, cfg)
+    assert sha(g0) == meta["g0_sha"], f"{name}: seed signal"
+    g32 = g0.astype(np.float32).astype(np.float64)
+    assert sha(gb.gift_filter(adj, g32, cfg)) == meta["filter_g32_sha"], f"{name}: fp64 filter"
+    placed, _ = gb.gift_place(fd, adj, cfg)
+    assert sha(placed) == meta["place_sha"], f"{name}: fp64 placement"
+
+
 def test_c1_full_size_matches_oracle(gb, orc):
     from paper_2502_17632_b200 import synth
 
     fd = synth.generate("c1", seed=1)
-    _oracle_parity(gb, orc, fd, None)
+    adj, _ = _oracle_parity(gb, orc, fd, None)
+    _reference_hashes(gb, adj, fd, _configs_meta()["c1_full"], "c1_full")
 
 
-@pytest.mark.parametrize("config,scale,cap", [("c2", 0.05, 200), ("c3", 0.03, 200), ("c4", 0.004, 100),
-                                              ("c2", 0.01, None)])
+SAMPLES = {("c2", 0.05, 200): "c2_s005", ("c3", 0.03, 200): "c3_s003", ("c4", 0.004, 100): "c4_s0004",
+           ("c2", 0.01, None): "c2_s001_uncapped"}
+
+
+@pytest.mark.parametrize("config,scale,cap", list(SAMPLES))
 def test_heavy_tail_configs_scaled_match_oracle(gb, orc, config, scale, cap):
     from paper_2502_17632_b200 import synth
 
     fd = synth.generate(config, seed=2, scale=scale, window=600)
-    _oracle_parity(gb, orc, fd, cap, check_place=(config != "c4"))
+    adj, _ = _oracle_parity(gb, orc, fd, cap, check_place=(config != "c4"))
+    name = SAMPLES[(config, scale, cap)]
+    _reference_hashes(gb, adj, fd, _configs_meta()[name], name)
+
+
+# Default tiled-copy shapes (csrc/bmt.cu bmt_shape_for): F = 4 copy 8192 x 4096
+# on long-row graphs (c3), 4096 x 8192 on short-row ones (c4); F <= 2 copy
+# 8192 x 16384 on both.
+FULL_SHAPES = {"c3": ((8192, 4096), (8192, 16384)), "c4": ((4096, 8192), (8192, 16384))}
+
+
+@pytest.mark.parametrize("config", ["c3", "c4"])
+def test_full_size_bench_config_matches_oracle(gb, orc, config):
+    """The exact workload bench.py times (full-size config, seed 1, fp32
+    seed of synth.signal_fp32, default bank) on the default kernel selection:
+    the first bank on the graph runs the row kernel, the second builds and
+    runs the tiled copies (8192-row tiles, 1024-thread CTAs, wide rows on the
+    side stream).  CSR + degrees bit-exact against the oracle, both banks and
+    the fused placement within 1e-5 relative L2."""
+    from paper_2502_17632_b200 import synth
+
+    fd = synth.generate(config, seed=1)
+    cap = fd.meta["max_clique_pins"]
+    adj = gb.build_clique_graph(fd, max_clique_pins=cap)
+    ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, cap)
+    assert adj.nnz == ref.nnz
+    assert np.array_equal(np.asarray(adj.indptr, np.int64), ref.indptr)
+    assert np.array_equal(np.asarray(adj.indices, np.int64), ref.indices)
+    assert_bits_equal(adj.values, ref.data, f"{config}: values")
+    deg = orc.degrees(ref)
+    assert_bits_equal(adj.degrees, deg, f"{config}: degrees")
+    adj._host = None  # drop the host mirror (GBs) before the filter runs
+    g32 = synth.signal_fp32(fd, seed=0)
+    want = orc.gift_filter(ref, g32.astype(np.float64), DEFAULT, deg)
+    centre = np.array(fd.region.center)
+    info0 = adj.tiled_info()
+    assert not info0["f4"]["built"] and not info0["f2"]["built"]
+    first = gb.gift_filter(adj, g32)  # one-shot bank: row kernel
+    assert not adj.tiled_info()["f4"]["built"]
+    second = gb.gift_filter(adj, g32)  # graph reused: tiled copies built and used
+    info = adj.tiled_info()
+    for key, shape in zip(("f4", "f2"), FULL_SHAPES[config]):
+        assert info[key]["built"] and info[key]["usable"], (key, info)
+        assert (info[key]["tile_rows"], info[key]["block_cols"]) == shape, (key, info)
+    for got in (first, second):
+        assert rel_l2(got, want) <= FP32_TOL
+        assert rel_l2(got - centre, want - centre) <= FP32_TOL
+    # placement through the fused epilogue on the tiled kernels
+    r = fd.region
+    mask = fd.fixed_mask()
+    g0 = gb.initial_signal(fd, gb.GiftConfig(seed=0, jitter_scale=10.0))
+    want_p = orc.place_epilogue(orc.gift_filter(ref, g0, DEFAULT, deg), mask, fd.fixed_positions(),
+                                [r.xmin, r.ymin, r.xmax, r.ymax])
+    got_p, _ = gb.gift_place(fd, adj, gb.GiftConfig(seed=0, jitter_scale=10.0))
+    assert rel_l2(got_p, want_p) <= FP32_TOL
+    assert np.array_equal(got_p[mask], fd.fixed_positions()[mask])
+    # the tiled bank is deterministic
+    assert np.array_equal(gb.gift_filter(adj, g32), second)
 
 
 def test_place_host_abi_end_to_end(gb, orc):
@@ -360,6 +455,7 @@ def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, monkeypatch, world,
     if tiled:
         monkeypatch.setenv("GIFT_BMT_MIN_ROWS", "1")
         monkeypatch.setenv("GIFT_BMT_MIN_MEAN", "1")
+        gb.set_tiled_policy("always")
 
     fd = synth.generate("c2", seed=4, scale=0.02, window=600)
     adj = gb.build_clique_graph(fd, max_clique_pins=200)
@@ -398,6 +494,7 @@ def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, monkeypatch, world,
     ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, 200)
     want = orc.place_epilogue(orc.gift_filter(ref, g32.astype(np.float64), DEFAULT), fd.fixed_mask(),
                               fd.fixed_positions(), fd.region.bounds())
+    gb.set_tiled_policy("on_reuse")
     assert rel_l2(full, want) <= FP32_TOL
     mask = fd.fixed_mask()
     assert np.array_equal(full[mask], fd.fixed_positions()[mask])
@@ -410,8 +507,8 @@ def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, monkeypatch, world,
     ("c1", 0.2, None, 4096, 1, 0, 1), ("c3", 0.03, 200, 2048, 0, 0, 0), ("c1", 0.2, None, 8192, 0, 0, 0),
     ("c2", 0.05, 200, 2048, 1, 12, 0), ("c1", 0.2, None, 4096, 1, 13, 0), ("c1", 0.2, None, 8192, 1, 12, 0),
     ("c4", 0.02, 100, 4096, 1, 13, 1), ("c4", 0.02, 100, 2048, 1, 11, 1), ("c2", 0.05, 200, 2048, 1, 14, 1)])
-def test_bmt_hop_matches_oracle_and_row_kernel(gb, orc, monkeypatch, config, scale, cap, tile_rows, db, col_bits,
-                                               nb):
+def test_bmt_hop_matches_oracle_and_row_kernel(gb, orc, monkeypatch, tiled_always, config, scale, cap, tile_rows, db,
+                                               col_bits, nb):
     """Force the block-major tiled hop (bmt.cu) on small graphs (it is normally
     reserved for >= 256k rows) and check it against the oracle and the
     row-parallel kernel; tile heights 2048 / 4096 / 8192, column blocks of
@@ -436,6 +533,8 @@ def test_bmt_hop_matches_oracle_and_row_kernel(gb, orc, monkeypatch, config, sca
     monkeypatch.setenv("GIFT_BMT_MIN_MEAN", "1")
     adj = gb.build_clique_graph(fd, max_clique_pins=cap)
     tiled = gb.gift_filter(adj, g32)
+    info = adj.tiled_info()
+    assert info["f4"]["built"] or info["f2"]["built"], info
     assert rel_l2(tiled, want) <= FP32_TOL
     assert rel_l2(tiled, row_kernel) <= 1e-6
     again = gb.gift_filter(adj, g32)
@@ -540,3 +639,93 @@ def test_filter_host_pinned_in_place_matches_staged(gb, config, scale):
 
 
 
+
+
+@pytest.mark.parametrize("cap", [0, 1, -3, 2])
+def test_small_caps_skip_nets_like_the_reference(gb, orc, cap):
+    """graph.py:136: a net is skipped when m > max_clique_pins, so any cap < 2
+    leaves no edge at all (0 is a cap, not "no cap")."""
+    from paper_2502_17632_b200 import synth
+
+    fd = synth.generate("c0", seed=3, scale=0.1)
+    adj = gb.build_clique_graph(fd, max_clique_pins=cap)
+    ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, cap)
+    assert adj.nnz == ref.nnz
+    if cap < 2:
+        assert adj.nnz == 0
+    else:
+        assert adj.nnz > 0
+        csr_equal(adj, ref.indptr, ref.indices, ref.data, f"cap {cap}")
+
+
+def test_tiled_policy(gb, monkeypatch):
+    """GIFT_TILED_ON_REUSE (default): the first bank on a graph runs the row
+    kernel and leaves no tiled copy; the second builds it.  NEVER never builds;
+    ALWAYS builds on the first hop.  Results agree within fp32 rounding."""
+    from paper_2502_17632_b200 import synth
+
+    monkeypatch.setenv("GIFT_BMT_MIN_ROWS", "1")
+    monkeypatch.setenv("GIFT_BMT_MIN_MEAN", "1")
+    fd = synth.generate("c2", seed=3, scale=0.02, window=600)
+    g32 = synth.signal_fp32(fd, seed=1)
+    adj = gb.build_clique_graph(fd, max_clique_pins=200)
+    a = gb.gift_filter(adj, g32)
+    assert not adj.tiled_info()["f4"]["built"]
+    b = gb.gift_filter(adj, g32)
+    info = adj.tiled_info()
+    assert info["f4"]["built"] and info["f2"]["built"]
+    assert rel_l2(a, b) <= 1e-6
+    try:
+        gb.set_tiled_policy("never")
+        adj2 = gb.build_clique_graph(fd, max_clique_pins=200)
+        for _ in range(3):
+            c = gb.gift_filter(adj2, g32)
+        assert not adj2.tiled_info()["f4"]["built"]
+        assert np.array_equal(c, a)  # both the row kernel
+        gb.set_tiled_policy("always")
+        adj3 = gb.build_clique_graph(fd, max_clique_pins=200)
+        d = gb.gift_filter(adj3, g32)
+        assert adj3.tiled_info()["f4"]["built"]
+        assert np.array_equal(d, b)
+    finally:
+        gb.set_tiled_policy("on_reuse")
+    with pytest.raises(ValueError):
+        gb.set_tiled_policy("sometimes")
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_device_row_split_matches_host_restatement(gb, world):
+    """gift_csr_row_bounds / gift_csr_split_rows (csrc/shard.cu) against the
+    host restatement in shard.py: same bounds, same local / ghost blocks
+    (entry order and fp64 value bits), same ghost id lists."""
+    import ctypes
+
+    from paper_2502_17632_b200 import _lib, shard, synth
+
+    fd = synth.generate("c2", seed=4, scale=0.02, window=600)
+    adj = gb.build_clique_graph(fd, max_clique_pins=200)
+    lib = _lib.load_library()
+    ctx = _lib.context()
+    bounds = np.zeros(world + 1, dtype=np.int64)
+    _lib.check(lib.gift_csr_row_bounds(ctx, adj.handle, world, bounds.ctypes.data_as(_lib.c_i64p)))
+    indptr = np.asarray(adj.indptr, np.int64)
+    assert np.array_equal(bounds, shard.nnz_balanced_bounds(indptr, world))
+    values = np.asarray(adj.values)
+    for rank in range(world):
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        hl, hg = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(lib.gift_csr_split_rows(ctx, adj.handle, r0, r1, ctypes.byref(hl), ctypes.byref(hg)))
+        ids_p, n_ids = ctypes.c_void_p(), ctypes.c_int64()
+        _lib.check(lib.gift_csr_ext_ids(hg.value, ctypes.byref(ids_p), ctypes.byref(n_ids)))
+        from paper_2502_17632_b200.graph import _memcpy_d2h
+
+        ids = np.empty(n_ids.value, np.int64)
+        _memcpy_d2h(ids, ids_p.value)
+        L = gb.SparseSymMatrix._from_handle(hl.value)
+        G = gb.SparseSymMatrix._from_handle(hg.value)
+        ghosts, loc, gh = shard.split_block(indptr, adj.indices, r0, r1)
+        assert np.array_equal(ids, ghosts)
+        for blk, (ptr, idx, pos) in ((L, loc), (G, gh)):
+            assert np.array_equal(np.asarray(blk.indptr, np.int64), ptr)
+            assert np.array_equal(np.asarray(blk.indices, np.int64), idx.astype(np.int64))
+            assert_bits_equal(blk.values, values[pos], f"rank {rank} block values")

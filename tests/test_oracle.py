@@ -152,3 +152,38 @@ def test_introsort_restatement_matches_libstdcxx(orc, kind):
         else:
             keys = orc.antiqsort_keys(n) // 4
         assert np.array_equal(orc.std_sort_perm_emulated(keys), orc.std_sort_perm_libstdcxx(keys)), (kind, n)
+
+
+def _configs_meta():
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "configs_meta.json")) as f:
+        return json.load(f)["samples"]
+
+
+@pytest.mark.parametrize("name", ["c1_full", "c2_s005", "c3_s003", "c4_s0004", "c2_s001_uncapped"])
+def test_config_samples_match_reference_hashes(orc, name):
+    """The oracle reproduces the reference bit for bit at c1 full size and on
+    the scaled c2/c3/c4 samples the GPU parity tests use (hashes made by
+    tests/golden/make_golden_configs.py from giftplace itself)."""
+    from paper_2502_17632_b200 import synth
+    import paper_2502_17632_b200 as gb
+
+    meta = _configs_meta()[name]
+    fd = synth.generate(meta["config"], seed=meta["seed"], scale=meta["scale"], window=meta["window"])
+    A = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, meta["cap"])
+    assert A.nnz == meta["nnz"]
+    assert sha(A.indptr) == meta["indptr_sha"]
+    assert sha(A.indices) == meta["indices_sha"]
+    assert sha(A.data) == meta["values_sha"]
+    deg = orc.degrees(A)
+    assert sha(deg) == meta["degrees_sha"]
+    g0 = gb.initial_signal(fd, gb.GiftConfig(seed=0, jitter_scale=10.0))
+    assert sha(g0) == meta["g0_sha"]
+    g32 = g0.astype(np.float32).astype(np.float64)
+    assert sha(orc.gift_filter(A, g32, DEFAULT, deg)) == meta["filter_g32_sha"]
+    r = fd.region
+    placed = orc.place_epilogue(orc.gift_filter(A, g0, DEFAULT, deg), fd.fixed_mask(), fd.fixed_positions(),
+                                [r.xmin, r.ymin, r.xmax, r.ymax])
+    assert sha(placed) == meta["place_sha"]

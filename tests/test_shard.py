@@ -121,9 +121,13 @@ def _worker(rank, world, port, results, scale, window):
         A = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, 200)
         deg = orc.degrees(A)
         ex = shard.TorchExchange(device="cpu")
-        plan = shard.make_shard_plan(A.indptr, A.indices, world, rank, ex.ids)
+        bounds = shard.nnz_balanced_bounds(A.indptr, world)
+        ghosts, loc, gh = shard.split_block(A.indptr, A.indices, int(bounds[rank]), int(bounds[rank + 1]))
+        plan = shard.exchange_plan(bounds, rank, ghosts, ex.ids)
         s_of = lambda sigma: (1.0 / np.sqrt(deg + sigma)).astype(np.float32)[plan.r0:plan.r1]  # noqa: E731
-        sf = shard.ShardedFilter(plan, A.data, NumpyBackend(), ex, s_of)
+        be = NumpyBackend()
+        sf = shard.ShardedFilter(plan, be.block(loc[0], loc[1], A.data[loc[2]]), be.block(gh[0], gh[1], A.data[gh[2]]),
+                                 be, ex, s_of)
         g32 = synth.signal_fp32(fd, seed=1)
         r0, r1 = plan.r0, plan.r1
         g = torch.from_numpy(np.ascontiguousarray(g32[r0:r1]))
@@ -137,7 +141,7 @@ def _worker(rank, world, port, results, scale, window):
             "ghost_sorted": bool(np.all(np.diff(plan.ghosts) > 0)),
             "ghost_not_owned": bool(np.all((plan.ghosts < r0) | (plan.ghosts >= r1))),
             "send_in_range": bool(np.all((plan.send_rows >= 0) & (plan.send_rows < r1 - r0))),
-            "nnz_split": int(plan.local_indptr[-1] + plan.ghost_indptr[-1]) == int(A.indptr[r1] - A.indptr[r0]),
+            "nnz_split": int(loc[0][-1] + gh[0][-1]) == int(A.indptr[r1] - A.indptr[r0]),
         }
         gathered = [None] * world if rank == 0 else None
         dist.gather_object((r0, out.numpy(), inv, plan.n_ghost), gathered, dst=0)
