@@ -359,6 +359,7 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-oneshot", action="store_true")
+    ap.add_argument("--e2e-out", choices=["f32", "f64"], default="f32", help="placement dtype of the e2e leg")
     ap.add_argument("--oneshot", choices=["python", "abi"], default=None, help=argparse.SUPPRESS)
     ap.add_argument("--dry-launch", action="store_true", help="form the process group and exit (launcher test)")
     args = ap.parse_args()
@@ -527,15 +528,20 @@ def main() -> None:
     h_g = torch.from_numpy(np.ascontiguousarray(g32[r0:r1])).pin_memory()
     h_mask = torch.from_numpy(np.ascontiguousarray(mask[r0:r1])).pin_memory()
     h_pos = torch.from_numpy(np.ascontiguousarray(fpos[r0:r1])).pin_memory()
-    h_out = torch.empty((r1 - r0, 2), dtype=torch.float64).pin_memory()
+    # the configs ask for an N x 2 fp32 placement (BASELINE.json configs[0]);
+    # fp32 output also halves the device-to-host bytes
+    e2e_f64 = args.e2e_out == "f64"
+    h_out = torch.empty((r1 - r0, 2), dtype=torch.float64 if e2e_f64 else torch.float32).pin_memory()
 
     if world == 1:
-        e2e_api = ("gift_filter_host (C ABI, pinned host buffers; output written in place by the final hop)"
+        e2e_api = ("gift_filter_host (C ABI, pinned host buffers; output written in place by the final hop; "
+                   f"{args.e2e_out} placement)"
                    if os.environ.get("GIFT_ZERO_COPY", "1") != "0" else "gift_filter_host (C ABI, pinned host buffers)")
 
         def step_e2e():
             _lib.check(lib.gift_filter_host(ctx, adj.handle, 3, sp_, kp_, ap_, 2, _lib.GIFT_DTYPE_F32,
-                                            _lib.c_vp(h_g.data_ptr()), _lib.GIFT_DTYPE_F64,
+                                            _lib.c_vp(h_g.data_ptr()),
+                                            _lib.GIFT_DTYPE_F64 if e2e_f64 else _lib.GIFT_DTYPE_F32,
                                             _lib.c_vp(h_out.data_ptr()), _lib.c_vp(h_mask.data_ptr()),
                                             _lib.c_vp(h_pos.data_ptr()), rp_, _lib.GIFT_PREC_FP32))
     else:
@@ -546,7 +552,7 @@ def main() -> None:
             dmask.copy_(h_mask, non_blocking=True)
             dpos.copy_(h_pos, non_blocking=True)
             step()
-            h_out.copy_(dout, non_blocking=True)
+            h_out.copy_(dout.to(h_out.dtype), non_blocking=True)
             torch.cuda.current_stream().synchronize()
 
     for _ in range(2):
@@ -571,7 +577,7 @@ def main() -> None:
         h2d = g32.nbytes + mask.nbytes + fpos.nbytes
     else:
         h2d = int(h_g.numel() * 4 + h_mask.numel() + h_pos.numel() * 8)
-    d2h = (r1 - r0) * 2 * 8
+    d2h = (r1 - r0) * 2 * (8 if e2e_f64 else 4)
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None

@@ -98,6 +98,19 @@ int gift_build_clique_graph(gift_ctx* ctx, int64_t n_cells, int64_t n_nets,
                             const int64_t* d_net_start, const int32_t* d_pin_cell,
                             int64_t max_clique_pins, gift_csr** out, int64_t* n_skipped);
 
+/* Opt-in extension (not in the reference): keep the nets with more than
+ * max_clique_pins pins -- which build_clique_graph skips (graph.py:136-138) --
+ * as an implicit O(pins) clique term of csr, a graph built from the same
+ * netlist with the same cap: A_e = (2/m)(b b^T - diag(b o b)) per net
+ * (b = cell multiplicities).  Afterwards degrees, s_sigma, the filter bank
+ * (both precisions) and matmul use A_cap + A_implicit, which equals the
+ * uncapped clique graph in exact arithmetic (no bit-exact contract for the
+ * implicit part; fp32 bank within 1e-5 of the uncapped reference).  Must be
+ * called before the graph is used; normalized_augmented_adjacency and the
+ * stepped hop refuse such a graph.  *n_implicit (nullable): nets kept. */
+int gift_csr_attach_high_fanout(gift_ctx* ctx, gift_csr* csr, int64_t n_nets, const int64_t* d_net_start,
+                                const int32_t* d_pin_cell, int64_t max_clique_pins, int64_t* n_implicit);
+
 /* from_coo(n, rows, cols, vals)  graph.py:114-117, followed by the
  * SparseSymMatrix checks (graph.py:55-65) when check_symmetric != 0.
  * Duplicates summed in scipy order, explicit zeros dropped. */

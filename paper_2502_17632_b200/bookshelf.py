@@ -52,93 +52,119 @@ _REASON = {
 }
 
 
-def _data_lines(path: str):
-    """(lineno, stripped line) skipping comments, blanks and UCLA headers (netlist.py:196-205)."""
+class _Record:
+    """One data line of a Bookshelf text: comment cut at '#', stripped; blank
+    lines and UCLA banners never become records (netlist.py:193-203)."""
+
+    __slots__ = ("lineno", "text", "tokens")
+
+    def __init__(self, lineno: int, text: str):
+        self.lineno = lineno
+        self.text = text
+        self.tokens = text.split()
+
+    @property
+    def value(self) -> str | None:
+        """Text after the first ':' of a 'Key : value' header, stripped (None: no colon)."""
+        head, colon, tail = self.text.partition(":")
+        return tail.strip() if colon else None
+
+
+def _records(path: str):
     with open(path, "r") as f:
         for lineno, raw in enumerate(f, start=1):
-            line = raw.split("#", 1)[0].strip()
-            if not line or line.startswith("UCLA"):
-                continue
-            yield lineno, line
+            text = raw.partition("#")[0].strip()
+            if text and not text.startswith("UCLA"):
+                yield _Record(lineno, text)
 
 
-def _header_value(line: str) -> str | None:
-    if ":" not in line:
-        return None
-    return line.split(":", 1)[1].strip()
+# .aux entries by extension: required ones, and the optional placement rows
+_AUX_REQUIRED = (".nodes", ".nets", ".pl")
+_AUX_KNOWN = frozenset(_AUX_REQUIRED + (".scl",))
 
 
 def aux_files(aux_path: str) -> dict[str, str]:
-    """{extension: path} from the .aux manifest; .nodes/.nets/.pl required, .scl optional."""
+    """{extension: path} from the .aux manifest (netlist.py:389-415 semantics):
+    every record is 'Tag : file ...'; .nodes/.nets/.pl are required, .scl is
+    optional, other files are skipped with a warning, listed files must exist."""
     if not os.path.isfile(aux_path):
         raise MissingFileError(aux_path)
     base = os.path.dirname(os.path.abspath(aux_path))
     listed: list[str] = []
-    for lineno, line in _data_lines(aux_path):
-        value = _header_value(line)
-        if value is None:
-            raise MalformedLineError(aux_path, lineno, line, "expected 'Tag : file ...'")
-        listed.extend(value.split())
-    by_ext: dict[str, str] = {}
+    for rec in _records(aux_path):
+        if rec.value is None:
+            raise MalformedLineError(aux_path, rec.lineno, rec.text, "expected 'Tag : file ...'")
+        listed += rec.value.split()
+    found: dict[str, str] = {}
     for fname in listed:
         ext = os.path.splitext(fname)[1]
-        path = os.path.join(base, fname)
-        if ext in (".nodes", ".nets", ".pl", ".scl"):
-            if not os.path.isfile(path):
-                raise MissingFileError(path)
-            by_ext[ext] = path
-        else:
+        if ext not in _AUX_KNOWN:
             log.warning("%s: unsupported file %s skipped", aux_path, fname)
-    for required in (".nodes", ".nets", ".pl"):
-        if required not in by_ext:
-            raise MissingFileError(os.path.join(base, f"<{required} entry in {os.path.basename(aux_path)}>"))
-    return by_ext
+            continue
+        path = os.path.join(base, fname)
+        if not os.path.isfile(path):
+            raise MissingFileError(path)
+        found[ext] = path
+    missing = [ext for ext in _AUX_REQUIRED if ext not in found]
+    if missing:
+        raise MissingFileError(os.path.join(base, f"<{missing[0]} entry in {os.path.basename(aux_path)}>"))
+    return found
+
+
+def _subrow_origin(rec: _Record) -> dict[str, float]:
+    """'SubrowOrigin : x [NumSites : s]' -> {"x": .., "num_sites": ..}."""
+    words = rec.text.replace(":", " ").split()
+    got = {"x": float(words[1])}
+    if "NumSites" in words:
+        got["num_sites"] = float(words[words.index("NumSites") + 1])
+    return got
+
+
+# attributes of a CoreRow block: keyword -> fields it sets (netlist.py:330-370 semantics)
+_ROW_ATTRS = {
+    "Coordinate": lambda rec: {"y": float(rec.value)},
+    "Height": lambda rec: {"height": float(rec.value)},
+    "Sitewidth": lambda rec: {"site_width": float(rec.value)},
+    "SubrowOrigin": _subrow_origin,
+}
+_ROW_NEEDS = frozenset(("y", "height", "x", "num_sites"))
 
 
 def _parse_scl(path: str) -> list[Row]:
-    """CoreRow blocks (netlist.py:330-377)."""
+    """CoreRow ... End blocks of a .scl file -> Rows.  Lines outside a block
+    are ignored; inside, 'Key : value' attributes from _ROW_ATTRS are read
+    (others and colon-less lines ignored, a bad number is a
+    MalformedLineError); a block missing any of y / height / x / num_sites is
+    skipped with a warning; site width defaults to 1."""
     rows: list[Row] = []
-    in_row = False
-    cur: dict[str, float] = {}
-    for lineno, line in _data_lines(path):
-        first = line.split(None, 1)[0]
-        if first == "CoreRow":
-            in_row, cur = True, {"site_width": 1.0}
+    block: dict[str, float] | None = None
+    for rec in _records(path):
+        key = rec.tokens[0]
+        if key == "CoreRow":
+            block = {"site_width": 1.0}
+        elif block is None:
             continue
-        if not in_row:
-            continue
-        if first == "End":
-            in_row = False
-            if {"y", "height", "x", "num_sites"} <= cur.keys():
-                rows.append(Row(y=cur["y"], height=cur["height"], x=cur["x"], num_sites=int(cur["num_sites"]),
-                                site_width=cur["site_width"]))
+        elif key == "End":
+            if _ROW_NEEDS <= block.keys():
+                rows.append(Row(y=block["y"], height=block["height"], x=block["x"],
+                                num_sites=int(block["num_sites"]), site_width=block["site_width"]))
             else:
-                log.warning("%s:%d: incomplete CoreRow block skipped", path, lineno)
-            continue
-        value = _header_value(line)
-        if value is None:
-            continue
-        try:
-            if first == "Coordinate":
-                cur["y"] = float(value)
-            elif first == "Height":
-                cur["height"] = float(value)
-            elif first == "Sitewidth":
-                cur["site_width"] = float(value)
-            elif first == "SubrowOrigin":
-                parts = line.replace(":", " ").split()
-                cur["x"] = float(parts[1])
-                if "NumSites" in parts:
-                    cur["num_sites"] = float(parts[parts.index("NumSites") + 1])
-        except (ValueError, IndexError):
-            raise MalformedLineError(path, lineno, line, "malformed row attribute")
+                log.warning("%s:%d: incomplete CoreRow block skipped", path, rec.lineno)
+            block = None
+        elif rec.value is not None and key in _ROW_ATTRS:
+            try:
+                block.update(_ROW_ATTRS[key](rec))
+            except (ValueError, IndexError):
+                raise MalformedLineError(path, rec.lineno, rec.text, "malformed row attribute") from None
     return rows
 
 
 def _region_from_rows(rows: list[Row]) -> Region:
-    return Region(xmin=min(r.x for r in rows), ymin=min(r.y for r in rows),
-                  xmax=max(r.x + r.num_sites * r.site_width for r in rows),
-                  ymax=max(r.y + r.height for r in rows), rows=rows)
+    """Bounding box of the rows (netlist.py:373-378)."""
+    xs = [(r.x, r.x + r.num_sites * r.site_width) for r in rows]
+    ys = [(r.y, r.y + r.height) for r in rows]
+    return Region(xmin=min(x0 for x0, _ in xs), ymin=min(y0 for y0, _ in ys),
+                  xmax=max(x1 for _, x1 in xs), ymax=max(y1 for _, y1 in ys), rows=rows)
 
 
 def _raise_parse_error(msg: str, paths: list[str]) -> None:

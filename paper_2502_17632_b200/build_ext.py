@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libgiftb200.so")
-SOURCES = ["csrc/abi.cu", "csrc/build.cu", "csrc/filter.cu", "csrc/bmt.cu", "csrc/metrics.cu", "csrc/plio.cu", "csrc/bookshelf.cu", "csrc/shard.cu"]
+SOURCES = ["csrc/abi.cu", "csrc/build.cu", "csrc/filter.cu", "csrc/bmt.cu", "csrc/metrics.cu", "csrc/plio.cu", "csrc/bookshelf.cu", "csrc/shard.cu", "csrc/hf.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -33,6 +33,9 @@ void gather_rows_f32(Ctx* ctx, int64_t n_idx, int F, const int64_t* idx, const f
 Csr* csr_from_arrays(Ctx* ctx, int64_t n_rows, int64_t nnz, const int64_t* d_indptr, const int32_t* d_indices,
                      const double* d_values);
 void csr_row_bounds(Ctx* ctx, const Csr* c, int world, int64_t* h_bounds);
+void free_bank_graphs(Ctx* ctx);
+int64_t csr_attach_high_fanout(Ctx* ctx, Csr* c, int64_t n_nets, const int64_t* d_net_start, const int32_t* d_pin_cell,
+                               int64_t cap);
 void csr_split_rows(Ctx* ctx, const Csr* c, int64_t r0, int64_t r1, Csr** local, Csr** ghost);
 
 double quadratic_wirelength(Ctx* ctx, const Csr* c, const double* g);
@@ -238,6 +241,8 @@ int gift_ctx_destroy(gift_ctx* ctx) {
     if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (auto& kv : ctx->tile_ctr) cudaFree(kv.second);
+  gift::free_bank_graphs(ctx);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   if (ctx->side) {
     cudaStreamSynchronize(ctx->side);
     cudaStreamDestroy(ctx->side);
@@ -592,6 +597,16 @@ int gift_ctx_set_tiled_policy(gift_ctx* ctx, int policy) {
           "unknown tiled policy");
   std::lock_guard<std::recursive_mutex> lk(ctx->mu);
   ctx->tiled_policy = policy;
+  GIFT_API_END
+}
+
+int gift_csr_attach_high_fanout(gift_ctx* ctx, gift_csr* csr, int64_t n_nets, const int64_t* d_net_start,
+                                const int32_t* d_pin_cell, int64_t max_clique_pins, int64_t* n_implicit) {
+  GIFT_API_BEGIN
+  require(ctx && csr && d_net_start, GIFT_ERR_VALUE, "null argument");
+  ApiScope g(ctx, csr);
+  const int64_t k = gift::csr_attach_high_fanout(ctx, csr, n_nets, d_net_start, d_pin_cell, max_clique_pins);
+  if (n_implicit) *n_implicit = k;
   GIFT_API_END
 }
 

@@ -266,28 +266,60 @@ __global__ void k_scatter_runs(int64_t nseg, const int64_t* __restrict__ seg_run
 // wildcard: it can sit on any zero row kC + r, so it takes a residue no other
 // lane of its half / quarter uses.
 //
-// One warp per slice, lane = the slice's lane: each lane buckets its own run by
-// residue (counting sort into tmp), then the two halves decide step by step,
-// lane after lane, with the half's used-residue masks kept warp-uniform
-// through shuffles.  (The first version ran one thread per half slice over
-// [16][16] count tables: local-memory bound, 560 ms of the c3 build.)
+// One warp per slice, lane = the slice's lane.  Each lane buckets its own run
+// by residue (counting sort into tmp); then the greedy runs as a WAVEFRONT
+// over (step, lane): lane l decides step k at iteration k + l, using the
+// used-residue masks of step k that lane l - 1 produced one iteration earlier
+// (shuffled up within the 16-lane half).  All 16 lanes of a half decide at
+// once, in L + 15 iterations instead of 16 L sequential decisions, and the
+// per-lane counts / bucket cursors live in registers (unrolled selects, no
+// dynamic indexing).  (Earlier versions: one thread per half slice over
+// [16][16] count tables, 560 ms of the c3 build; lane-serial decisions with
+// shuffles, 350 ms.)
+__device__ __forceinline__ int sel16(const int (&v)[16], int r) {
+  int x = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x = (i == r) ? v[i] : x;
+  return x;
+}
+
+__device__ __forceinline__ void add16(int (&v)[16], int r, int d) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] += (i == r) ? d : 0;
+}
+
+// residue with the largest count among the set bits of m (-1 if none);
+// counts of residue 0 are the real (non-padding) entries only
+__device__ __forceinline__ int argmax16(const int (&cnt)[16], int real0, unsigned m) {
+  int best = -1, bc = 0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int c = r == 0 ? real0 : cnt[r];
+    const bool take = ((m >> r) & 1u) && c > bc;
+    bc = take ? c : bc;
+    best = take ? r : best;
+  }
+  return best;
+}
+
 __global__ void __launch_bounds__(256) k_slice_schedule(int64_t nslices, int kC, const int64_t* __restrict__ slice_off,
                                                         uint16_t* __restrict__ col, float* __restrict__ w,
                                                         uint16_t* __restrict__ tcol, float* __restrict__ tw) {
   const int lane = threadIdx.x & 31;
+  const int hl = lane & 15;  // position in the 16-lane half
+  const int q = hl >> 3;     // quarter within the half
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t sl = warp0; sl < nslices; sl += nwarps) {
     const int64_t off = slice_off[sl];
-    const int64_t L = (slice_off[sl + 1] - off) / 32;  // slots per lane
-    int cnt[16];
-    int next[16];
+    const int L = (int)((slice_off[sl + 1] - off) / 32);  // slots per lane
+    int cnt[16], next[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) cnt[r] = 0;
     int real0 = 0;
-    for (int64_t k = 0; k < L; ++k) {
-      const int cv = col[off + (k / 4) * 128 + lane * 4 + (k % 4)];
-      cnt[cv & 15]++;
+    for (int k = 0; k < L; ++k) {
+      const int cv = col[off + (k >> 2) * 128 + lane * 4 + (k & 3)];
+      add16(cnt, cv & 15, 1);
       real0 += ((cv & 15) == 0 && cv < kC);
     }
     {
@@ -303,82 +335,62 @@ __global__ void __launch_bounds__(256) k_slice_schedule(int64_t nslices, int kC,
       int pos[16];
 #pragma unroll
       for (int r = 0; r < 16; ++r) pos[r] = next[r];
-      for (int64_t k = 0; k < L; ++k) {
-        const int64_t slot = off + (k / 4) * 128 + lane * 4 + (k % 4);
+      for (int k = 0; k < L; ++k) {
+        const int64_t slot = off + (k >> 2) * 128 + lane * 4 + (k & 3);
         const uint16_t cv = col[slot];
         const int r = cv & 15;
-        tcol[base + pos[r]] = cv;
-        tw[base + pos[r]] = w[slot];
-        pos[r]++;
+        const int p = sel16(pos, r);
+        tcol[base + p] = cv;
+        tw[base + p] = w[slot];
+        add16(pos, r, 1);
       }
     }
-    const int pad_first = next[0] + real0;  // first padding entry of bucket 0
     int pads = cnt[0] - real0;
-    int reals0 = real0;
-    const int hl = lane & 15;        // position in the half
-    const int q = hl >> 3;           // quarter within the half
-    for (int64_t k = 0; k < L; ++k) {
-      unsigned used16 = 0, used8 = 0;  // this lane's half: residues mod 16 / mod 8 (bits 0-7 quarter 0, 8-15 quarter 1)
-      for (int l = 0; l < 16; ++l) {
-        int choice = 0;  // residue | 16 if a padding wildcard
-        if (hl == l) {
-          unsigned avail = 0;
+    unsigned out16 = 0, out8 = 0;  // masks after this lane's decision (read by lane + 1)
+    for (int t = 0; t < L + 15; ++t) {
+      unsigned in16 = __shfl_up_sync(0xffffffffu, out16, 1, 16);
+      unsigned in8 = __shfl_up_sync(0xffffffffu, out8, 1, 16);
+      if (hl == 0) in16 = in8 = 0;
+      const int k = t - hl;
+      out16 = in16;
+      out8 = in8;
+      if (k < 0 || k >= L) continue;
+      unsigned avail = 0;
 #pragma unroll
-          for (int r = 0; r < 16; ++r) avail |= ((r == 0 ? reals0 : cnt[r]) > 0 ? 1u : 0u) << r;
-          const unsigned q8 = (used8 >> (8 * q)) & 0xffu;
-          const unsigned blocked = q8 | (q8 << 8);
-          const unsigned c_best = avail & ~used16 & ~blocked, c_ok8 = avail & ~blocked;
-          auto pick = [&](unsigned m) {
-            int best = -1, bc = 0;
-            while (m) {
-              const int r = __ffs(m) - 1;
-              m &= m - 1;
-              const int c = r == 0 ? reals0 : cnt[r];
-              if (c > bc) {
-                bc = c;
-                best = r;
-              }
-            }
-            return best;
-          };
-          int r = pick(c_best);
-          if (r < 0 && pads > 0) {
-            // no conflict-free real entry: a padding slot on a free zero row
-            const unsigned f16 = ~used16 & ~blocked & 0xffffu, f8 = ~blocked & 0xffffu;
-            r = f16 ? __ffs(f16) - 1 : (f8 ? __ffs(f8) - 1 : 0);
-            choice = r | 16;
-          } else {
-            if (r < 0) r = pick(c_ok8);
-            if (r < 0) r = pick(avail);
-            if (r < 0) r = 0;  // only padding left
-            choice = r;
-          }
-        }
-        const int got = __shfl_sync(0xffffffffu, choice, (lane & 16) | l);
-        const int rr = got & 15;
-        used16 |= 1u << rr;
-        used8 |= 1u << ((rr & 7) + 8 * (l >> 3));
-        if (hl == l) {
-          const int64_t slot = off + (k / 4) * 128 + lane * 4 + (k % 4);
-          if (got & 16) {  // padding wildcard (weight 0)
-            pads--;
-            cnt[0]--;
-            col[slot] = (uint16_t)(kC + rr);
-            w[slot] = tw[base + pad_first + pads];
-          } else if (rr == 0 && reals0 == 0) {  // residue 0 with only padding left: a plain padding slot
-            pads--;
-            cnt[0]--;
-            col[slot] = (uint16_t)kC;
-            w[slot] = tw[base + pad_first + pads];
-          } else {
-            const int src = next[rr]++;
-            cnt[rr]--;
-            if (rr == 0) reals0--;
-            col[slot] = tcol[base + src];
-            w[slot] = tw[base + src];
-          }
+      for (int r = 0; r < 16; ++r) avail |= ((r == 0 ? real0 : cnt[r]) > 0 ? 1u : 0u) << r;
+      const unsigned q8 = (in8 >> (8 * q)) & 0xffu;
+      const unsigned blocked = q8 | (q8 << 8);
+      int r = argmax16(cnt, real0, avail & ~in16 & ~blocked);
+      bool wildcard = false;
+      if (r < 0 && pads > 0) {
+        // no conflict-free real entry: a padding slot on a free zero row
+        const unsigned f16 = ~in16 & ~blocked & 0xffffu, f8 = ~blocked & 0xffffu;
+        r = f16 ? __ffs(f16) - 1 : (f8 ? __ffs(f8) - 1 : 0);
+        wildcard = true;
+      } else {
+        if (r < 0) r = argmax16(cnt, real0, avail & ~blocked);
+        if (r < 0) r = argmax16(cnt, real0, avail);
+        if (r < 0) {  // nothing real left (cannot happen while pads > 0 is handled above)
+          r = 0;
+          wildcard = true;
         }
       }
+      const int64_t slot = off + (k >> 2) * 128 + lane * 4 + (k & 3);
+      if (wildcard) {
+        pads--;
+        add16(cnt, 0, -1);
+        col[slot] = (uint16_t)(kC + r);
+        w[slot] = 0.f;
+      } else {
+        const int src = sel16(next, r);
+        add16(next, r, 1);
+        add16(cnt, r, -1);
+        if (r == 0) real0--;
+        col[slot] = tcol[base + src];
+        w[slot] = tw[base + src];
+      }
+      out16 = in16 | (1u << r);
+      out8 = in8 | (1u << ((r & 7) + 8 * q));
     }
   }
 }
@@ -1367,6 +1379,12 @@ const float* csr_w32_public(Ctx* ctx, Csr* c);
 void launch_row_list(Ctx* ctx, cudaStream_t st, const HopArgs& base, const int32_t* rows, int64_t nrows, int fin,
                      int fout, int G);
 
+bool bmt_possible(Ctx* ctx, const Csr* c) {
+  if (env_int("GIFT_BMT", 1) == 0 || !c->sorted_rows || !c->square) return false;
+  if (ctx->tiled_policy == GIFT_TILED_NEVER && !c->bmt.ready && !c->bmt_wide.ready) return false;
+  return c->n >= env_int("GIFT_BMT_MIN_ROWS", 262144) && c->mean_row >= env_int("GIFT_BMT_MIN_MEAN", 32);
+}
+
 bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
   if (env_int("GIFT_BMT", 1) == 0 || !c->sorted_rows || !c->square) return false;
   // building the tiled copy costs ~a few hops; only resident graphs amortise it
@@ -1381,7 +1399,9 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
                    (ctx->tiled_policy == GIFT_TILED_ON_REUSE && c->fp32_hops < kReuseHops)))
     return false;
   if (c->n < env_int("GIFT_BMT_MIN_ROWS", 262144) || c->mean_row < env_int("GIFT_BMT_MIN_MEAN", 32)) return false;
-  if (a.row_begin != 0 || a.n != c->n || a.part_in) return false;  // part_out: the epilogue writes partials
+  // whole square graphs only; partial sums in (part_in: the high-fanout term)
+  // or out (part_out: a shard's local block) pass through the row epilogue
+  if (a.row_begin != 0 || a.n != c->n) return false;
   if (!B.ready) {
     B.ready = true;
     // the tiled copy is an optimisation: if device memory runs out while it is

@@ -70,6 +70,19 @@ struct Ctx {
     cudaEvent_t a, b;
   };
   std::vector<Rec> recs;
+  // small-graph fp32 banks replayed as CUDA graphs (filter.cu), most recent last
+  struct BankGraph {
+    uint64_t uid = 0;             // Csr::uid the graph was captured on
+    std::vector<double> key;      // terms, widths, dtypes, epilogue
+    cudaGraphExec_t exec = nullptr;
+    void* gin = nullptr;          // staged input / output / mask / fixed centres
+    void* gout = nullptr;
+    uint8_t* gmask = nullptr;
+    double* gpos = nullptr;
+    int64_t kernels = 0;          // launches inside the graph
+  };
+  std::vector<BankGraph> graphs;
+  cudaStream_t cap_stream = nullptr;  // private stream the graphs are captured on
 };
 
 // brackets one launch with events when ctx->profiling (see gift_ctx_set_profiling)
@@ -168,6 +181,19 @@ struct Csr {
                                     // then 32x4 f32 weights
   } bmt, bmt_wide;  // bmt_wide: signal widths <= 2; bmt: F = 4 (bmt.cu bmt_shape_for)
   int64_t fp32_hops = 0;          // fp32 hop launches served (tiled-copy policy: build on reuse)
+  uint64_t uid = 0;               // identity for cached CUDA graphs (0 = none yet; never reused)
+  // implicit clique term of the nets above the cap (hf.cu; opt-in extension)
+  struct Hf {
+    int64_t nets = 0, pins = 0, cells = 0;
+    int64_t* net_start = nullptr;  // [nets + 1] the selected nets' pin table
+    int32_t* pin_cell = nullptr;   // [pins]
+    double* coef = nullptr;        // [nets] 2/m
+    int32_t* cell = nullptr;       // [cells] cells with high-fanout pins, ascending
+    int64_t* occ_ptr = nullptr;    // [cells + 1] their pin occurrences (net order)
+    int32_t* occ_net = nullptr;    // [pins] net of each occurrence
+    double* occ_b = nullptr;       // [pins] multiplicity of the cell in that net
+    void* tbuf = nullptr;          // [nets * 4] fp64 per-hop net sums
+  } hf;
   int64_t ext_n = 0;              // ghost block of a row shard: its columns >= n index these
   int64_t* ext_ids = nullptr;     // [ext_n] global ids of the ghost columns, ascending
   std::vector<void*> owned;       // everything above, freed on destroy

@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <set>
 #include <climits>
@@ -32,6 +33,12 @@
 #include "hop.cuh"
 
 namespace gift {
+
+// hf.cu: implicit clique term of the nets above the cap (opt-in)
+void hf_add_degrees(Ctx* ctx, const Csr* c, double* deg);
+void hf_apply_f32(Ctx* ctx, const Csr* c, int F, const float* z, float* out);
+void hf_apply_f64(Ctx* ctx, const Csr* c, int nc, const double* x, int64_t ld, int64_t c0, const double* s,
+                  double* out);
 
 namespace {
 
@@ -195,7 +202,7 @@ template <int MODE>
 __global__ void k_matvec_exact(int64_t n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
                                const double* __restrict__ val, const double* __restrict__ s, double sigma,
                                int64_t ld, int64_t c0, int nc, const double* __restrict__ x,
-                               double* __restrict__ y) {
+                               double* __restrict__ y, const double* __restrict__ extra) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     const double si = MODE ? s[i] : 0.0;
@@ -221,6 +228,8 @@ __global__ void k_matvec_exact(int64_t n, const int64_t* __restrict__ indptr, co
       const double d = __dmul_rn(__dmul_rn(sigma, si), si);
       for (int c = 0; c < nc; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(d, x[i * ld + c0 + c]));
     }
+    if (extra)  // implicit high-fanout term (hf.cu): (A_hf (s o x))_i, scaled by s_i
+      for (int c = 0; c < nc; ++c) acc[c] = __dadd_rn(acc[c], MODE ? __dmul_rn(si, extra[i * 4 + c]) : extra[i * 4 + c]);
     for (int c = 0; c < nc; ++c) y[i * ld + c0 + c] = acc[c];
   }
 }
@@ -434,6 +443,7 @@ const double* csr_degrees(Ctx* ctx, Csr* c) {
       k_degrees<<<grid_for(c->n, kBlock, 1LL << 30), kBlock, 0, ctx->stream>>>(c->n, c->indptr, c->values,
                                                                              c->degrees);
       GIFT_LAUNCH_CHECK(ctx);
+      hf_add_degrees(ctx, c, c->degrees);  // + the implicit high-fanout term, if any
     }
   }
   return c->degrees;
@@ -485,6 +495,9 @@ static const double* csr_scale(Ctx* ctx, Csr* c, double sigma) {
 }
 
 Csr* normalized_augmented_adjacency(Ctx* ctx, Csr* c, double sigma) {
+  if (c->hf.nets)
+    throw_error(GIFT_ERR_VALUE, "the graph has an implicit high-fanout term; it cannot be materialised "
+                                "(build it with max_clique_pins=None for an explicit operator)");
   const double* s = csr_scale(ctx, c, sigma);
   cudaStream_t st = ctx->stream;
   const int64_t n = c->n;
@@ -524,10 +537,15 @@ Csr* normalized_augmented_adjacency(Ctx* ctx, Csr* c, double sigma) {
 
 void csr_matmul(Ctx* ctx, const Csr* c, int64_t ncols, const double* x, double* y) {
   if (c->n == 0 || ncols == 0) return;
+  DevBuf<double> extra(ctx, c->hf.nets ? c->n * 4 : 0);
   for (int64_t c0 = 0; c0 < ncols; c0 += 4) {
     const int nc = (int)std::min<int64_t>(4, ncols - c0);
+    if (c->hf.nets) {
+      GIFT_CUDA(cudaMemsetAsync(extra.p, 0, c->n * 4 * sizeof(double), ctx->stream));
+      hf_apply_f64(ctx, c, nc, x, ncols, c0, nullptr, extra.p);
+    }
     k_matvec_exact<0><<<grid_for(c->n, kBlock, 1LL << 30), kBlock, 0, ctx->stream>>>(
-        c->n, c->indptr, c->indices, c->values, nullptr, 0.0, ncols, c0, nc, x, y);
+        c->n, c->indptr, c->indices, c->values, nullptr, 0.0, ncols, c0, nc, x, y, c->hf.nets ? extra.p : nullptr);
     GIFT_LAUNCH_CHECK(ctx);
   }
 }
@@ -574,6 +592,7 @@ static void bank_fp64_exact(Ctx* ctx, Csr* c, const std::vector<TermGroup>& grou
   for (auto& grp : groups) csr_scale(ctx, c, grp.sigma);  // raise before any work, like the reference would
   if (m == 0) return;
   DevBuf<double> x(ctx, m), pa(ctx, m), pb(ctx, m), acc(ctx, m);
+  DevBuf<double> extra(ctx, c->hf.nets ? n * 4 : 0);  // implicit high-fanout term (not in the reference)
   k_load_f64<<<grid_for(m, kBlock), kBlock, 0, st>>>(m, in_dtype, g, x.p);
   GIFT_LAUNCH_CHECK(ctx);
   GIFT_CUDA(cudaMemsetAsync(acc.p, 0, m * sizeof(double), st));
@@ -586,8 +605,13 @@ static void bank_fp64_exact(Ctx* ctx, Csr* c, const std::vector<TermGroup>& grou
         double* dst = (power == pa.p) ? pb.p : pa.p;
         for (int64_t c0 = 0; c0 < ncols; c0 += 4) {
           const int nc = (int)std::min<int64_t>(4, ncols - c0);
+          if (c->hf.nets) {
+            GIFT_CUDA(cudaMemsetAsync(extra.p, 0, n * 4 * sizeof(double), st));
+            hf_apply_f64(ctx, c, nc, power, ncols, c0, s, extra.p);
+          }
           k_matvec_exact<1><<<grid_for(n, kBlock, 1LL << 30), kBlock, 0, st>>>(
-              n, c->indptr, c->indices, c->values, s, grp.sigma, ncols, c0, nc, power, dst);
+              n, c->indptr, c->indices, c->values, s, grp.sigma, ncols, c0, nc, power, dst,
+              c->hf.nets ? extra.p : nullptr);
           GIFT_LAUNCH_CHECK(ctx);
         }
         power = dst;
@@ -699,6 +723,13 @@ static void bank_fp32(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, in
         a.fixed_mask = fixed_mask;
         a.fixed_pos = fixed_pos;
         a.reg = reg;
+        if (c->hf.nets) {
+          // implicit high-fanout term: its row sums enter the hop as partial sums
+          float* part = static_cast<float*>(scratch(ctx, 3, n * 4 * sizeof(float) + 64));
+          GIFT_CUDA(cudaMemsetAsync(part, 0, n * fin * sizeof(float), ctx->stream));
+          hf_apply_f32(ctx, c, fin, zin, part);
+          a.part_in = part;
+        }
         launch_hop(ctx, c, a, fin, fout, G, true);
         if (a.any_term) acc_written = true;
         active.swap(next);
@@ -720,6 +751,7 @@ void scale_vectors(Ctx* ctx, Csr* c, double sigma, const double** s64, const flo
 const float* weights32(Ctx* ctx, Csr* c) { return csr_w32(ctx, c); }
 
 void hop_fp32(Ctx* ctx, Csr* c, const gift_hop_desc* d) {
+  if (c->hf.nets) throw_error(GIFT_ERR_VALUE, "the stepped (sharded) hop does not support the high-fanout term");
   if (d->fin != 1 && d->fin != 2 && d->fin != 4) throw_error(GIFT_ERR_VALUE, "fin must be 1, 2 or 4");
   if (d->fout != 0 && d->fout != 1 && d->fout != 2 && d->fout != 4) throw_error(GIFT_ERR_VALUE, "bad fout");
   if (d->nch < 1 || d->nch > 4 || d->wcols < 1 || d->wcols * d->nch > d->fin)
@@ -828,6 +860,130 @@ Csr* csr_from_arrays(Ctx* ctx, int64_t n_rows, int64_t nnz, const int64_t* d_ind
   return c;
 }
 
+// ---------------------------------------------------------------------------
+// Small graphs are launch-bound (c0: ~5 MB per hop, L2-resident; the bank's
+// 6-8 launches plus the host's planning cost more than the hops).  Their fp32
+// bank is captured once per (graph, terms, widths, dtypes, epilogue) as a CUDA
+// graph over staged buffers and replayed: copy in, one graph launch, copy out.
+constexpr int64_t kGraphMaxRows = 262144;  // below the tiled hop's size threshold
+constexpr size_t kMaxGraphs = 8;
+
+static uint64_t next_uid() {
+  static std::atomic<uint64_t> u{0};
+  return ++u;
+}
+
+static void free_bank_graph(Ctx* ctx, Ctx::BankGraph& e) {
+  if (e.exec) cudaGraphExecDestroy(e.exec);
+  dev_free(ctx, e.gin);
+  dev_free(ctx, e.gout);
+  dev_free(ctx, e.gmask);
+  dev_free(ctx, e.gpos);
+  e = Ctx::BankGraph{};
+}
+
+void free_bank_graphs(Ctx* ctx) {
+  for (auto& e : ctx->graphs) free_bank_graph(ctx, e);
+  ctx->graphs.clear();
+}
+
+static bool bank_graph(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, int n_terms, const double* sigma,
+                       const int64_t* k, const double* alpha, int64_t ncols, int in_dtype, const void* g,
+                       int out_dtype, void* out, const uint8_t* fixed_mask, const double* fixed_pos,
+                       const double* region) {
+  if (ctx->profiling || c->n <= 0 || c->n >= kGraphMaxRows || ncols <= 0 || env_int("GIFT_GRAPHS", 1) == 0)
+    return false;
+  if (bmt_possible(ctx, c)) return false;  // a tiled-copy build cannot run inside a capture
+  const int64_t n = c->n;
+  const size_t in_b = (size_t)(n * ncols) * (in_dtype == GIFT_DTYPE_F64 ? 8 : 4);
+  const size_t out_b = (size_t)(n * ncols) * (out_dtype == GIFT_DTYPE_F64 ? 8 : 4);
+  std::vector<double> key = {(double)n_terms, (double)ncols, (double)in_dtype, (double)out_dtype,
+                             fixed_mask ? 1.0 : 0.0};
+  for (int t = 0; t < n_terms; ++t) {
+    key.push_back(sigma[t]);
+    key.push_back((double)k[t]);
+    key.push_back(alpha[t]);
+  }
+  if (fixed_mask)
+    for (int i = 0; i < 4; ++i) key.push_back(region[i]);
+  if (!c->uid) c->uid = next_uid();
+  size_t hit = ctx->graphs.size();
+  for (size_t i = 0; i < ctx->graphs.size(); ++i)
+    if (ctx->graphs[i].uid == c->uid && ctx->graphs[i].key.size() == key.size() &&
+        memcmp(ctx->graphs[i].key.data(), key.data(), key.size() * sizeof(double)) == 0)
+      hit = i;
+  if (hit == ctx->graphs.size()) {
+    // everything that may synchronise or allocate happens before the capture
+    for (auto& grp : groups) csr_scale(ctx, c, grp.sigma);
+    csr_w32(ctx, c);
+    for (int slot = 0; slot < 3; ++slot) scratch(ctx, slot, n * 4 * sizeof(float) + 64);
+    if (c->hf.nets) scratch(ctx, 3, n * 4 * sizeof(float) + 64);
+    Ctx::BankGraph e;
+    e.uid = c->uid;
+    e.key = key;
+    e.gin = dev_alloc(ctx, in_b);
+    e.gout = dev_alloc(ctx, out_b);
+    if (fixed_mask) {
+      e.gmask = static_cast<uint8_t*>(dev_alloc(ctx, n));
+      e.gpos = static_cast<double*>(dev_alloc(ctx, 2 * n * sizeof(double)));
+    }
+    if (!ctx->cap_stream) GIFT_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    // the capture stream must see the buffers' allocations (stream-ordered pool)
+    cudaEvent_t ready;
+    GIFT_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    GIFT_CUDA(cudaEventRecord(ready, ctx->stream));
+    GIFT_CUDA(cudaStreamWaitEvent(ctx->cap_stream, ready, 0));
+    GIFT_CUDA(cudaStreamSynchronize(ctx->cap_stream));
+    cudaEventDestroy(ready);
+    cudaStream_t user = ctx->stream;
+    const int64_t l0 = ctx->launches;
+    cudaGraph_t graph = nullptr;
+    ctx->stream = ctx->cap_stream;
+    try {
+      GIFT_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      bank_fp32(ctx, c, groups, ncols, in_dtype, e.gin, out_dtype, e.gout, e.gmask, e.gpos, region);
+      GIFT_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+      GIFT_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
+    } catch (...) {
+      cudaGraph_t dummy = nullptr;
+      cudaStreamEndCapture(ctx->stream, &dummy);
+      if (dummy) cudaGraphDestroy(dummy);
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      ctx->stream = user;
+      free_bank_graph(ctx, e);
+      throw;
+    }
+    ctx->stream = user;
+    cudaGraphDestroy(graph);
+    e.kernels = ctx->launches - l0;
+    ctx->launches = l0;
+    if (ctx->graphs.size() >= kMaxGraphs) {
+      free_bank_graph(ctx, ctx->graphs.front());
+      ctx->graphs.erase(ctx->graphs.begin());
+    }
+    ctx->graphs.push_back(std::move(e));
+    hit = ctx->graphs.size() - 1;
+  } else if (hit + 1 != ctx->graphs.size()) {  // most recent last
+    Ctx::BankGraph e = std::move(ctx->graphs[hit]);
+    ctx->graphs.erase(ctx->graphs.begin() + hit);
+    ctx->graphs.push_back(std::move(e));
+    hit = ctx->graphs.size() - 1;
+  }
+  Ctx::BankGraph& e = ctx->graphs[hit];
+  cudaStream_t st = ctx->stream;
+  GIFT_CUDA(cudaMemcpyAsync(e.gin, g, in_b, cudaMemcpyDefault, st));
+  if (fixed_mask) {
+    GIFT_CUDA(cudaMemcpyAsync(e.gmask, fixed_mask, n, cudaMemcpyDefault, st));
+    GIFT_CUDA(cudaMemcpyAsync(e.gpos, fixed_pos, 2 * n * sizeof(double), cudaMemcpyDefault, st));
+  }
+  GIFT_CUDA(cudaGraphLaunch(e.exec, st));
+  GIFT_CUDA(cudaMemcpyAsync(out, e.gout, out_b, cudaMemcpyDefault, st));
+  ctx->launches += e.kernels;
+  c->fp32_hops += 4;
+  return true;
+}
+
 void filter(Ctx* ctx, Csr* c, int n_terms, const double* sigma, const int64_t* k, const double* alpha, int64_t ncols,
             int in_dtype, const void* g, int out_dtype, void* out, const uint8_t* fixed_mask, const double* fixed_pos,
             const double* region, int precision) {
@@ -839,9 +995,11 @@ void filter(Ctx* ctx, Csr* c, int n_terms, const double* sigma, const int64_t* k
   auto groups = plan_groups(n_terms, sigma, k, alpha);
   if (precision == GIFT_PREC_FP64_EXACT)
     bank_fp64_exact(ctx, c, groups, ncols, in_dtype, g, out_dtype, out, fixed_mask, fixed_pos, region);
-  else if (precision == GIFT_PREC_FP32)
-    bank_fp32(ctx, c, groups, ncols, in_dtype, g, out_dtype, out, fixed_mask, fixed_pos, region);
-  else
+  else if (precision == GIFT_PREC_FP32) {
+    if (!bank_graph(ctx, c, groups, n_terms, sigma, k, alpha, ncols, in_dtype, g, out_dtype, out, fixed_mask,
+                    fixed_pos, region))
+      bank_fp32(ctx, c, groups, ncols, in_dtype, g, out_dtype, out, fixed_mask, fixed_pos, region);
+  } else
     throw_error(GIFT_ERR_VALUE, "unknown precision");
 }
 

@@ -200,5 +200,7 @@ __device__ __forceinline__ void row_epilogue(const HopArgs& a, int64_t row, floa
 struct Csr;
 // block-major tiled hop (bmt.cu); false when not applicable -> caller uses the row kernel
 bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout);
+// whether bmt_hop could ever serve (or build a tiled copy for) this graph
+bool bmt_possible(Ctx* ctx, const Csr* c);
 
 }  // namespace gift

@@ -19,8 +19,10 @@ libgiftb200.so.
   "fp32"  (default) fused pre-scaled bank, sigma chains packed per pass,
           <= 1e-5 relative L2 against the reference (north star);
   "fp64"  reference operation order in fp64 -- bit-identical output.
-Outputs are float64 numpy arrays like the reference's; fixed rows are copied
-exactly from the fp64 fixed positions in either mode.
+Outputs are float64 numpy arrays like the reference's (fixed rows copied
+exactly from the fp64 fixed positions in either mode);
+`GiftConfig.output_dtype="float32"` returns float32 instead (the configs'
+"N x 2 fp32 output", half the device-to-host bytes).
 """
 
 from __future__ import annotations
@@ -52,6 +54,7 @@ class GiftConfig:
     seed: int = 0
     jitter_scale: float | None = None  # None = JITTER_REGION_FRACTION * min region dim
     precision: str = "fp32"            # extension: "fp32" (fast, fused) | "fp64" (bit-exact)
+    output_dtype: str = "float64"      # extension: "float64" (reference) | "float32" (half the D2H bytes)
 
     def __post_init__(self) -> None:
         self.terms = tuple(self.terms)
@@ -59,6 +62,8 @@ class GiftConfig:
             raise ValueError("filter needs at least one term")
         if self.precision not in _PRECISIONS:
             raise ValueError(f"precision must be one of {sorted(_PRECISIONS)}, got {self.precision!r}")
+        if self.output_dtype not in ("float64", "float32"):
+            raise ValueError(f"output_dtype must be 'float64' or 'float32', got {self.output_dtype!r}")
 
 
 def _jitter_scale(design, config: GiftConfig) -> float:
@@ -98,7 +103,8 @@ def _run_bank(adj: SparseSymMatrix, g: np.ndarray, config: GiftConfig, design=No
     ncols = 1 if g.ndim == 1 else int(np.prod(g.shape[1:]))
     ctx = _lib.context()
     dg = torch.from_numpy(np.ascontiguousarray(g).reshape(adj.n, ncols)).cuda()
-    out = torch.empty((adj.n, ncols), dtype=torch.float64, device=dg.device)
+    f32_out = config.output_dtype == "float32"
+    out = torch.empty((adj.n, ncols), dtype=torch.float32 if f32_out else torch.float64, device=dg.device)
     sig, kk, al = _term_arrays(config.terms)
     in_dtype = _lib.GIFT_DTYPE_F32 if g.dtype == np.float32 else _lib.GIFT_DTYPE_F64
     mask_p = pos_p = None
@@ -115,7 +121,8 @@ def _run_bank(adj: SparseSymMatrix, g: np.ndarray, config: GiftConfig, design=No
         region = np.array([r.xmin, r.ymin, r.xmax, r.ymax], dtype=np.float64)
     st = lib.gift_filter(
         ctx, adj.handle, len(sig), sig.ctypes.data_as(_lib.c_dp), kk.ctypes.data_as(_lib.c_i64p),
-        al.ctypes.data_as(_lib.c_dp), ncols, in_dtype, _lib.dptr(dg), _lib.GIFT_DTYPE_F64, _lib.dptr(out),
+        al.ctypes.data_as(_lib.c_dp), ncols, in_dtype, _lib.dptr(dg),
+        _lib.GIFT_DTYPE_F32 if f32_out else _lib.GIFT_DTYPE_F64, _lib.dptr(out),
         mask_p, pos_p, region.ctypes.data_as(_lib.c_dp) if region is not None else None,
         _PRECISIONS[config.precision])
     _lib.check(st)

@@ -87,6 +87,7 @@ class SparseSymMatrix:
         self._nnz = int(nnz.value)
         self._host = None
         self._degrees = None
+        self._implicit_nets = 0
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -105,6 +106,11 @@ class SparseSymMatrix:
     @property
     def n(self) -> int:
         return self._n
+
+    @property
+    def implicit_nets(self) -> int:
+        """Nets carried by the implicit high-fanout term (0 = a plain CSR)."""
+        return self._implicit_nets
 
     @property
     def nnz(self) -> int:
@@ -179,13 +185,20 @@ class SparseSymMatrix:
         return out
 
     def to_dense(self, limit: int = DENSE_LIMIT) -> np.ndarray:
+        self._explicit_only("to_dense")
         if self.n > limit:
             raise TooLargeForDenseError(self.n, limit)
         return self.to_scipy().toarray()
 
+    def _explicit_only(self, what: str) -> None:
+        if self._implicit_nets:
+            raise ValueError(f"{what}: the graph has an implicit high-fanout term ({self._implicit_nets} nets); "
+                             "build it with high_fanout='skip' or max_clique_pins=None for an explicit matrix")
+
     def to_scipy(self):
         import scipy.sparse as sp
 
+        self._explicit_only("to_scipy")
         indptr, indices, values = self._mirror()
         return sp.csr_matrix((values, indices, indptr), shape=(self.n, self.n))
 
@@ -234,14 +247,27 @@ def from_coo(n: int, rows, cols, vals) -> SparseSymMatrix:
     return SparseSymMatrix._from_handle(_coo_handle(n, rows, cols, vals, True))
 
 
-def build_clique_graph(design, max_clique_pins: int | None = None) -> SparseSymMatrix:
+def build_clique_graph(design, max_clique_pins: int | None = None, *, high_fanout: str = "skip") -> SparseSymMatrix:
     """Expand every net into a clique with edge weight 2/M (M = pin count), on the GPU.
 
     Same contract as graph.py:120-158: weights of parallel nets accumulate,
     pins of one net on the same cell produce no edge, nets with < 2 pins are
     ignored, nets above `max_clique_pins` are skipped (and logged).
     Accepts a `Design` (object model) or a `FlatDesign` (array native).
+
+    high_fanout (extension, keyword only): "skip" is the reference behaviour;
+    "implicit" keeps the nets above the cap as an O(pins) implicit clique term
+    (csrc/hf.cu) instead of dropping them, so the filter sees the UNCAPPED
+    clique graph (A_cap explicit + sum_e (2/m)(b b^T - diag(b o b))) without
+    its O(m^2) entries.  `indptr`/`indices`/`values` then hold the explicit
+    part only; `degrees`, `matmul`, `gift_filter` and `gift_place` use the
+    whole operator (fp32 within 1e-5 of the uncapped reference; no bit-exact
+    contract for the implicit part).
     """
+    if high_fanout not in ("skip", "implicit"):
+        raise ValueError(f"high_fanout must be 'skip' or 'implicit', got {high_fanout!r}")
+    if high_fanout == "implicit" and max_clique_pins is None:
+        raise ValueError("high_fanout='implicit' needs a max_clique_pins cap")
     torch = _lib.torch_cuda()
     lib = _lib.load_library()
     net_start, pin_cell = pin_arrays(design)
@@ -254,9 +280,15 @@ def build_clique_graph(design, max_clique_pins: int | None = None) -> SparseSymM
     skipped = ctypes.c_int64(0)
     _lib.check(lib.gift_build_clique_graph(ctx, n, len(net_start) - 1, _lib.dptr(d_ns), _lib.dptr(d_pc), cap,
                                            ctypes.byref(h), ctypes.byref(skipped)))
-    if skipped.value:
+    adj = SparseSymMatrix._from_handle(h.value)
+    if high_fanout == "implicit":
+        kept = ctypes.c_int64(0)
+        _lib.check(lib.gift_csr_attach_high_fanout(ctx, adj.handle, len(net_start) - 1, _lib.dptr(d_ns),
+                                                   _lib.dptr(d_pc), cap, ctypes.byref(kept)))
+        adj._implicit_nets = int(kept.value)
+    elif skipped.value:
         log.info("clique expansion skipped %d nets with more than %d pins", skipped.value, max_clique_pins)
-    return SparseSymMatrix._from_handle(h.value)
+    return adj
 
 
 def normalized_augmented_adjacency(adj: SparseSymMatrix, sigma: float) -> SparseSymMatrix:

@@ -474,6 +474,8 @@ def cuda_sharded_filter(adj, world: int, rank: int, device: int, exchange=None, 
     so it is the single-GPU vector."""
     from . import _lib
 
+    if getattr(adj, "implicit_nets", 0):
+        raise ValueError("row sharding does not support the implicit high-fanout term")
     be = CudaBackend(device)
     ex = exchange or TorchExchange(group=group, device=f"cuda:{device}")
     lib = _lib.load_library()

@@ -626,12 +626,15 @@ def test_filter_host_pinned_in_place_matches_staged(gb, config, scale):
                                         reg.ctypes.data_as(_lib.c_dp), _lib.GIFT_PREC_FP32))
 
     out_pg = np.empty((fd.num_cells, 2))
-    run(g32.ctypes.data, out_pg.ctypes.data, mask.ctypes.data, pos.ctypes.data)
+    # twice: the first bank on the graph runs the row kernel, the second builds
+    # and runs the tiled copy (graphs above the tiled-hop size threshold)
+    for _ in range(2):
+        run(g32.ctypes.data, out_pg.ctypes.data, mask.ctypes.data, pos.ctypes.data)
     h_g = torch.from_numpy(g32.copy()).pin_memory()
     h_m = torch.from_numpy(mask.copy()).pin_memory()
     h_p = torch.from_numpy(pos.copy()).pin_memory()
     h_o = torch.full((fd.num_cells, 2), np.nan, dtype=torch.float64).pin_memory()
-    for _ in range(2):  # twice: the BMT copy is built by the first call
+    for _ in range(2):
         run(h_g.data_ptr(), h_o.data_ptr(), h_m.data_ptr(), h_p.data_ptr())
         assert_bits_equal(h_o.numpy(), out_pg, "pinned in-place output vs staged")
     fixed = mask.astype(bool)
@@ -729,3 +732,95 @@ def test_device_row_split_matches_host_restatement(gb, world):
             assert np.array_equal(np.asarray(blk.indptr, np.int64), ptr)
             assert np.array_equal(np.asarray(blk.indices, np.int64), idx.astype(np.int64))
             assert_bits_equal(blk.values, values[pos], f"rank {rank} block values")
+
+
+# ------------------------------------- high-fanout nets (opt-in extension) --
+
+HF_CASES = [("c0", 1.0, None, 20), ("c1", 0.3, None, 40), ("c2", 0.01, 600, 200), ("dupnets", 0, 0, 4)]
+
+
+@pytest.mark.parametrize("config,scale,window,cap", HF_CASES)
+def test_implicit_high_fanout_matches_uncapped_oracle(gb, orc, golden, monkeypatch, config, scale, window, cap):
+    """build_clique_graph(..., high_fanout="implicit"): nets above the cap
+    become the O(pins) implicit clique term (csrc/hf.cu).  The explicit part is
+    the capped graph bit for bit; degrees, matmul and both banks match the
+    UNCAPPED oracle (the reference's graph without the skip): fp64 to ~1e-12,
+    fp32 within the 1e-5 bar, on the row kernel and on the tiled kernels."""
+    from paper_2502_17632_b200 import synth
+
+    if config == "dupnets":  # repeated cells inside nets: multiplicities b > 1
+        n = int(golden["dupnets__n"][0])
+        fd = flat(gb, golden["dupnets__net_start"], golden["dupnets__pin_cell"], n)
+    else:
+        fd = synth.generate(config, seed=7, scale=scale, window=window)
+    adj = gb.build_clique_graph(fd, max_clique_pins=cap, high_fanout="implicit")
+    assert adj.implicit_nets > 0
+    capped = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, cap)
+    csr_equal(adj, capped.indptr, capped.indices, capped.data, f"{config}: explicit part")
+    full = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, None)
+    deg = orc.degrees(full)
+    assert rel_l2(adj.degrees, deg) <= 1e-13
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((fd.num_cells, 2)) * 10.0
+    assert rel_l2(adj.matmul(x), orc.matmul(full, x)) <= 1e-13
+    g32 = (rng.standard_normal((fd.num_cells, 2)) * 10.0 + 500.0).astype(np.float32)
+    want = orc.gift_filter(full, g32.astype(np.float64), DEFAULT, deg)
+    got64 = gb.gift_filter(adj, g32, gb.GiftConfig(precision="fp64"))
+    assert rel_l2(got64, want) <= 1e-12
+    got = gb.gift_filter(adj, g32)
+    assert rel_l2(got, want) <= FP32_TOL
+    assert rel_l2(got - 500.0, want - 500.0) <= FP32_TOL
+    assert np.array_equal(gb.gift_filter(adj, g32), got)  # deterministic
+    # the capped (reference-semantics) filter really differs: the term matters
+    assert rel_l2(orc.gift_filter(capped, g32.astype(np.float64), DEFAULT), want) > 10 * FP32_TOL
+    if config != "dupnets":
+        monkeypatch.setenv("GIFT_BMT_MIN_ROWS", "1")
+        monkeypatch.setenv("GIFT_BMT_MIN_MEAN", "1")
+        gb.set_tiled_policy("always")
+        try:
+            adj2 = gb.build_clique_graph(fd, max_clique_pins=cap, high_fanout="implicit")
+            tiled = gb.gift_filter(adj2, g32)
+            assert adj2.tiled_info()["f4"]["built"]
+        finally:
+            gb.set_tiled_policy("on_reuse")
+        assert rel_l2(tiled, want) <= FP32_TOL
+        placed, _ = gb.gift_place(fd, adj, gb.GiftConfig(seed=1, jitter_scale=10.0))
+        mask = fd.fixed_mask()
+        assert np.array_equal(placed[mask], fd.fixed_positions()[mask])
+    with pytest.raises(ValueError):
+        adj.to_scipy()
+    with pytest.raises(ValueError):
+        gb.normalized_augmented_adjacency(adj, 2.0)
+
+
+def test_small_graph_bank_replays_as_cuda_graph(gb, monkeypatch):
+    """Below the tiled-hop threshold the fp32 bank is captured once per
+    (graph, terms, widths, dtypes, epilogue) and replayed as a CUDA graph; the
+    replay runs the same kernels in the same order, so results are bit-identical
+    to direct launches, for every key (signal width, terms, epilogue region)."""
+    from paper_2502_17632_b200 import _lib, synth
+
+    fd = synth.generate("c0", seed=8, scale=0.5)
+    g32 = synth.signal_fp32(fd, seed=4)
+    cfg = gb.GiftConfig(seed=4, jitter_scale=10.0)
+    terms = (gb.FilterTerm(1.0, 3, 0.5), gb.FilterTerm(3.0, 1, 0.5))
+
+    def runs():
+        adj = gb.build_clique_graph(fd)
+        out = [gb.gift_filter(adj, g32), gb.gift_filter(adj, g32[:, :1].copy()),
+               gb.gift_filter(adj, g32, gb.GiftConfig(terms=terms)), gb.gift_place(fd, adj, cfg)[0]]
+        out.append(gb.gift_filter(adj, g32))  # replay of the first key
+        del adj
+        adj = gb.build_clique_graph(fd)  # a new graph (possibly at the same address) captures anew
+        out.append(gb.gift_place(fd, adj, cfg)[0])
+        return out
+
+    monkeypatch.setenv("GIFT_GRAPHS", "0")
+    direct = runs()
+    monkeypatch.setenv("GIFT_GRAPHS", "1")
+    n0 = _lib.launch_count()
+    graphed = runs()
+    assert _lib.launch_count() > n0  # replayed kernels are counted
+    for a, b in zip(direct, graphed):
+        assert np.array_equal(np.asarray(a).view(np.int64), np.asarray(b).view(np.int64))
+    assert np.array_equal(graphed[0], graphed[4])
