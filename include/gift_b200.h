@@ -76,6 +76,14 @@ int64_t gift_last_error_arg(void);
 const char* gift_version(void);
 /* Tiled-copy policy of this context (GIFT_TILED_*). */
 int gift_ctx_set_tiled_policy(gift_ctx* ctx, int policy);
+/* Kernel-selection options of this context (results stay within the fp32
+ * tolerance whatever they are; defaults are the tuned choices):
+ *   "tiled" 0/1, "tiled_min_rows", "tiled_min_mean" (when the tiled hop applies),
+ *   "tile_rows" 0/4096/8192/16384 and "col_bits" 0/11..14 (force a tile shape),
+ *   "barrier_free" 0/1, "graphs" 0/1 (CUDA-graph replay of small banks),
+ *   "zero_copy" 0/1 (pinned host buffers used in place), "schedule" 0/1,
+ *   "row_lanes" 0/8/16/32.  Unknown names or values: GIFT_ERR_VALUE. */
+int gift_ctx_set_option(gift_ctx* ctx, const char* name, int64_t value);
 /* Number of kernels this library launched on ctx since creation (for the bench's gpu_launches). */
 int64_t gift_ctx_launch_count(const gift_ctx* ctx);
 /* Launch timing: when on, every filter-bank kernel is bracketed by CUDA

@@ -58,6 +58,7 @@ SIGNATURES = [
     ("gift_last_error_arg", c_i64, []),
     ("gift_version", ctypes.c_char_p, []),
     ("gift_ctx_set_tiled_policy", c_int, [c_vp, c_int]),
+    ("gift_ctx_set_option", c_int, [c_vp, ctypes.c_char_p, c_i64]),
     ("gift_csr_tiled_info", c_int, [c_vp, c_int, c_i64p]),
     ("gift_ctx_launch_count", c_i64, [c_vp]),
     ("gift_ctx_set_profiling", c_int, [c_vp, c_int]),
@@ -107,6 +108,7 @@ _lib = None
 _lock = threading.Lock()
 _ctxs: dict[tuple[int, int], int] = {}  # (thread id, device) -> gift_ctx*
 _policy = GIFT_TILED_ON_REUSE
+_options: dict[str, int] = {}
 
 
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
@@ -168,6 +170,8 @@ def context(device: int | None = None) -> int:
         check(lib.gift_ctx_create(dev, ctypes.byref(h)))
         ctx = h.value
         check(lib.gift_ctx_set_tiled_policy(ctx, _policy))
+        for name, value in _options.items():
+            check(lib.gift_ctx_set_option(ctx, name.encode(), int(value)))
         with _lock:
             _ctxs[key] = ctx
     stream = torch.cuda.current_stream(dev).cuda_stream
@@ -189,6 +193,47 @@ def set_tiled_policy(policy: str) -> None:
         ctxs = list(_ctxs.values())
     for ctx in ctxs:
         check(lib.gift_ctx_set_tiled_policy(ctx, _policy))
+
+
+DEFAULT_OPTIONS = {"tiled": 1, "tiled_min_rows": 262144, "tiled_min_mean": 32, "tile_rows": 0, "col_bits": 0,
+                   "barrier_free": 1, "graphs": 1, "zero_copy": 1, "schedule": 1, "row_lanes": 0}
+
+
+def set_option(name: str, value: int) -> None:
+    """Kernel-selection option (gift_ctx_set_option) for every context, present
+    and future: tiled, tiled_min_rows, tiled_min_mean, tile_rows, col_bits,
+    barrier_free, graphs, zero_copy, schedule, row_lanes."""
+    if name not in DEFAULT_OPTIONS:
+        raise ValueError(f"unknown option {name!r}")
+    lib = load_library()
+    with _lock:
+        ctxs = list(_ctxs.values())
+    for ctx in ctxs:
+        check(lib.gift_ctx_set_option(ctx, name.encode(), int(value)))
+    if value == DEFAULT_OPTIONS[name]:
+        _options.pop(name, None)
+    else:
+        _options[name] = int(value)
+
+
+class options:
+    """Context manager: `with options(tiled_min_rows=1): ...` sets kernel
+    options and restores the previous values on exit (tests, sweeps)."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.prev = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.prev[k] = _options.get(k, DEFAULT_OPTIONS.get(k))
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.prev.items():
+            set_option(k, v)
+        return False
 
 
 def launch_count(device: int | None = None) -> int:

@@ -109,6 +109,56 @@ void* pinned(Ctx* ctx, size_t bytes) {
   return ctx->pinned;
 }
 
+void set_option(Ctx* ctx, const std::string& name, int64_t v) {
+  auto bad = [&]() { throw_error(GIFT_ERR_VALUE, "bad value " + std::to_string(v) + " for option " + name); };
+  Ctx::Options& o = ctx->opt;
+  if (name == "tiled") {
+    if (v != 0 && v != 1) bad();
+    o.tiled = v;
+  } else if (name == "tiled_min_rows") {
+    if (v < 0) bad();
+    o.tiled_min_rows = v;
+  } else if (name == "tiled_min_mean") {
+    if (v < 0) bad();
+    o.tiled_min_mean = v;
+  } else if (name == "tile_rows") {
+    if (v != 0 && v != 4096 && v != 8192 && v != 16384
+#ifdef GIFT_TUNING
+        && v != 1024 && v != 2048
+#endif
+    )
+      bad();
+    o.tile_rows = v;
+  } else if (name == "col_bits") {
+    if (v != 0 && (v < 11 || v > 14)) bad();
+    o.col_bits = v;
+  } else if (name == "barrier_free" || name == "graphs" || name == "zero_copy" || name == "schedule") {
+    if (v != 0 && v != 1) bad();
+    (name == "barrier_free" ? o.barrier_free : name == "graphs" ? o.graphs : name == "zero_copy" ? o.zero_copy
+                                                                                               : o.schedule) = v;
+  } else if (name == "row_lanes") {
+    if (v != 0 && v != 8 && v != 16 && v != 32) bad();
+    o.row_lanes = v;
+  } else {
+    throw_error(GIFT_ERR_VALUE, "unknown option " + name);
+  }
+}
+
+#ifdef GIFT_TUNING
+// tuning builds: the GIFT_* environment variables of the sweep tools (tools/)
+static void options_from_env(Ctx* ctx) {
+  const std::pair<const char*, const char*> names[] = {
+      {"GIFT_BMT", "tiled"},          {"GIFT_BMT_MIN_ROWS", "tiled_min_rows"}, {"GIFT_BMT_MIN_MEAN", "tiled_min_mean"},
+      {"GIFT_BMT_TILE_ROWS", "tile_rows"}, {"GIFT_BMT_COL_BITS", "col_bits"}, {"GIFT_BMT_NB", "barrier_free"},
+      {"GIFT_GRAPHS", "graphs"},      {"GIFT_ZERO_COPY", "zero_copy"},        {"GIFT_BMT_SCHEDULE", "schedule"},
+      {"GIFT_HOP_G", "row_lanes"}};
+  for (auto& nv : names) {
+    const char* v = std::getenv(nv.first);
+    if (v && *v) set_option(ctx, nv.second, std::atoll(v));
+  }
+}
+#endif
+
 void* csr_alloc(Ctx* ctx, Csr* c, size_t bytes) {
   void* p = dev_alloc(ctx, bytes + 64);  // vector loads may read up to 3 elements past the end
   c->owned.push_back(p);
@@ -228,6 +278,14 @@ int gift_ctx_create(int device, gift_ctx** out) {
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   cudaDeviceGetAttribute(&c->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+#ifdef GIFT_TUNING
+  try {
+    gift::options_from_env(c);
+  } catch (...) {
+    delete c;
+    throw;
+  }
+#endif
   *out = c;
   GIFT_API_END
 }
@@ -415,8 +473,7 @@ int gift_filter_host(gift_ctx* ctx, gift_csr* adj, int n_terms, const double* h_
   // fp32 bank writes each output row exactly once, from its final hop, so the
   // placement streams to the host while that hop runs instead of after it;
   // fixed centres are read only for fixed rows.  Pageable buffers are staged.
-  const char* zc_env = std::getenv("GIFT_ZERO_COPY");
-  const bool zc = !(zc_env && zc_env[0] == '0');
+  const bool zc = ctx->opt.zero_copy != 0;
   void* z_out = (zc && precision == GIFT_PREC_FP32) ? mapped_host(h_out) : nullptr;
   const double* z_pos = (zc && h_fixed_mask) ? static_cast<const double*>(mapped_host(h_fixed_pos)) : nullptr;
   gift::DevBuf<char> dg(ctx, in_b), dout(ctx, z_out ? 0 : out_b);
@@ -456,8 +513,7 @@ int gift_place_host(gift_ctx* ctx, int64_t n_cells, int64_t n_nets, const int64_
     const int64_t n = n_cells;
     const size_t out_b = (size_t)(n * 2) * (out_dtype == GIFT_DTYPE_F64 ? 8 : 4);
     // pinned host buffers in place, as in gift_filter_host
-    const char* zc_env = std::getenv("GIFT_ZERO_COPY");
-    const bool zc = !(zc_env && zc_env[0] == '0');
+    const bool zc = ctx->opt.zero_copy != 0;
     void* z_out = (zc && precision == GIFT_PREC_FP32) ? mapped_host(h_out) : nullptr;
     const double* z_pos = (zc && h_fixed_mask) ? static_cast<const double*>(mapped_host(h_fixed_pos)) : nullptr;
     gift::DevBuf<float> dg(ctx, 2 * n);
@@ -635,6 +691,14 @@ int gift_csr_ext_ids(const gift_csr* ghost, const int64_t** d_ids, int64_t* n_id
   require(ghost && d_ids && n_ids, GIFT_ERR_VALUE, "null argument");
   *d_ids = ghost->ext_ids;
   *n_ids = ghost->ext_n;
+  GIFT_API_END
+}
+
+int gift_ctx_set_option(gift_ctx* ctx, const char* name, int64_t value) {
+  GIFT_API_BEGIN
+  require(ctx && name, GIFT_ERR_VALUE, "null argument");
+  std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+  gift::set_option(ctx, name, value);
   GIFT_API_END
 }
 

@@ -83,12 +83,10 @@ namespace {
 struct BmtShape {
   int kR, cb;
 };
-BmtShape bmt_shape_for(double mean_row, bool wide_blocks) {
+BmtShape bmt_shape_for(const Ctx* ctx, double mean_row, bool wide_blocks) {
   BmtShape s = wide_blocks ? BmtShape{8192, 14} : (mean_row >= 160.0 ? BmtShape{8192, 12} : BmtShape{4096, 13});
-  const int fr = env_int("GIFT_BMT_TILE_ROWS", 0);  // 1024 .. 16384 (tuning)
-  if (fr == 1024 || fr == 2048 || fr == 4096 || fr == 8192 || fr == 16384) s.kR = fr;
-  const int fc = env_int("GIFT_BMT_COL_BITS", 0);  // 11..14 (tuning)
-  if (fc >= 11 && fc <= 14) s.cb = fc;
+  if (ctx->opt.tile_rows) s.kR = (int)ctx->opt.tile_rows;  // forced shape (option "tile_rows")
+  if (ctx->opt.col_bits) s.cb = (int)ctx->opt.col_bits;    // option "col_bits"
   return s;
 }
 constexpr int kPadRows = 16;      // one zero row per bank residue mod 16 (padding never conflicts)
@@ -969,11 +967,18 @@ size_t bmt_smem_nb(int fin, int kR, int kC) { return 2 * ((size_t)(kC + kPadRows
 
 size_t bmt_smem(int fin, int kR, int kC) { return (size_t)(kC + kPadRows) * fin * 4 + (size_t)kR * fin * 4; }
 
+#ifdef GIFT_TUNING
 size_t bmt_smem_db(int fin, int kR, int kC) { return bmt_smem(fin, kR, kC) + (size_t)(kC + kPadRows) * fin * 4; }
+#endif
 
 template <int FIN, int FOUT, bool DB>
 void launch_bmt_k(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, int tpb, size_t smem) {
+#ifdef GIFT_TUNING
   auto kern = tpb == 1024 ? k_hop_bmt<FIN, FOUT, 1024, DB> : k_hop_bmt<FIN, FOUT, 512, DB>;
+#else
+  auto kern = k_hop_bmt<FIN, FOUT, 1024, DB>;  // default shapes are >= 4096 rows: 1 CTA x 1024 per SM
+  (void)tpb;
+#endif
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, int> occ;  // resident CTAs per SM per (instance, device)
   int per_sm = 0;
@@ -1026,29 +1031,38 @@ void launch_bmt(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles) {
   // (A/B on B200: c4 F=2 pass 1.83 -> 1.63 ms at 1 x 1024; c3 F=4 pass 1.16 ->
   // 1.25 ms when its 197 KB footprint drops it from 2 x 512 to 1 x 1024).  The
   // bulk copies need a 16-byte aligned signal.
-  if (env_int("GIFT_BMT_NB", 1) && !b.ctr && ((uintptr_t)a.zin & 15) == 0) {
+  if (ctx->opt.barrier_free && !b.ctr && ((uintptr_t)a.zin & 15) == 0) {
     const size_t nb = bmt_smem_nb(FIN, b.tile_rows, b.kC), fixed = 3 * 1024;
+#ifdef GIFT_TUNING
     if (b.tile_rows <= 2048 && 2 * (nb + fixed) <= 228 * 1024) {
       launch_bmt_nb<FIN, FOUT, 512>(ctx, a, b, ntiles, nb);
       return;
     }
+#endif
     if (b.tile_rows > 2048 && nb + fixed <= 228 * 1024) {
       launch_bmt_nb<FIN, FOUT, 1024>(ctx, a, b, ntiles, nb);
       return;
     }
   }
-  // 2048-row tiles: 2 CTAs x 512 threads per SM when two fit; taller tiles
-  // (or a footprint only one CTA fits): 1 CTA x 1024.  Double-buffered staging
-  // when both buffers fit at that occupancy.
-  const size_t smem1 = bmt_smem(FIN, b.tile_rows, b.kC), smem2 = bmt_smem_db(FIN, b.tile_rows, b.kC);
+  // the barrier kernel: 1 CTA x 1024 threads per SM on the default (>= 4096-row)
+  // tiles.  Tuning builds also have 2 x 512 for 2048-row tiles and a
+  // double-buffered (cp.async) variant; neither won on the default shapes
+  // (DESIGN.md §4).
+  const size_t smem1 = bmt_smem(FIN, b.tile_rows, b.kC);
+#ifdef GIFT_TUNING
+  const size_t smem2 = bmt_smem_db(FIN, b.tile_rows, b.kC);
   const int tpb = (b.tile_rows > 2048 || 2 * (smem1 + 3 * 1024) > 228 * 1024) ? 1024 : 512;
   const int per_sm = tpb == 512 ? 2 : 1;
   const bool db = env_int("GIFT_BMT_DB", 1) && ((uintptr_t)a.zin & 15) == 0 &&
                   (size_t)per_sm * (smem2 + 3 * 1024) <= 228 * 1024;
-  if (db)
+  if (db) {
     launch_bmt_k<FIN, FOUT, true>(ctx, a, b, ntiles, tpb, smem2);
-  else
-    launch_bmt_k<FIN, FOUT, false>(ctx, a, b, ntiles, tpb, smem1);
+    return;
+  }
+  launch_bmt_k<FIN, FOUT, false>(ctx, a, b, ntiles, tpb, smem1);
+#else
+  launch_bmt_k<FIN, FOUT, false>(ctx, a, b, ntiles, 1024, smem1);
+#endif
 }
 
 template <int FIN>
@@ -1090,7 +1104,7 @@ void exclusive_sum(Ctx* ctx, const int64_t* in, int64_t* out, int64_t n) {
 bool bmt_build(Ctx* ctx, Csr* c, const float* w32, Csr::Bmt& B, bool wide_blocks) {
   cudaStream_t st = ctx->stream;
   const int64_t n = c->n, nnz_all = c->nnz;
-  const BmtShape shape = bmt_shape_for(c->mean_row, wide_blocks);
+  const BmtShape shape = bmt_shape_for(ctx, c->mean_row, wide_blocks);
   const int kR = shape.kR, cb = shape.cb, kC = 1 << cb;
   const int64_t ntiles = (n + kR - 1) / kR;
   const int64_t nblocks = (n + kC - 1) / kC;
@@ -1316,7 +1330,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32, Csr::Bmt& B, bool wide_blocks
       nseg, seg_run.p, B.seg_slice, run_perm.p, run_start.p, nruns, nnz, cb, pay_s.p, B.slice_off, B.slice_rows, bcol,
       bw);
   GIFT_LAUNCH_CHECK(ctx);
-  if (env_int("GIFT_BMT_SCHEDULE", 1)) {
+  if (ctx->opt.schedule) {
     DevBuf<uint16_t> tcol(ctx, total + 8);
     DevBuf<float> tw(ctx, total + 8);
     k_slice_schedule<<<grid_for(nslices * 32, 256, 1LL << 30), 256, 0, st>>>(nslices, kC, B.slice_off, bcol, bw,
@@ -1380,25 +1394,24 @@ void launch_row_list(Ctx* ctx, cudaStream_t st, const HopArgs& base, const int32
                      int fout, int G);
 
 bool bmt_possible(Ctx* ctx, const Csr* c) {
-  if (env_int("GIFT_BMT", 1) == 0 || !c->sorted_rows || !c->square) return false;
+  if (!ctx->opt.tiled || !c->sorted_rows || !c->square) return false;
   if (ctx->tiled_policy == GIFT_TILED_NEVER && !c->bmt.ready && !c->bmt_wide.ready) return false;
-  return c->n >= env_int("GIFT_BMT_MIN_ROWS", 262144) && c->mean_row >= env_int("GIFT_BMT_MIN_MEAN", 32);
+  return c->n >= ctx->opt.tiled_min_rows && c->mean_row >= (double)ctx->opt.tiled_min_mean;
 }
 
 bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
-  if (env_int("GIFT_BMT", 1) == 0 || !c->sorted_rows || !c->square) return false;
+  if (!ctx->opt.tiled || !c->sorted_rows || !c->square) return false;
   // building the tiled copy costs ~a few hops; only resident graphs amortise it
   // signal widths <= 2 use the wide-block copy, F = 4 its own (unless a
   // tuning shape is forced: then one copy serves every width)
-  const bool wide_blocks = fin <= 2 && env_int("GIFT_BMT_TILE_ROWS", 0) == 0 && env_int("GIFT_BMT_COL_BITS", 0) == 0 &&
-                           env_int("GIFT_BMT_WIDE", 1);
+  const bool wide_blocks = fin <= 2 && ctx->opt.tile_rows == 0 && ctx->opt.col_bits == 0;
   Csr::Bmt& B = wide_blocks ? c->bmt_wide : c->bmt;
   // build policy (GIFT_TILED_*): a graph filtered once (gift_place on a fresh
   // design, cli.py:203-220) never pays for the copy; one filtered again gets it
   if (!B.ready && (ctx->tiled_policy == GIFT_TILED_NEVER ||
                    (ctx->tiled_policy == GIFT_TILED_ON_REUSE && c->fp32_hops < kReuseHops)))
     return false;
-  if (c->n < env_int("GIFT_BMT_MIN_ROWS", 262144) || c->mean_row < env_int("GIFT_BMT_MIN_MEAN", 32)) return false;
+  if (c->n < ctx->opt.tiled_min_rows || c->mean_row < (double)ctx->opt.tiled_min_mean) return false;
   // whole square graphs only; partial sums in (part_in: the high-fanout term)
   // or out (part_out: a shard's local block) pass through the row epilogue
   if (a.row_begin != 0 || a.n != c->n) return false;
@@ -1437,7 +1450,9 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
     GIFT_CUDA(cudaEventRecord(ctx->join_ev, ctx->side));
   }
   unsigned* ctr = nullptr;
-  const int32_t* order = env_int("GIFT_BMT_LPT", 1) ? B.tile_order : nullptr;
+  const int32_t* order = B.tile_order;
+#ifdef GIFT_TUNING
+  if (!env_int("GIFT_BMT_LPT", 1)) order = nullptr;
   if (env_int("GIFT_BMT_PERSIST", 0)) {
     order = B.tile_order;
     unsigned*& slot = ctx->tile_ctr[ctx->stream];
@@ -1447,6 +1462,7 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
     }
     ctr = slot;
   }
+#endif
   BmtArgs b{c->n,         B.tile_rows,  B.kC,         B.data,      B.wide,      B.res_rowptr, B.res_col,     B.res_w,
             B.tile_seg,   B.seg_code,   B.seg_slice, B.slice_off, B.slice_rows, order,         ctr,
             B.ntiles,     B.res_rows,   B.tile_res};

@@ -52,6 +52,20 @@ struct Ctx {
   int num_sms = 148;
   int smem_optin = 0;             // max dynamic shared memory per block (opt-in), this device
   int tiled_policy = GIFT_TILED_ON_REUSE;  // when the fp32 hop builds the tiled (BMT) copy of a graph
+  // kernel-selection options (gift_ctx_set_option; a -DGIFT_TUNING build also
+  // reads them from GIFT_* environment variables at context creation)
+  struct Options {
+    int64_t tiled = 1;              // "tiled": 0 = row kernel only
+    int64_t tiled_min_rows = 262144;  // "tiled_min_rows": smaller graphs stay on the row kernel
+    int64_t tiled_min_mean = 32;    // "tiled_min_mean": mean row length below which too
+    int64_t tile_rows = 0;          // "tile_rows": force the tile height (4096 / 8192 / 16384), 0 = per graph
+    int64_t col_bits = 0;           // "col_bits": force log2 of the block width (11..14), 0 = per graph
+    int64_t barrier_free = 1;       // "barrier_free": the bulk-copy pipeline where it fits
+    int64_t graphs = 1;             // "graphs": replay small-graph banks as CUDA graphs
+    int64_t zero_copy = 1;          // "zero_copy": *_host calls use pinned buffers in place
+    int64_t schedule = 1;           // "schedule": bank-conflict-aware entry order in the tiled copy
+    int64_t row_lanes = 0;          // "row_lanes": force lanes per row of the row kernel (8 / 16 / 32)
+  } opt;
   std::recursive_mutex mu;        // entry points serialise on the context (scratch, stream, logs)
   // persistent BMT tile scheduler counters [next tile, finished CTAs], one
   // pair per stream (launches on one stream never overlap; self-resetting)
@@ -218,6 +232,7 @@ struct Bookshelf {
 void* csr_alloc(Ctx* ctx, Csr* c, size_t bytes);
 void csr_destroy(Csr* c);
 void csr_touch(Ctx* ctx, Csr* c);
+void set_option(Ctx* ctx, const std::string& name, int64_t value);
 
 // ---- launch helpers --------------------------------------------------------
 inline unsigned grid_for(int64_t work, int block, int64_t cap = 148LL * 64) {

@@ -372,22 +372,24 @@ int pow2_ceil(int v) {
 template <int FIN, int FOUT>
 void launch_hop_g(Ctx* ctx, cudaStream_t st, const HopArgs& a, int G) {
   if (a.n <= a.row_begin) return;
-  G = env_int("GIFT_HOP_G", G);
-  const int U = env_int("GIFT_HOP_U", 1);
+  if (ctx->opt.row_lanes) G = (int)ctx->opt.row_lanes;
   const int64_t threads = (a.n - a.row_begin) * (int64_t)G;
   const unsigned grid = (unsigned)((threads + kBlock - 1) / kBlock);
-  if (U >= 2) {
+#ifdef GIFT_TUNING
+  if (env_int("GIFT_HOP_U", 1) >= 2) {  // two 4-entry chunks in flight per lane (tuning sweeps)
     switch (G) {
       case 8: k_hop<FIN, FOUT, 8, 2><<<grid, kBlock, 0, st>>>(a); break;
       case 16: k_hop<FIN, FOUT, 16, 2><<<grid, kBlock, 0, st>>>(a); break;
       default: k_hop<FIN, FOUT, 32, 2><<<grid, kBlock, 0, st>>>(a); break;
     }
-  } else {
-    switch (G) {
-      case 8: k_hop<FIN, FOUT, 8, 1><<<grid, kBlock, 0, st>>>(a); break;
-      case 16: k_hop<FIN, FOUT, 16, 1><<<grid, kBlock, 0, st>>>(a); break;
-      default: k_hop<FIN, FOUT, 32, 1><<<grid, kBlock, 0, st>>>(a); break;
-    }
+    GIFT_LAUNCH_CHECK(ctx);
+    return;
+  }
+#endif
+  switch (G) {
+    case 8: k_hop<FIN, FOUT, 8, 1><<<grid, kBlock, 0, st>>>(a); break;
+    case 16: k_hop<FIN, FOUT, 16, 1><<<grid, kBlock, 0, st>>>(a); break;
+    default: k_hop<FIN, FOUT, 32, 1><<<grid, kBlock, 0, st>>>(a); break;
   }
   GIFT_LAUNCH_CHECK(ctx);
 }
@@ -891,7 +893,7 @@ static bool bank_graph(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, i
                        const int64_t* k, const double* alpha, int64_t ncols, int in_dtype, const void* g,
                        int out_dtype, void* out, const uint8_t* fixed_mask, const double* fixed_pos,
                        const double* region) {
-  if (ctx->profiling || c->n <= 0 || c->n >= kGraphMaxRows || ncols <= 0 || env_int("GIFT_GRAPHS", 1) == 0)
+  if (ctx->profiling || c->n <= 0 || c->n >= kGraphMaxRows || ncols <= 0 || !ctx->opt.graphs)
     return false;
   if (bmt_possible(ctx, c)) return false;  // a tiled-copy build cannot run inside a capture
   const int64_t n = c->n;

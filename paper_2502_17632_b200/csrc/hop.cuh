@@ -12,7 +12,8 @@
 
 namespace gift {
 
-// lanes per row and chunks in flight; GIFT_HOP_G / GIFT_HOP_U override (tuning sweeps)
+// environment knobs of -DGIFT_TUNING builds (tools/ sweeps); the default
+// build takes its options from gift_ctx_set_option only
 inline int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v && *v ? atoi(v) : dflt;

@@ -416,6 +416,17 @@ class ShardedFilter:
         self.sendbuf = backend.empty(len(plan.send_rows), 4)
         self.send_idx = backend.upload(plan.send_rows)
 
+    def block_nnz(self) -> int:
+        """Stored entries of this rank's row block (local + ghost parts)."""
+        from . import _lib
+
+        tot = 0
+        for blk in (self.local, self.ghost):
+            n, nnz = ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(_lib.load_library().gift_csr_shape(blk.h, ctypes.byref(n), ctypes.byref(nnz)))
+            tot += nnz.value
+        return tot
+
     def _exchange(self, z, F):
         p = self.plan
         n, ng = p.n_local, p.n_ghost

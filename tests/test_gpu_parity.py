@@ -33,6 +33,23 @@ def gb():
 
 
 @pytest.fixture
+def opts():
+    """Set kernel options (gift_ctx_set_option) for the test; restored after."""
+    from paper_2502_17632_b200 import _lib
+
+    saved = []
+
+    def set_(**kw):
+        for k, v in kw.items():
+            saved.append((k, _lib._options.get(k, _lib.DEFAULT_OPTIONS[k])))
+            _lib.set_option(k, v)
+
+    yield set_
+    for k, v in reversed(saved):
+        _lib.set_option(k, v)
+
+
+@pytest.fixture
 def tiled_always(gb):
     """Build the tiled copy on a graph's first fp32 hop (default: on reuse)."""
     gb.set_tiled_policy("always")
@@ -439,7 +456,7 @@ def _flat(nets):
 # ---------------------------------------------------------- sharded path --
 
 @pytest.mark.parametrize("world,tiled", [(2, False), (4, False), (2, True), (3, True)])
-def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, monkeypatch, world, tiled):
+def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, opts, world, tiled):
     """The multi-GPU code path (partition, ghost pack, split local/ghost hops,
     fused epilogue) with `world` virtual ranks as threads on one device; the
     all-to-all is replaced by stream-ordered device copies (ThreadExchange),
@@ -453,8 +470,7 @@ def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, monkeypatch, world,
     from paper_2502_17632_b200 import shard, synth
 
     if tiled:
-        monkeypatch.setenv("GIFT_BMT_MIN_ROWS", "1")
-        monkeypatch.setenv("GIFT_BMT_MIN_MEAN", "1")
+        opts(tiled_min_rows=1, tiled_min_mean=1)
         gb.set_tiled_policy("always")
 
     fd = synth.generate("c2", seed=4, scale=0.02, window=600)
@@ -501,36 +517,32 @@ def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, monkeypatch, world,
     assert rel_l2(full, single) <= FP32_TOL
 
 
-@pytest.mark.parametrize("config,scale,cap,tile_rows,db,col_bits,nb", [
-    ("c2", 0.05, 200, 0, 1, 0, 1), ("c3", 0.03, 200, 0, 1, 0, 1), ("c1", 0.2, None, 0, 1, 0, 1),
-    ("c0", 1.0, None, 0, 1, 0, 1), ("c2", 0.01, None, 0, 1, 0, 1), ("c2", 0.05, 200, 4096, 1, 0, 1),
-    ("c1", 0.2, None, 4096, 1, 0, 1), ("c3", 0.03, 200, 2048, 0, 0, 0), ("c1", 0.2, None, 8192, 0, 0, 0),
-    ("c2", 0.05, 200, 2048, 1, 12, 0), ("c1", 0.2, None, 4096, 1, 13, 0), ("c1", 0.2, None, 8192, 1, 12, 0),
-    ("c4", 0.02, 100, 4096, 1, 13, 1), ("c4", 0.02, 100, 2048, 1, 11, 1), ("c2", 0.05, 200, 2048, 1, 14, 1)])
-def test_bmt_hop_matches_oracle_and_row_kernel(gb, orc, monkeypatch, tiled_always, config, scale, cap, tile_rows, db,
-                                               col_bits, nb):
+@pytest.mark.parametrize("config,scale,cap,tile_rows,col_bits,nb", [
+    ("c2", 0.05, 200, 0, 0, 1), ("c3", 0.03, 200, 0, 0, 1), ("c1", 0.2, None, 0, 0, 1),
+    ("c0", 1.0, None, 0, 0, 1), ("c2", 0.01, None, 0, 0, 1), ("c2", 0.05, 200, 4096, 0, 1),
+    ("c1", 0.2, None, 4096, 0, 1), ("c3", 0.03, 200, 16384, 0, 0), ("c1", 0.2, None, 8192, 0, 0),
+    ("c2", 0.05, 200, 4096, 12, 0), ("c1", 0.2, None, 4096, 13, 0), ("c1", 0.2, None, 8192, 12, 0),
+    ("c4", 0.02, 100, 4096, 13, 1), ("c4", 0.02, 100, 4096, 11, 1), ("c2", 0.05, 200, 8192, 14, 1),
+    ("c3", 0.03, 200, 8192, 12, 1)])
+def test_bmt_hop_matches_oracle_and_row_kernel(gb, orc, opts, tiled_always, config, scale, cap, tile_rows, col_bits,
+                                               nb):
     """Force the block-major tiled hop (bmt.cu) on small graphs (it is normally
     reserved for >= 256k rows) and check it against the oracle and the
-    row-parallel kernel; tile heights 2048 / 4096 / 8192, column blocks of
+    row-parallel kernel; tile heights 4096 / 8192 / 16384, column blocks of
     2048 .. 16384 (a shape too large for F = 4 falls back to the row kernel for
-    that pass), the barrier-free pipeline (nb) and the barrier kernels with
-    single- and double-buffered block staging."""
+    that pass), the barrier-free bulk-copy pipeline (nb) and the barrier
+    kernel."""
     from paper_2502_17632_b200 import synth
 
-    monkeypatch.setenv("GIFT_BMT_TILE_ROWS", str(tile_rows))
-    monkeypatch.setenv("GIFT_BMT_COL_BITS", str(col_bits))
-    monkeypatch.setenv("GIFT_BMT_DB", str(db))
-    monkeypatch.setenv("GIFT_BMT_NB", str(nb))
+    opts(tile_rows=tile_rows, col_bits=col_bits, barrier_free=nb)
 
     fd = synth.generate(config, seed=6, scale=scale, window=900)
     ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, cap)
     g32 = synth.signal_fp32(fd, seed=3)
     want = orc.gift_filter(ref, g32.astype(np.float64), DEFAULT)
-    monkeypatch.setenv("GIFT_BMT", "0")
+    opts(tiled=0)
     row_kernel = gb.gift_filter(gb.build_clique_graph(fd, max_clique_pins=cap), g32)
-    monkeypatch.setenv("GIFT_BMT", "1")
-    monkeypatch.setenv("GIFT_BMT_MIN_ROWS", "1")
-    monkeypatch.setenv("GIFT_BMT_MIN_MEAN", "1")
+    opts(tiled=1, tiled_min_rows=1, tiled_min_mean=1)
     adj = gb.build_clique_graph(fd, max_clique_pins=cap)
     tiled = gb.gift_filter(adj, g32)
     info = adj.tiled_info()
@@ -661,14 +673,13 @@ def test_small_caps_skip_nets_like_the_reference(gb, orc, cap):
         csr_equal(adj, ref.indptr, ref.indices, ref.data, f"cap {cap}")
 
 
-def test_tiled_policy(gb, monkeypatch):
+def test_tiled_policy(gb, opts):
     """GIFT_TILED_ON_REUSE (default): the first bank on a graph runs the row
     kernel and leaves no tiled copy; the second builds it.  NEVER never builds;
     ALWAYS builds on the first hop.  Results agree within fp32 rounding."""
     from paper_2502_17632_b200 import synth
 
-    monkeypatch.setenv("GIFT_BMT_MIN_ROWS", "1")
-    monkeypatch.setenv("GIFT_BMT_MIN_MEAN", "1")
+    opts(tiled_min_rows=1, tiled_min_mean=1)
     fd = synth.generate("c2", seed=3, scale=0.02, window=600)
     g32 = synth.signal_fp32(fd, seed=1)
     adj = gb.build_clique_graph(fd, max_clique_pins=200)
@@ -740,7 +751,7 @@ HF_CASES = [("c0", 1.0, None, 20), ("c1", 0.3, None, 40), ("c2", 0.01, 600, 200)
 
 
 @pytest.mark.parametrize("config,scale,window,cap", HF_CASES)
-def test_implicit_high_fanout_matches_uncapped_oracle(gb, orc, golden, monkeypatch, config, scale, window, cap):
+def test_implicit_high_fanout_matches_uncapped_oracle(gb, orc, golden, opts, config, scale, window, cap):
     """build_clique_graph(..., high_fanout="implicit"): nets above the cap
     become the O(pins) implicit clique term (csrc/hf.cu).  The explicit part is
     the capped graph bit for bit; degrees, matmul and both banks match the
@@ -774,8 +785,7 @@ def test_implicit_high_fanout_matches_uncapped_oracle(gb, orc, golden, monkeypat
     # the capped (reference-semantics) filter really differs: the term matters
     assert rel_l2(orc.gift_filter(capped, g32.astype(np.float64), DEFAULT), want) > 10 * FP32_TOL
     if config != "dupnets":
-        monkeypatch.setenv("GIFT_BMT_MIN_ROWS", "1")
-        monkeypatch.setenv("GIFT_BMT_MIN_MEAN", "1")
+        opts(tiled_min_rows=1, tiled_min_mean=1)
         gb.set_tiled_policy("always")
         try:
             adj2 = gb.build_clique_graph(fd, max_clique_pins=cap, high_fanout="implicit")
@@ -793,7 +803,7 @@ def test_implicit_high_fanout_matches_uncapped_oracle(gb, orc, golden, monkeypat
         gb.normalized_augmented_adjacency(adj, 2.0)
 
 
-def test_small_graph_bank_replays_as_cuda_graph(gb, monkeypatch):
+def test_small_graph_bank_replays_as_cuda_graph(gb, opts):
     """Below the tiled-hop threshold the fp32 bank is captured once per
     (graph, terms, widths, dtypes, epilogue) and replayed as a CUDA graph; the
     replay runs the same kernels in the same order, so results are bit-identical
@@ -815,9 +825,9 @@ def test_small_graph_bank_replays_as_cuda_graph(gb, monkeypatch):
         out.append(gb.gift_place(fd, adj, cfg)[0])
         return out
 
-    monkeypatch.setenv("GIFT_GRAPHS", "0")
+    opts(graphs=0)
     direct = runs()
-    monkeypatch.setenv("GIFT_GRAPHS", "1")
+    opts(graphs=1)
     n0 = _lib.launch_count()
     graphed = runs()
     assert _lib.launch_count() > n0  # replayed kernels are counted

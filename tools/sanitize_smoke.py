@@ -9,11 +9,14 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("GIFT_BMT_MIN_ROWS", "1")
-os.environ.setdefault("GIFT_BMT_MIN_MEAN", "1")
+# the tiled hop is forced on small graphs through the option API (below)
 
 import paper_2502_17632_b200 as gb  # noqa: E402
-from paper_2502_17632_b200 import synth  # noqa: E402
+from paper_2502_17632_b200 import _lib, synth  # noqa: E402
+
+_lib.set_option("tiled_min_rows", 1)
+_lib.set_option("tiled_min_mean", 1)
+gb.set_tiled_policy("always")
 
 fd = synth.generate("c2", seed=5, scale=0.004, window=300)
 adj = gb.build_clique_graph(fd, max_clique_pins=200)
