@@ -80,9 +80,13 @@ int gift_ctx_set_tiled_policy(gift_ctx* ctx, int policy);
  * tolerance whatever they are; defaults are the tuned choices):
  *   "tiled" 0/1, "tiled_min_rows", "tiled_min_mean" (when the tiled hop applies),
  *   "tile_rows" 0/4096/8192/16384 and "col_bits" 0/11..14 (force a tile shape),
- *   "barrier_free" 0/1, "graphs" 0/1 (CUDA-graph replay of small banks),
+ *   "barrier_free" 0/1, "fused" 0/1 (small banks as one cooperative kernel),
+ *   "graphs" 0/1 (CUDA-graph replay of small banks the fused kernel does not take),
  *   "zero_copy" 0/1 (pinned host buffers used in place), "schedule" 0/1,
- *   "row_lanes" 0/8/16/32.  Unknown names or values: GIFT_ERR_VALUE. */
+ *   "row_lanes" 0/8/16/32, "codes" 0 (1 only in -DGIFT_TUNING builds: u8
+ *   weight codes in the F <= 2 tiled copy, an experiment that measured slower),
+ *   "prefetch" 0/1 (tiled hop: L2 bulk prefetch of each warp's next slice; off).
+ *   Unknown names or values: GIFT_ERR_VALUE. */
 int gift_ctx_set_option(gift_ctx* ctx, const char* name, int64_t value);
 /* Number of kernels this library launched on ctx since creation (for the bench's gpu_launches). */
 int64_t gift_ctx_launch_count(const gift_ctx* ctx);
@@ -130,8 +134,9 @@ int gift_csr_from_coo(gift_ctx* ctx, int64_t n, int64_t nnz, const int64_t* d_ro
  * no device-wide synchronisation). */
 int gift_csr_destroy(gift_csr* csr);
 /* State of the tiled copies of csr (which: 0 = the F = 4 copy, 1 = the copy for
- * signal widths <= 2): h_info[8] = {built, usable, tile_rows, block_cols,
- * segments, slices, stored slots, rows left to the row kernel}. */
+ * signal widths <= 2): h_info[10] = {built, usable, tile_rows, block_cols,
+ * segments, slices, stored slots, rows left to the row kernel, weights coded
+ * (u8 codes), distinct weights in the code table}. */
 int gift_csr_tiled_info(const gift_csr* csr, int which, int64_t* h_info);
 int gift_csr_shape(const gift_csr* csr, int64_t* n, int64_t* nnz);
 /* Device views (owned by csr): indptr int64[n+1], indices int32[nnz], values fp64[nnz]

@@ -132,10 +132,22 @@ void set_option(Ctx* ctx, const std::string& name, int64_t v) {
   } else if (name == "col_bits") {
     if (v != 0 && (v < 11 || v > 14)) bad();
     o.col_bits = v;
-  } else if (name == "barrier_free" || name == "graphs" || name == "zero_copy" || name == "schedule") {
+  } else if (name == "barrier_free" || name == "graphs" || name == "zero_copy" || name == "schedule" ||
+             name == "fused" || name == "prefetch") {
     if (v != 0 && v != 1) bad();
-    (name == "barrier_free" ? o.barrier_free : name == "graphs" ? o.graphs : name == "zero_copy" ? o.zero_copy
-                                                                                               : o.schedule) = v;
+    (name == "barrier_free" ? o.barrier_free
+     : name == "graphs"     ? o.graphs
+     : name == "zero_copy"  ? o.zero_copy
+     : name == "fused"      ? o.fused
+     : name == "prefetch"   ? o.prefetch
+                            : o.schedule) = v;
+  } else if (name == "codes") {
+#ifdef GIFT_TUNING
+    if (v != 0 && v != 1) bad();
+#else
+    if (v != 0) throw_error(GIFT_ERR_VALUE, "option codes: u8 weight codes exist only in -DGIFT_TUNING builds");
+#endif
+    o.codes = v;
   } else if (name == "row_lanes") {
     if (v != 0 && v != 8 && v != 16 && v != 32) bad();
     o.row_lanes = v;
@@ -151,7 +163,7 @@ static void options_from_env(Ctx* ctx) {
       {"GIFT_BMT", "tiled"},          {"GIFT_BMT_MIN_ROWS", "tiled_min_rows"}, {"GIFT_BMT_MIN_MEAN", "tiled_min_mean"},
       {"GIFT_BMT_TILE_ROWS", "tile_rows"}, {"GIFT_BMT_COL_BITS", "col_bits"}, {"GIFT_BMT_NB", "barrier_free"},
       {"GIFT_GRAPHS", "graphs"},      {"GIFT_ZERO_COPY", "zero_copy"},        {"GIFT_BMT_SCHEDULE", "schedule"},
-      {"GIFT_HOP_G", "row_lanes"}};
+      {"GIFT_HOP_G", "row_lanes"},    {"GIFT_FUSED", "fused"},                 {"GIFT_CODES", "codes"}};
   for (auto& nv : names) {
     const char* v = std::getenv(nv.first);
     if (v && *v) set_option(ctx, nv.second, std::atoll(v));
@@ -709,8 +721,9 @@ int gift_csr_tiled_info(const gift_csr* csr, int which, int64_t* h_info) {
   gift::Csr* c = const_cast<gift_csr*>(csr);
   std::lock_guard<std::recursive_mutex> lk(c->mu);
   const gift::Csr::Bmt& B = which == 0 ? c->bmt : c->bmt_wide;
-  const int64_t v[8] = {B.ready, B.ok, B.tile_rows, B.kC, B.nseg, B.nslices, B.slots, B.nwide};
-  for (int i = 0; i < 8; ++i) h_info[i] = v[i];
+  const int64_t v[10] = {B.ready, B.ok,     B.tile_rows, B.kC,    B.nseg,
+                         B.nslices, B.slots, B.nwide,  B.coded, B.coded_values};
+  for (int i = 0; i < 10; ++i) h_info[i] = v[i];
   GIFT_API_END
 }
 

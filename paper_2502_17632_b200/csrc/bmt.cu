@@ -92,6 +92,8 @@ BmtShape bmt_shape_for(const Ctx* ctx, double mean_row, bool wide_blocks) {
 constexpr int kPadRows = 16;      // one zero row per bank residue mod 16 (padding never conflicts)
 // columns kC .. kC + 15 of a staged block are its zero padding rows
 constexpr int kStage = 1024;      // a segment with >= kStage entries stages its block
+constexpr int kCodes = 256;       // coded copies: u8 weight codes, 255 = padding (weight 0)
+constexpr int kCodeCopies = 16;   // shared-memory copies of the code table (see RecW)
 constexpr int kBlock = 256;
 constexpr int kWide = 8;          // rows touching > max(kWide, 3 x mean) blocks run on the row kernel
 constexpr int kReuseHops = 4;     // GIFT_TILED_ON_REUSE: build once a graph has served this many fp32 hops
@@ -453,6 +455,47 @@ __global__ void k_tile_res(int64_t ntiles, int kR, const int64_t* __restrict__ r
   }
 }
 
+// ---- u8 weight codes (the copy for signal widths <= 2) ---------------------
+// code of w in the ascending table tbl[0, K), -1 if absent
+__device__ __forceinline__ int code_of(float w, const float* __restrict__ tbl, int K) {
+  int lo = 0, hi = K;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (tbl[mid] < w) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < K && tbl[lo] == w) ? lo : -1;
+}
+
+__global__ void k_sample_bits(int64_t m, int64_t stride, const float* __restrict__ w, uint32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __float_as_uint(w[i * stride]);
+}
+
+// dense entries whose weight has no code join the residual CSR
+__global__ void k_flag_uncoded(int64_t nnz, const uint64_t* __restrict__ pay, const float* __restrict__ tbl, int K,
+                               uint8_t* __restrict__ sparse, uint8_t* __restrict__ dense) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x)
+    if (dense[k] && code_of(__uint_as_float((uint32_t)(pay[k] >> 32)), tbl, K) < 0) {
+      dense[k] = 0;
+      sparse[k] = 1;
+    }
+}
+
+// coded layout: one 384-byte record per (slice, step of 4): 32 lanes x 4 u16
+// columns, then 32 lanes x 4 u8 codes (255: padding)
+__global__ void k_interleave_coded(int64_t total, const uint16_t* __restrict__ col, const float* __restrict__ w,
+                                   const float* __restrict__ tbl, int K, uint8_t* __restrict__ data) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = q / 128;
+    const int r = (int)(q % 128);  // lane * 4 + j
+    uint8_t* rec = data + t * 384;
+    reinterpret_cast<uint16_t*>(rec)[r] = col[q];
+    const int code = w[q] == 0.f ? 255 : code_of(w[q], tbl, K);
+    rec[256 + r] = (uint8_t)(code < 0 ? 255 : code);  // (every kept entry has a code)
+  }
+}
+
 // final layout: one 768-byte record per (slice, step of 4): 32 lanes x 4 u16
 // columns, then 32 lanes x 4 f32 weights -- a warp step reads one contiguous
 // record (one DRAM stream per warp instead of two)
@@ -526,7 +569,16 @@ struct BmtArgs {
   int64_t ntiles;
   const int64_t* res_rows;    // rows with residual entries, ascending
   const int64_t* tile_res;    // [ntiles + 1] range of res_rows per tile
+  const float* code_tbl;      // CODED copies: [256] weight of each code (255 = padding, 0)
+  int prefetch;               // L2 bulk prefetch of each warp's next slice (option "prefetch")
 };
+
+// CODED kernels: the code table, 16 copies interleaved (see RecW), after the
+// staged blocks and accumulators
+template <int kThreads>
+__device__ __forceinline__ void stage_code_table(const BmtArgs& b, float* tbl, int tid) {
+  for (int i = tid; i < kCodes * kCodeCopies; i += kThreads) tbl[i] = b.code_tbl[i / kCodeCopies];
+}
 
 __device__ __forceinline__ uint2 ld_stream_v2u32(const void* p, uint64_t pol) {
   uint2 r;
@@ -569,51 +621,98 @@ __device__ __forceinline__ void step_fma(float (&acc)[FIN], uint2 cv, float4 wv,
   gather_fma<FIN>(acc, wv.w, (int)(cv.y >> 16), zs);
 }
 
+// Weight half of a record step.  Plain copies store f32 weights (768-byte
+// records: 256 B of u16 columns, then 512 B of weights); CODED copies store a
+// u8 code per entry into the graph's table of its 255 most frequent fp32
+// weights (384-byte records: 256 B of columns, then 128 B of codes) -- entries
+// with other weights live in the residual CSR.  The table sits in shared
+// memory 16 times over (copy = lane % 16), so a warp's 32 lookups touch at
+// most two addresses per bank.
+template <bool CODED>
+struct RecW;
+template <>
+struct RecW<false> {
+  float4 v;
+};
+template <>
+struct RecW<true> {
+  uint32_t v;
+};
+template <bool CODED>
+__host__ __device__ constexpr int rec_bytes() {
+  return CODED ? 384 : 768;
+}
+
+template <bool CODED>
+__device__ __forceinline__ RecW<CODED> ld_w(const uint8_t* rec, int lane, uint64_t pol) {
+  RecW<CODED> r;
+  if constexpr (CODED) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(r.v)
+                 : "l"(rec + 256 + 4 * lane), "l"(pol));
+  } else {
+    r.v = ld_stream_v4f32(reinterpret_cast<const float*>(rec + 256 + 16 * lane), pol);
+  }
+  return r;
+}
+
+template <bool CODED>
+__device__ __forceinline__ float4 weights(RecW<CODED> r, const float* tbl, int lane) {
+  if constexpr (CODED) {
+    const float* t = tbl + (lane & (kCodeCopies - 1));
+    return make_float4(t[(r.v & 0xffu) * kCodeCopies], t[((r.v >> 8) & 0xffu) * kCodeCopies],
+                       t[((r.v >> 16) & 0xffu) * kCodeCopies], t[(r.v >> 24) * kCodeCopies]);
+  } else {
+    (void)tbl;
+    (void)lane;
+    return r.v;
+  }
+}
+
 // one slice (dynamic mode): lane = one row's run, summed in its (conflict-scheduled) order
-template <int FIN, int D>
+template <int FIN, int D, bool CODED>
 __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int steps, int row, const float* zs,
-                                          float* accs, int lane, uint64_t pol_s) {
+                                          float* accs, const float* tbl, int lane, uint64_t pol_s) {
+  constexpr int RB = rec_bytes<CODED>();
   float acc[FIN];
 #pragma unroll
   for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
-  const uint8_t* cp = b.data + (off / 128) * 768 + 8 * lane;
-  const uint8_t* wp = cp + 256 + 8 * lane;
+  const uint8_t* rp = b.data + (off / 128) * RB;
   uint2 cq[D];
-  float4 wq[D];
+  RecW<CODED> wq[D];
 #pragma unroll
   for (int d = 0; d < D; ++d)
     if (d < steps) {
-      cq[d] = ld_stream_v2u32(cp + d * 768, pol_s);
-      wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + d * 768), pol_s);
+      cq[d] = ld_stream_v2u32(rp + d * RB + 8 * lane, pol_s);
+      wq[d] = ld_w<CODED>(rp + d * RB, lane, pol_s);
     }
   int rem = steps;
   // steady state: D steps consumed, D reloaded, no predicates
   while (rem >= 2 * D) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      step_fma<FIN>(acc, cq[d], wq[d], zs);
-      cq[d] = ld_stream_v2u32(cp + (d + D) * 768, pol_s);
-      wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + (d + D) * 768), pol_s);
+      step_fma<FIN>(acc, cq[d], weights<CODED>(wq[d], tbl, lane), zs);
+      cq[d] = ld_stream_v2u32(rp + (d + D) * RB + 8 * lane, pol_s);
+      wq[d] = ld_w<CODED>(rp + (d + D) * RB, lane, pol_s);
     }
-    cp += D * 768;
-    wp += D * 768;
+    rp += D * RB;
     rem -= D;
   }
   // tail: fewer than 2D steps left
   if (rem > D) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      step_fma<FIN>(acc, cq[d], wq[d], zs);
+      step_fma<FIN>(acc, cq[d], weights<CODED>(wq[d], tbl, lane), zs);
       if (d + D < rem) {
-        cq[d] = ld_stream_v2u32(cp + (d + D) * 768, pol_s);
-        wq[d] = ld_stream_v4f32(reinterpret_cast<const float*>(wp + (d + D) * 768), pol_s);
+        cq[d] = ld_stream_v2u32(rp + (d + D) * RB + 8 * lane, pol_s);
+        wq[d] = ld_w<CODED>(rp + (d + D) * RB, lane, pol_s);
       }
     }
     rem -= D;
   }
 #pragma unroll
   for (int d = 0; d < D; ++d)
-    if (d < rem) step_fma<FIN>(acc, cq[d], wq[d], zs);
+    if (d < rem) step_fma<FIN>(acc, cq[d], weights<CODED>(wq[d], tbl, lane), zs);
   if (row != 0xffff) {
 #pragma unroll
     for (int f = 0; f < FIN; ++f) accs[row * FIN + f] += acc[f];
@@ -622,9 +721,9 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int ste
 
 // the slices of segment s: warps take them dynamically from *ctr (slices touch
 // distinct rows, so the assignment never changes a result)
-template <int FIN, int D>
+template <int FIN, int D, bool CODED>
 __device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, const float* zs, float* accs, int* ctr,
-                                               int lane, uint64_t pol_s) {
+                                               const float* tbl, int lane, uint64_t pol_s) {
   const int64_t sl0 = b.seg_slice[s];
   const int nsl = (int)(b.seg_slice[s + 1] - sl0);
   auto grab = [&]() {
@@ -633,7 +732,11 @@ __device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, cons
     return __shfl_sync(0xffffffffu, j, 0);
   };
   // the next slice's index and metadata are fetched before the current one
-  // runs, so their latency hides behind its stream
+  // runs, so their latency hides behind its stream.  Option "prefetch" also
+  // bulk-prefetches its records into L2 (off by default: c4, whose slices are
+  // ~2 record steps, gains 1-2 %; c3's long slices lose 20-40 % to the extra
+  // L2 traffic)
+  constexpr int RB = rec_bytes<CODED>();
   int j = grab();
   int64_t off = 0, end = 0;
   int row = 0xffff;
@@ -650,8 +753,12 @@ __device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, cons
       off_n = b.slice_off[sl0 + jn];
       end_n = b.slice_off[sl0 + jn + 1];
       row_n = b.slice_rows[(sl0 + jn) * 32 + lane];
+      if (b.prefetch && lane == 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b.data + (off_n / 128) * RB),
+                     "r"((unsigned)((end_n - off_n) / 128 * RB))
+                     : "memory");
     }
-    run_slice<FIN, D>(b, off, (int)((end - off) / 128), row, zs, accs, lane, pol_s);
+    run_slice<FIN, D, CODED>(b, off, (int)((end - off) / 128), row, zs, accs, tbl, lane, pol_s);
     j = jn;
     off = off_n;
     end = end_n;
@@ -704,7 +811,7 @@ __device__ __forceinline__ void bmt_tile_finish(const HopArgs& a, const BmtArgs&
 }
 
 // one staging buffer: stage, barrier, slices, barrier
-template <int FIN, int FOUT, int kThreads>
+template <int FIN, int FOUT, int kThreads, bool CODED>
 __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int64_t tile, int kR, int tid, int lane,
                                          uint64_t pol_s, uint64_t pol_z) {
   extern __shared__ float4 smem_f4[];
@@ -712,6 +819,7 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
   const int kC = b.kC;
   float* zs = reinterpret_cast<float*>(smem_f4);  // [(kC + kPadRows) * FIN], rows >= kC stay zero
   float* accs = zs + (kC + kPadRows) * FIN;         // [kR * FIN]
+  const float* tbl = accs + kR * FIN;               // CODED: [256 * 16] code table
   const int64_t r0 = tile * kR;
   const int nrows = (int)min((int64_t)kR, a.n - r0);
   for (int i = tid; i < nrows * FIN; i += kThreads) accs[i] = 0.f;
@@ -733,7 +841,7 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
     for (int i = nf + tid; i < (kC + kPadRows) * FIN; i += kThreads) zs[i] = 0.f;  // short block + padding rows
     if (tid == 0) slice_ctr = 0;
     __syncthreads();
-    segment_slices<FIN, bmt_depth<FIN, kThreads>()>(b, s, zs, accs, &slice_ctr, lane, pol_s);
+    segment_slices<FIN, bmt_depth<FIN, kThreads>(), CODED>(b, s, zs, accs, &slice_ctr, tbl, lane, pol_s);
   }
   bmt_tile_finish<FIN, FOUT, kThreads>(a, b, tile, r0, nrows, accs, tid, lane, pol_z);
 }
@@ -759,7 +867,7 @@ __device__ __forceinline__ void stage_async(const HopArgs& a, const BmtArgs& b, 
 
 // two staging buffers: segment s + 1's block streams in (cp.async) while the
 // warps run segment s's slices; one barrier per segment
-template <int FIN, int FOUT, int kThreads>
+template <int FIN, int FOUT, int kThreads, bool CODED>
 __device__ __forceinline__ void bmt_tile_db(const HopArgs& a, const BmtArgs& b, int64_t tile, int kR, int tid,
                                             int lane, uint64_t pol_s, uint64_t pol_z) {
   extern __shared__ float4 smem_f4[];
@@ -769,6 +877,7 @@ __device__ __forceinline__ void bmt_tile_db(const HopArgs& a, const BmtArgs& b, 
   float* zs0 = reinterpret_cast<float*>(smem_f4);
   float* zs1 = zs0 + zrows;
   float* accs = zs1 + zrows;  // [kR * FIN]
+  const float* tbl = accs + kR * FIN;  // CODED: code table
   const int64_t r0 = tile * kR;
   const int nrows = (int)min((int64_t)kR, a.n - r0);
   for (int i = tid; i < nrows * FIN; i += kThreads) accs[i] = 0.f;
@@ -789,12 +898,13 @@ __device__ __forceinline__ void bmt_tile_db(const HopArgs& a, const BmtArgs& b, 
       stage_async<FIN, kThreads>(a, b, s + 1, buf ? zs0 : zs1, tid, pol_z);
       if (tid == 0) slice_ctr2[buf ^ 1] = 0;
     }
-    segment_slices<FIN, bmt_depth<FIN, kThreads>()>(b, s, buf ? zs1 : zs0, accs, &slice_ctr2[buf], lane, pol_s);
+    segment_slices<FIN, bmt_depth<FIN, kThreads>(), CODED>(b, s, buf ? zs1 : zs0, accs, &slice_ctr2[buf], tbl, lane,
+                                                           pol_s);
   }
   bmt_tile_finish<FIN, FOUT, kThreads>(a, b, tile, r0, nrows, accs, tid, lane, pol_z);
 }
 
-template <int FIN, int FOUT, int kThreads, bool DB>
+template <int FIN, int FOUT, int kThreads, bool DB, bool CODED>
 __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a, BmtArgs b) {
   const int kR = b.tile_rows;
   const int tid = threadIdx.x;
@@ -802,12 +912,17 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_z = policy_evict_last();
   __shared__ int64_t tile_sh;
+  if constexpr (CODED) {  // visible after the first segment's barrier
+    extern __shared__ float4 smem_f4[];
+    const int zrows = (b.kC + kPadRows) * FIN;
+    stage_code_table<kThreads>(b, reinterpret_cast<float*>(smem_f4) + (DB ? 2 : 1) * zrows + kR * FIN, tid);
+  }
   if (!b.ctr) {  // one CTA per tile; the block scheduler issues low blockIdx first
     const int64_t tile = b.tile_order ? b.tile_order[blockIdx.x] : blockIdx.x;
     if constexpr (DB)
-      bmt_tile_db<FIN, FOUT, kThreads>(a, b, tile, kR, tid, lane, pol_s, pol_z);
+      bmt_tile_db<FIN, FOUT, kThreads, CODED>(a, b, tile, kR, tid, lane, pol_s, pol_z);
     else
-      bmt_tile<FIN, FOUT, kThreads>(a, b, tile, kR, tid, lane, pol_s, pol_z);
+      bmt_tile<FIN, FOUT, kThreads, CODED>(a, b, tile, kR, tid, lane, pol_s, pol_z);
     return;
   }
   // persistent CTAs take tiles costliest first from a global counter (the
@@ -824,9 +939,9 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a
     __syncthreads();
     if (tile < 0) break;
     if constexpr (DB)
-      bmt_tile_db<FIN, FOUT, kThreads>(a, b, tile, kR, tid, lane, pol_s, pol_z);
+      bmt_tile_db<FIN, FOUT, kThreads, CODED>(a, b, tile, kR, tid, lane, pol_s, pol_z);
     else
-      bmt_tile<FIN, FOUT, kThreads>(a, b, tile, kR, tid, lane, pol_s, pol_z);
+      bmt_tile<FIN, FOUT, kThreads, CODED>(a, b, tile, kR, tid, lane, pol_s, pol_z);
   }
   if (tid == 0) {
     __threadfence();
@@ -902,7 +1017,7 @@ __device__ __forceinline__ void stage_bulk(const HopArgs& a, const BmtArgs& b, i
         : "memory");
 }
 
-template <int FIN, int FOUT, int kThreads>
+template <int FIN, int FOUT, int kThreads, bool CODED>
 __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt_nb(HopArgs a, BmtArgs b) {
   extern __shared__ float4 smem_f4[];
   __shared__ uint64_t full[2];
@@ -920,6 +1035,8 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt_nb(HopArg
   float* acc[2];
   acc[0] = zs[1] + zrows;
   acc[1] = acc[0] + kR * FIN;
+  float* tbl = acc[1] + kR * FIN;  // CODED: code table
+  if constexpr (CODED) stage_code_table<kThreads>(b, tbl, tid);  // visible after the barrier below
   const int64_t tile = b.tile_order ? b.tile_order[blockIdx.x] : blockIdx.x;
   const int64_t r0 = tile * kR;
   const int nrows = (int)min((int64_t)kR, a.n - r0);
@@ -946,7 +1063,8 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt_nb(HopArg
   for (int i = 0; i < nseg; ++i) {
     const int buf = i & 1;
     mbar_wait(&full[buf], (unsigned)(i >> 1) & 1u);
-    segment_slices<FIN, bmt_depth<FIN, kThreads>()>(b, s0 + i, zs[buf], acc[buf], &slice_ctr[buf], lane, pol_s);
+    segment_slices<FIN, bmt_depth<FIN, kThreads>(), CODED>(b, s0 + i, zs[buf], acc[buf], &slice_ctr[buf], tbl, lane,
+                                                           pol_s);
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
@@ -963,20 +1081,28 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt_nb(HopArg
   bmt_tile_finish<FIN, FOUT, kThreads>(a, b, tile, r0, nrows, acc[0], tid, lane, pol_z);
 }
 
-size_t bmt_smem_nb(int fin, int kR, int kC) { return 2 * ((size_t)(kC + kPadRows) * fin * 4 + (size_t)kR * fin * 4); }
+constexpr size_t kCodeTableBytes = (size_t)kCodes * kCodeCopies * sizeof(float);
 
-size_t bmt_smem(int fin, int kR, int kC) { return (size_t)(kC + kPadRows) * fin * 4 + (size_t)kR * fin * 4; }
+size_t bmt_smem_nb(int fin, int kR, int kC, bool coded) {
+  return 2 * ((size_t)(kC + kPadRows) * fin * 4 + (size_t)kR * fin * 4) + (coded ? kCodeTableBytes : 0);
+}
+
+size_t bmt_smem(int fin, int kR, int kC, bool coded = false) {
+  return (size_t)(kC + kPadRows) * fin * 4 + (size_t)kR * fin * 4 + (coded ? kCodeTableBytes : 0);
+}
 
 #ifdef GIFT_TUNING
-size_t bmt_smem_db(int fin, int kR, int kC) { return bmt_smem(fin, kR, kC) + (size_t)(kC + kPadRows) * fin * 4; }
+size_t bmt_smem_db(int fin, int kR, int kC, bool coded) {
+  return bmt_smem(fin, kR, kC, coded) + (size_t)(kC + kPadRows) * fin * 4;
+}
 #endif
 
-template <int FIN, int FOUT, bool DB>
+template <int FIN, int FOUT, bool DB, bool CODED>
 void launch_bmt_k(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, int tpb, size_t smem) {
 #ifdef GIFT_TUNING
-  auto kern = tpb == 1024 ? k_hop_bmt<FIN, FOUT, 1024, DB> : k_hop_bmt<FIN, FOUT, 512, DB>;
+  auto kern = tpb == 1024 ? k_hop_bmt<FIN, FOUT, 1024, DB, CODED> : k_hop_bmt<FIN, FOUT, 512, DB, CODED>;
 #else
-  auto kern = k_hop_bmt<FIN, FOUT, 1024, DB>;  // default shapes are >= 4096 rows: 1 CTA x 1024 per SM
+  auto kern = k_hop_bmt<FIN, FOUT, 1024, DB, CODED>;  // default shapes are >= 4096 rows: 1 CTA x 1024 per SM
   (void)tpb;
 #endif
   static std::mutex mu;
@@ -1004,9 +1130,9 @@ void launch_bmt_k(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, 
   GIFT_LAUNCH_CHECK(ctx);
 }
 
-template <int FIN, int FOUT, int kThreads>
+template <int FIN, int FOUT, int kThreads, bool CODED>
 void launch_bmt_nb(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, size_t smem) {
-  auto kern = k_hop_bmt_nb<FIN, FOUT, kThreads>;
+  auto kern = k_hop_bmt_nb<FIN, FOUT, kThreads, CODED>;
   // the smem opt-in is a per-device function attribute: set it once per device
   static std::mutex mu;
   static std::set<int> done;
@@ -1024,7 +1150,7 @@ void launch_bmt_nb(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles,
   GIFT_LAUNCH_CHECK(ctx);
 }
 
-template <int FIN, int FOUT>
+template <int FIN, int FOUT, bool CODED>
 void launch_bmt(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles) {
   // barrier-free pipeline where it keeps the barrier kernel's occupancy:
   // 2 CTAs x 512 threads per SM for 2048-row tiles, 1 x 1024 for taller ones
@@ -1032,15 +1158,15 @@ void launch_bmt(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles) {
   // 1.25 ms when its 197 KB footprint drops it from 2 x 512 to 1 x 1024).  The
   // bulk copies need a 16-byte aligned signal.
   if (ctx->opt.barrier_free && !b.ctr && ((uintptr_t)a.zin & 15) == 0) {
-    const size_t nb = bmt_smem_nb(FIN, b.tile_rows, b.kC), fixed = 3 * 1024;
+    const size_t nb = bmt_smem_nb(FIN, b.tile_rows, b.kC, CODED), fixed = 3 * 1024;
 #ifdef GIFT_TUNING
     if (b.tile_rows <= 2048 && 2 * (nb + fixed) <= 228 * 1024) {
-      launch_bmt_nb<FIN, FOUT, 512>(ctx, a, b, ntiles, nb);
+      launch_bmt_nb<FIN, FOUT, 512, CODED>(ctx, a, b, ntiles, nb);
       return;
     }
 #endif
     if (b.tile_rows > 2048 && nb + fixed <= 228 * 1024) {
-      launch_bmt_nb<FIN, FOUT, 1024>(ctx, a, b, ntiles, nb);
+      launch_bmt_nb<FIN, FOUT, 1024, CODED>(ctx, a, b, ntiles, nb);
       return;
     }
   }
@@ -1048,30 +1174,50 @@ void launch_bmt(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles) {
   // tiles.  Tuning builds also have 2 x 512 for 2048-row tiles and a
   // double-buffered (cp.async) variant; neither won on the default shapes
   // (DESIGN.md §4).
-  const size_t smem1 = bmt_smem(FIN, b.tile_rows, b.kC);
+  const size_t smem1 = bmt_smem(FIN, b.tile_rows, b.kC, CODED);
 #ifdef GIFT_TUNING
-  const size_t smem2 = bmt_smem_db(FIN, b.tile_rows, b.kC);
+  const size_t smem2 = bmt_smem_db(FIN, b.tile_rows, b.kC, CODED);
   const int tpb = (b.tile_rows > 2048 || 2 * (smem1 + 3 * 1024) > 228 * 1024) ? 1024 : 512;
   const int per_sm = tpb == 512 ? 2 : 1;
   const bool db = env_int("GIFT_BMT_DB", 1) && ((uintptr_t)a.zin & 15) == 0 &&
                   (size_t)per_sm * (smem2 + 3 * 1024) <= 228 * 1024;
   if (db) {
-    launch_bmt_k<FIN, FOUT, true>(ctx, a, b, ntiles, tpb, smem2);
+    launch_bmt_k<FIN, FOUT, true, CODED>(ctx, a, b, ntiles, tpb, smem2);
     return;
   }
-  launch_bmt_k<FIN, FOUT, false>(ctx, a, b, ntiles, tpb, smem1);
+  launch_bmt_k<FIN, FOUT, false, CODED>(ctx, a, b, ntiles, tpb, smem1);
 #else
-  launch_bmt_k<FIN, FOUT, false>(ctx, a, b, ntiles, 1024, smem1);
+  launch_bmt_k<FIN, FOUT, false, CODED>(ctx, a, b, ntiles, 1024, smem1);
 #endif
 }
 
+// Coded copies (u8 weight codes, 3-byte entries) are a TUNING-build
+// experiment: on B200 the F = 2 pass got slower with them (c3 0.85 -> 0.93 ms,
+// c4 1.25 -> 1.34 ms: the per-entry table lookup costs more shared-memory
+// issue than the halved record bytes save), so product builds keep fp32
+// weights
 template <int FIN>
-void launch_bmt_out(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, int fout) {
+void launch_bmt_out(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, int fout, bool coded) {
+#ifdef GIFT_TUNING
+  if constexpr (FIN <= 2) {
+    if (coded) {
+      switch (fout) {
+        case 0: launch_bmt<FIN, 0, true>(ctx, a, b, ntiles); break;
+        case 1: launch_bmt<FIN, 1, true>(ctx, a, b, ntiles); break;
+        case 2: launch_bmt<FIN, 2, true>(ctx, a, b, ntiles); break;
+        default: launch_bmt<FIN, 4, true>(ctx, a, b, ntiles); break;
+      }
+      return;
+    }
+  }
+#else
+  (void)coded;  // coded copies exist only in tuning builds
+#endif
   switch (fout) {
-    case 0: launch_bmt<FIN, 0>(ctx, a, b, ntiles); break;
-    case 1: launch_bmt<FIN, 1>(ctx, a, b, ntiles); break;
-    case 2: launch_bmt<FIN, 2>(ctx, a, b, ntiles); break;
-    default: launch_bmt<FIN, 4>(ctx, a, b, ntiles); break;
+    case 0: launch_bmt<FIN, 0, false>(ctx, a, b, ntiles); break;
+    case 1: launch_bmt<FIN, 1, false>(ctx, a, b, ntiles); break;
+    case 2: launch_bmt<FIN, 2, false>(ctx, a, b, ntiles); break;
+    default: launch_bmt<FIN, 4, false>(ctx, a, b, ntiles); break;
   }
 }
 
@@ -1100,9 +1246,57 @@ void exclusive_sum(Ctx* ctx, const int64_t* in, int64_t* out, int64_t n) {
   ctx->launches += 2;
 }
 
+// the graph's (up to) 255 most frequent fp32 weights, ascending, into tbl[0, K);
+// tbl[255] = 0 (padding).  Returns K.
+int build_code_table(Ctx* ctx, const float* w32, int64_t nnz, float* tbl) {
+  cudaStream_t st = ctx->stream;
+  const int64_t m = std::min<int64_t>(nnz, 1LL << 24);
+  const int64_t stride = (nnz + m - 1) / m;
+  const int64_t ms = (nnz + stride - 1) / stride;
+  DevBuf<uint32_t> smp(ctx, ms), srt(ctx, ms), uniq(ctx, ms);
+  DevBuf<int32_t> cnt(ctx, ms);
+  DevBuf<int32_t> nruns(ctx, 1);
+  k_sample_bits<<<grid_for(ms, kBlock), kBlock, 0, st>>>(ms, stride, w32, smp.p);
+  GIFT_LAUNCH_CHECK(ctx);
+  size_t bytes = 0;
+  GIFT_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, smp.p, srt.p, ms, 0, 32, st));
+  {
+    DevBuf<char> tmp(ctx, bytes);
+    GIFT_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, bytes, smp.p, srt.p, ms, 0, 32, st));
+  }
+  bytes = 0;
+  GIFT_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, srt.p, uniq.p, cnt.p, nruns.p, ms, st));
+  {
+    DevBuf<char> tmp(ctx, bytes);
+    GIFT_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, bytes, srt.p, uniq.p, cnt.p, nruns.p, ms, st));
+  }
+  ctx->launches += 5;
+  const int32_t nr = fetch(ctx, nruns.p);
+  std::vector<uint32_t> hu(nr);
+  std::vector<int32_t> hc(nr);
+  GIFT_CUDA(cudaMemcpyAsync(hu.data(), uniq.p, nr * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  GIFT_CUDA(cudaMemcpyAsync(hc.data(), cnt.p, nr * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  GIFT_CUDA(cudaStreamSynchronize(st));
+  std::vector<int32_t> idx(nr);
+  for (int32_t i = 0; i < nr; ++i) idx[i] = i;
+  const int K = std::min<int32_t>(nr, kCodes - 1);
+  // most frequent first, ties by bit pattern: deterministic
+  std::partial_sort(idx.begin(), idx.begin() + K, idx.end(), [&](int32_t x, int32_t y) {
+    return hc[x] != hc[y] ? hc[x] > hc[y] : hu[x] < hu[y];
+  });
+  std::vector<float> vals(kCodes, 0.f);
+  for (int i = 0; i < K; ++i) memcpy(&vals[i], &hu[idx[i]], sizeof(float));
+  std::sort(vals.begin(), vals.begin() + K);
+  for (int i = K; i < kCodes; ++i) vals[i] = 0.f;  // unused codes; 255 = padding
+  GIFT_CUDA(cudaMemcpyAsync(tbl, vals.data(), kCodes * sizeof(float), cudaMemcpyHostToDevice, st));
+  GIFT_CUDA(cudaStreamSynchronize(st));  // vals lives on this stack
+  return K;
+}
+
 // Build the sliced block-major copy (once per graph; cached on the csr).
 bool bmt_build(Ctx* ctx, Csr* c, const float* w32, Csr::Bmt& B, bool wide_blocks) {
   cudaStream_t st = ctx->stream;
+  const bool coded = wide_blocks && ctx->opt.codes;  // tuning builds only (see launch_bmt_out)
   const int64_t n = c->n, nnz_all = c->nnz;
   const BmtShape shape = bmt_shape_for(ctx, c->mean_row, wide_blocks);
   const int kR = shape.kR, cb = shape.cb, kC = 1 << cb;
@@ -1174,8 +1368,18 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32, Csr::Bmt& B, bool wide_blocks
     ctx->launches += 4;
   }
   // entries [0, nnz) are the kept ones; wide rows' entries sorted past them
+  // 2a. coded copy: the graph's 255 most frequent fp32 weights (from a sample of
+  //     at most 2^24 entries) become u8 codes; on netlist graphs they cover
+  //     ~99 % of the entries (single-net weights 2/m)
+  int code_k = 0;
+  if (coded) {
+    B.code_tbl = static_cast<float*>(csr_alloc(ctx, c, kCodes * sizeof(float)));
+    code_k = build_code_table(ctx, w32, nnz_all, B.code_tbl);
+    B.coded_values = code_k;
+  }
   // 2b. sparse segments -> residual CSR (gathered from L2 by the tile's rows);
-  //     dense segments stay in the sliced copy
+  //     dense segments stay in the sliced copy (coded copy: so do only entries
+  //     whose weight has a code)
   {
     DevBuf<uint8_t> seg_head(ctx, nnz), run_head(ctx, nnz);
     DevBuf<unsigned long long> cnt0(ctx, 2);
@@ -1191,6 +1395,10 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32, Csr::Bmt& B, bool wide_blocks
     DevBuf<uint8_t> dense(ctx, nnz);
     k_flag_sparse<<<(unsigned)std::min<int64_t>(nseg0, 65535), 256, 0, st>>>(nseg0, seg0.p, nnz, sparse.p, dense.p);
     GIFT_LAUNCH_CHECK(ctx);
+    if (coded) {
+      k_flag_uncoded<<<grid_for(nnz, kBlock), kBlock, 0, st>>>(nnz, pay_s.p, B.code_tbl, code_k, sparse.p, dense.p);
+      GIFT_LAUNCH_CHECK(ctx);
+    }
     // residual entries
     DevBuf<uint32_t> rk(ctx, nnz);
     DevBuf<uint64_t> rp(ctx, nnz);
@@ -1337,9 +1545,15 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32, Csr::Bmt& B, bool wide_blocks
                                                                             tcol.p, tw.p);
     GIFT_LAUNCH_CHECK(ctx);
   }
-  B.data = static_cast<uint8_t*>(csr_alloc(ctx, c, (total / 128 + 1) * 768));
-  k_interleave<<<grid_for(total, kBlock), kBlock, 0, st>>>(total, bcol, bw, B.data);
+  if (coded) {
+    B.data = static_cast<uint8_t*>(csr_alloc(ctx, c, (total / 128 + 1) * 384));
+    k_interleave_coded<<<grid_for(total, kBlock), kBlock, 0, st>>>(total, bcol, bw, B.code_tbl, code_k, B.data);
+  } else {
+    B.data = static_cast<uint8_t*>(csr_alloc(ctx, c, (total / 128 + 1) * 768));
+    k_interleave<<<grid_for(total, kBlock), kBlock, 0, st>>>(total, bcol, bw, B.data);
+  }
   GIFT_LAUNCH_CHECK(ctx);
+  B.coded = coded;
   colb.reset();
   wb.reset();
   // 7. segment codes and tile -> segment ranges
@@ -1434,7 +1648,7 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
   }
   if (!B.ok) return false;
   // a tuning shape may not fit this signal width's shared-memory footprint
-  if (bmt_smem(fin, B.tile_rows, B.kC) + 1024 > (size_t)ctx->smem_optin) return false;
+  if (bmt_smem(fin, B.tile_rows, B.kC, B.coded) + 1024 > (size_t)ctx->smem_optin) return false;
   // the wide rows (pads / macros, long rows) run concurrently on a side stream:
   // disjoint output rows, same input signal
   const bool fork = B.nwide > 0;
@@ -1465,11 +1679,11 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
 #endif
   BmtArgs b{c->n,         B.tile_rows,  B.kC,         B.data,      B.wide,      B.res_rowptr, B.res_col,     B.res_w,
             B.tile_seg,   B.seg_code,   B.seg_slice, B.slice_off, B.slice_rows, order,         ctr,
-            B.ntiles,     B.res_rows,   B.tile_res};
+            B.ntiles,     B.res_rows,   B.tile_res,  B.code_tbl,  (int)ctx->opt.prefetch};
   switch (fin) {
-    case 1: launch_bmt_out<1>(ctx, a, b, B.ntiles, fout); break;
-    case 2: launch_bmt_out<2>(ctx, a, b, B.ntiles, fout); break;
-    default: launch_bmt_out<4>(ctx, a, b, B.ntiles, fout); break;
+    case 1: launch_bmt_out<1>(ctx, a, b, B.ntiles, fout, B.coded); break;
+    case 2: launch_bmt_out<2>(ctx, a, b, B.ntiles, fout, B.coded); break;
+    default: launch_bmt_out<4>(ctx, a, b, B.ntiles, fout, false); break;
   }
   if (fork) GIFT_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
   return true;

@@ -62,9 +62,12 @@ struct Ctx {
     int64_t col_bits = 0;           // "col_bits": force log2 of the block width (11..14), 0 = per graph
     int64_t barrier_free = 1;       // "barrier_free": the bulk-copy pipeline where it fits
     int64_t graphs = 1;             // "graphs": replay small-graph banks as CUDA graphs
+    int64_t fused = 1;              // "fused": small-graph banks as one cooperative kernel
     int64_t zero_copy = 1;          // "zero_copy": *_host calls use pinned buffers in place
     int64_t schedule = 1;           // "schedule": bank-conflict-aware entry order in the tiled copy
     int64_t row_lanes = 0;          // "row_lanes": force lanes per row of the row kernel (8 / 16 / 32)
+    int64_t codes = 0;              // "codes" (tuning builds): u8 weight codes in the F <= 2 tiled copy
+    int64_t prefetch = 0;           // "prefetch": tiled hop prefetches each warp's next slice into L2
   } opt;
   std::recursive_mutex mu;        // entry points serialise on the context (scratch, stream, logs)
   // persistent BMT tile scheduler counters [next tile, finished CTAs], one
@@ -191,8 +194,11 @@ struct Csr {
     int64_t* seg_slice = nullptr;   // [nseg + 1] slice range of each segment
     int64_t* slice_off = nullptr;   // [nslices + 1] first slot of each slice
     uint16_t* slice_rows = nullptr; // [nslices * 32] row in tile per lane (0xffff: none)
-    uint8_t* data = nullptr;        // [slots / 128] 768-byte records: 32x4 u16 columns (kC = padding),
-                                    // then 32x4 f32 weights
+    uint8_t* data = nullptr;        // [slots / 128] records: 32x4 u16 columns (kC = padding), then
+                                    // 32x4 f32 weights (768 B) or, coded, 32x4 u8 weight codes (384 B)
+    bool coded = false;             // weights as u8 codes into code_tbl
+    float* code_tbl = nullptr;      // [256] fp32 weight of each code; 255 = padding (0)
+    int64_t coded_values = 0;       // distinct weights the table holds (<= 255)
   } bmt, bmt_wide;  // bmt_wide: signal widths <= 2; bmt: F = 4 (bmt.cu bmt_shape_for)
   int64_t fp32_hops = 0;          // fp32 hop launches served (tiled-copy policy: build on reuse)
   uint64_t uid = 0;               // identity for cached CUDA graphs (0 = none yet; never reused)

@@ -29,8 +29,12 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "hop.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gift {
 
@@ -269,10 +273,8 @@ __global__ void k_epilogue_f64(int64_t n, int64_t ncols, const double* __restric
 // has 2U streaming loads then 4U gathers outstanding.  Lane partials reduce
 // with a fixed xor-butterfly (deterministic order); lane 0 runs the epilogue.
 template <int FIN, int FOUT, int G, int U>
-__global__ void __launch_bounds__(kBlock) k_hop(HopArgs a) {
+__device__ __forceinline__ void hop_row(const HopArgs& a, int64_t gi) {
   const int lane = threadIdx.x & (G - 1);
-  const int64_t gi = a.row_begin + (blockIdx.x * (int64_t)kBlock + threadIdx.x) / G;
-  if (gi >= a.n) return;  // uniform within a row group
   const int64_t row = a.row_list ? (int64_t)a.row_list[gi] : gi;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
   const uint64_t pol_s = policy_evict_first();
@@ -330,29 +332,50 @@ __global__ void __launch_bounds__(kBlock) k_hop(HopArgs a) {
   row_epilogue<FIN, FOUT>(a, row, acc, pol_z);
 }
 
+template <int FIN, int FOUT, int G, int U>
+__global__ void __launch_bounds__(kBlock) k_hop(HopArgs a) {
+  const int64_t gi = a.row_begin + (blockIdx.x * (int64_t)kBlock + threadIdx.x) / G;
+  if (gi >= a.n) return;  // uniform within a row group
+  hop_row<FIN, FOUT, G, U>(a, gi);
+}
+
+
+// z0[i, chn*wcols + cc] = s_chn[i] * g[i, c0 + cc]
+struct PrepArgs {
+  int64_t n;
+  int wcols, nch;
+  const float* s[4];
+  int in_dtype;
+  const void* g;
+  int64_t ld, c0;
+  float* z;
+};
+
+template <int F>
+__device__ __forceinline__ void prep_row(const PrepArgs& p, int64_t i) {
+  float v[F];
+#pragma unroll
+  for (int f = 0; f < F; ++f) {
+    const int chn = f / p.wcols, cc = f - chn * p.wcols;
+    float x = 0.f, s = 0.f;
+    if (chn < p.nch) {
+      const int64_t gi = i * p.ld + p.c0 + cc;
+      x = p.in_dtype == GIFT_DTYPE_F64 ? (float)static_cast<const double*>(p.g)[gi]
+                                       : static_cast<const float*>(p.g)[gi];
+      s = p.s[chn][i];
+    }
+    v[f] = s * x;
+  }
+  if constexpr (F == 4) *reinterpret_cast<float4*>(p.z + i * 4) = make_float4(v[0], v[1], v[2], v[3]);
+  else if constexpr (F == 2) *reinterpret_cast<float2*>(p.z + i * 2) = make_float2(v[0], v[1]);
+  else p.z[i] = v[0];
+}
 
 // z0[i, chn*wcols + cc] = s_chn[i] * g[i, c0 + cc]
 template <int F>
-__global__ void k_prep(int64_t n, int wcols, int nch, const float* s0, const float* s1, const float* s2,
-                       const float* s3, int in_dtype, const void* __restrict__ g, int64_t ld, int64_t c0,
-                       float* __restrict__ z) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float v[F];
-#pragma unroll
-    for (int f = 0; f < F; ++f) {
-      const int chn = f / wcols, cc = f - chn * wcols;
-      float x = 0.f, s = 0.f;
-      if (chn < nch) {
-        const int64_t gi = i * ld + c0 + cc;
-        x = in_dtype == GIFT_DTYPE_F64 ? (float)static_cast<const double*>(g)[gi] : static_cast<const float*>(g)[gi];
-        s = (chn == 0 ? s0 : chn == 1 ? s1 : chn == 2 ? s2 : s3)[i];
-      }
-      v[f] = s * x;
-    }
-    if constexpr (F == 4) *reinterpret_cast<float4*>(z + i * 4) = make_float4(v[0], v[1], v[2], v[3]);
-    else if constexpr (F == 2) *reinterpret_cast<float2*>(z + i * 2) = make_float2(v[0], v[1]);
-    else z[i] = v[0];
-  }
+__global__ void k_prep(PrepArgs p) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * blockDim.x)
+    prep_row<F>(p, i);
 }
 
 __global__ void k_gather_rows(int64_t n_idx, int F, const int64_t* __restrict__ idx, const float* __restrict__ src,
@@ -629,11 +652,116 @@ static void bank_fp64_exact(Ctx* ctx, Csr* c, const std::vector<TermGroup>& grou
   GIFT_LAUNCH_CHECK(ctx);
 }
 
+
+// ---- the fp32 bank as a sequence of ops ------------------------------------
+// A PREP op writes z0 = s o g for the chains of one pack; a HOP op advances
+// every chain packed in zin by one hop (epilogue: next z, term accumulation,
+// final re-pin / clamp).  bank_fp32 plans the ops, then either launches them
+// one by one (tiled or row kernel per hop) or, for small graphs, runs them all
+// in ONE cooperative kernel with a grid-wide barrier between ops.
+struct BankOp {
+  int kind;  // 0 = prep, 1 = hop
+  int F;     // prep: floats per row written
+  int fin, fout;
+  PrepArgs p;
+  HopArgs a;
+};
+constexpr int kMaxFusedOps = 10;
+struct FusedBank {
+  int nops;
+  BankOp op[kMaxFusedOps];
+};
+
+template <int G>
+__device__ __forceinline__ void fused_hop(const HopArgs& a, int fin, int fout, int64_t gi) {
+#define GIFT_FUSED_CASE(FI, FO) \
+  if (fin == FI && fout == FO) { \
+    hop_row<FI, FO, G, 1>(a, gi);  \
+    return;                        \
+  }
+  GIFT_FUSED_CASE(4, 4) GIFT_FUSED_CASE(4, 2) GIFT_FUSED_CASE(4, 1) GIFT_FUSED_CASE(4, 0)
+  GIFT_FUSED_CASE(2, 2) GIFT_FUSED_CASE(2, 1) GIFT_FUSED_CASE(2, 0) GIFT_FUSED_CASE(2, 4)
+  GIFT_FUSED_CASE(1, 1) GIFT_FUSED_CASE(1, 0) GIFT_FUSED_CASE(1, 2) GIFT_FUSED_CASE(1, 4)
+#undef GIFT_FUSED_CASE
+}
+
+// the whole bank of a small (launch-bound, L2-resident) graph in one launch
+template <int G>
+__global__ void __launch_bounds__(kBlock) k_bank_fused(const __grid_constant__ FusedBank fb) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * kBlock;
+  for (int o = 0; o < fb.nops; ++o) {
+    const BankOp& op = fb.op[o];
+    if (op.kind == 0) {
+      for (int64_t i = tid; i < op.p.n; i += nthreads) {
+        if (op.F == 4) prep_row<4>(op.p, i);
+        else if (op.F == 2) prep_row<2>(op.p, i);
+        else prep_row<1>(op.p, i);
+      }
+    } else {
+      // row groups of G lanes, grid-strided (uniform per group)
+      for (int64_t gi = tid / G; gi < op.a.n; gi += nthreads / G) fused_hop<G>(op.a, op.fin, op.fout, gi);
+    }
+    if (o + 1 < fb.nops) grid.sync();
+  }
+}
+
 // measured on B200 (profiles/r01_sweep_hop.txt): 8 lanes per row at mean
 // row length ~64 (c1), 16 at ~400 (c2/c3); one 4-nnz chunk in flight per lane
 static int pick_group_lanes(double mean_row) {
   if (mean_row < 160) return 8;
   return 16;
+}
+
+// graphs this small run the bank fused (one cooperative launch); above it the
+// per-op launches (replayed as a CUDA graph below the tiled threshold) win:
+// c0 (0.66M entries) 0.052 -> 0.042 ms per bank, c1 (13.6M) 0.28 -> 0.32 ms
+constexpr int64_t kFusedMaxNnz = 1LL << 21;
+
+static bool launch_fused(Ctx* ctx, Csr* c, const std::vector<BankOp>& ops, int G) {
+  if ((int)ops.size() > kMaxFusedOps || !ctx->opt.fused || c->nnz > kFusedMaxNnz || c->hf.nets ||
+      bmt_possible(ctx, c) || ctx->profiling)
+    return false;
+  FusedBank fb{};
+  fb.nops = (int)ops.size();
+  for (size_t i = 0; i < ops.size(); ++i) fb.op[i] = ops[i];
+  void* kern = G == 16 ? (void*)k_bank_fused<16> : (void*)k_bank_fused<8>;
+  static std::mutex mu;
+  static std::map<std::pair<void*, int>, int> grid_of;  // co-resident CTAs (x SMs) per (kernel, device)
+  int grid = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_pair(kern, ctx->device);
+    auto it = grid_of.find(key);
+    if (it == grid_of.end()) {
+      int per_sm = 0;
+      GIFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, 0));
+      grid = std::max(per_sm, 1) * ctx->num_sms;
+      grid_of[key] = grid;
+    } else {
+      grid = it->second;
+    }
+  }
+  void* args[] = {&fb};
+  GIFT_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kBlock), args, 0, ctx->stream));
+  GIFT_LAUNCH_CHECK(ctx);
+  c->fp32_hops += (int64_t)ops.size();
+  return true;
+}
+
+// ops bank_fp32 plans: per column slice, per pack of chains, one prep + its longest chain's hops
+static int64_t bank_ops(const std::vector<TermGroup>& groups, int64_t ncols) {
+  int64_t ops = 0;
+  for (int64_t c0 = 0; c0 < ncols; c0 += 4) {
+    const int per = std::max(1, 4 / (int)std::min<int64_t>(4, ncols - c0));
+    for (size_t g0 = 0; g0 < groups.size(); g0 += per) {
+      int64_t maxk = 0;
+      for (size_t j = g0; j < std::min(groups.size(), g0 + per); ++j) maxk = std::max(maxk, groups[j].maxk);
+      ops += 1 + maxk;
+    }
+  }
+  return ops;
 }
 
 // GIFT_PREC_FP32: fused pre-scaled bank.
@@ -647,34 +775,28 @@ static void bank_fp32(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, in
   const int G = pick_group_lanes(c->mean_row);
   Region4 reg{};
   if (region) memcpy(reg.v, region, sizeof(reg.v));
+  float* zA = static_cast<float*>(scratch(ctx, 0, n * 4 * sizeof(float) + 64));
+  float* zB = static_cast<float*>(scratch(ctx, 1, n * 4 * sizeof(float) + 64));
+  float* accb = static_cast<float*>(scratch(ctx, 2, n * 4 * sizeof(float) + 64));
+  std::vector<BankOp> ops;
   // column slices of <= 4 columns; chains of a slice packed <= 4 floats per row
   for (int64_t c0 = 0; c0 < ncols; c0 += 4) {
     const int wcols = (int)std::min<int64_t>(4, ncols - c0);
     const int per = std::max(1, 4 / wcols);
-    float* zA = static_cast<float*>(scratch(ctx, 0, n * 4 * sizeof(float) + 64));
-    float* zB = static_cast<float*>(scratch(ctx, 1, n * 4 * sizeof(float) + 64));
-    float* accb = static_cast<float*>(scratch(ctx, 2, n * 4 * sizeof(float) + 64));
     bool acc_written = false;
     for (size_t g0 = 0; g0 < groups.size(); g0 += per) {
       const int nch = (int)std::min<size_t>(per, groups.size() - g0);
       const bool last_pack = g0 + nch >= groups.size();
-      const float* sp[4] = {nullptr, nullptr, nullptr, nullptr};
+      BankOp prep{};
+      prep.kind = 0;
+      prep.F = pow2_ceil(wcols * nch);
+      prep.p = PrepArgs{n, wcols, nch, {nullptr, nullptr, nullptr, nullptr}, in_dtype, g, ncols, c0, zA};
       int64_t maxk = 0;
       for (int j = 0; j < nch; ++j) {
-        sp[j] = c->s32[groups[g0 + j].sigma];
+        prep.p.s[j] = c->s32[groups[g0 + j].sigma];
         maxk = std::max(maxk, groups[g0 + j].maxk);
       }
-      const int F0 = pow2_ceil(wcols * nch);
-      {
-        ProfScope prof(ctx, 0, nch);
-        const unsigned grid = grid_for(n, kBlock, 1LL << 30);
-        switch (F0) {
-          case 1: k_prep<1><<<grid, kBlock, 0, ctx->stream>>>(n, wcols, nch, sp[0], sp[1], sp[2], sp[3], in_dtype, g, ncols, c0, zA); break;
-          case 2: k_prep<2><<<grid, kBlock, 0, ctx->stream>>>(n, wcols, nch, sp[0], sp[1], sp[2], sp[3], in_dtype, g, ncols, c0, zA); break;
-          default: k_prep<4><<<grid, kBlock, 0, ctx->stream>>>(n, wcols, nch, sp[0], sp[1], sp[2], sp[3], in_dtype, g, ncols, c0, zA); break;
-        }
-        GIFT_LAUNCH_CHECK(ctx);
-      }
+      ops.push_back(prep);
       // active chains (indices into groups) in packing order
       std::vector<int> active;
       for (int j = 0; j < nch; ++j) active.push_back((int)g0 + j);
@@ -713,8 +835,10 @@ static void bank_fp32(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, in
             ch.cont = -1;
           }
         }
-        const int fin = pow2_ceil(wcols * (int)active.size());
-        const int fout = next.empty() ? 0 : pow2_ceil(wcols * (int)next.size());
+        BankOp hop{};
+        hop.kind = 1;
+        hop.fin = pow2_ceil(wcols * (int)active.size());
+        hop.fout = next.empty() ? 0 : pow2_ceil(wcols * (int)next.size());
         a.acc = accb;
         a.acc_read = acc_written ? 1 : 0;
         a.is_final = (last_pack && h == maxk) ? 1 : 0;
@@ -725,23 +849,37 @@ static void bank_fp32(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, in
         a.fixed_mask = fixed_mask;
         a.fixed_pos = fixed_pos;
         a.reg = reg;
-        if (c->hf.nets) {
-          // implicit high-fanout term: its row sums enter the hop as partial sums
-          float* part = static_cast<float*>(scratch(ctx, 3, n * 4 * sizeof(float) + 64));
-          GIFT_CUDA(cudaMemsetAsync(part, 0, n * fin * sizeof(float), ctx->stream));
-          hf_apply_f32(ctx, c, fin, zin, part);
-          a.part_in = part;
-        }
-        launch_hop(ctx, c, a, fin, fout, G, true);
+        hop.a = a;
+        ops.push_back(hop);
         if (a.any_term) acc_written = true;
         active.swap(next);
         std::swap(zin, zout);
       }
     }
   }
+  if (launch_fused(ctx, c, ops, G)) return;
+  for (BankOp& op : ops) {
+    if (op.kind == 0) {
+      ProfScope prof(ctx, 0, op.p.nch);
+      const unsigned grid = grid_for(n, kBlock, 1LL << 30);
+      switch (op.F) {
+        case 1: k_prep<1><<<grid, kBlock, 0, ctx->stream>>>(op.p); break;
+        case 2: k_prep<2><<<grid, kBlock, 0, ctx->stream>>>(op.p); break;
+        default: k_prep<4><<<grid, kBlock, 0, ctx->stream>>>(op.p); break;
+      }
+      GIFT_LAUNCH_CHECK(ctx);
+      continue;
+    }
+    if (c->hf.nets) {
+      // implicit high-fanout term: its row sums enter the hop as partial sums
+      float* part = static_cast<float*>(scratch(ctx, 3, n * 4 * sizeof(float) + 64));
+      GIFT_CUDA(cudaMemsetAsync(part, 0, n * op.fin * sizeof(float), ctx->stream));
+      hf_apply_f32(ctx, c, op.fin, op.a.zin, part);
+      op.a.part_in = part;
+    }
+    launch_hop(ctx, c, op.a, op.fin, op.fout, G, true);
+  }
 }
-
-static int pick_group_lanes(double mean_row);
 
 // ---- stepped building blocks for host-driven (sharded) banks ----------------
 void scale_vectors(Ctx* ctx, Csr* c, double sigma, const double** s64, const float** s32) {
@@ -802,10 +940,11 @@ void pack_fp32(Ctx* ctx, int64_t n, int wcols, int nch, const float* const* s, i
   const float* sp[4] = {nullptr, nullptr, nullptr, nullptr};
   for (int j = 0; j < nch && j < 4; ++j) sp[j] = s[j];
   const unsigned grid = grid_for(n, kBlock, 1LL << 30);
+  const PrepArgs p{n, wcols, nch, {sp[0], sp[1], sp[2], sp[3]}, in_dtype, g, ld, c0, z};
   switch (F) {
-    case 1: k_prep<1><<<grid, kBlock, 0, ctx->stream>>>(n, wcols, nch, sp[0], sp[1], sp[2], sp[3], in_dtype, g, ld, c0, z); break;
-    case 2: k_prep<2><<<grid, kBlock, 0, ctx->stream>>>(n, wcols, nch, sp[0], sp[1], sp[2], sp[3], in_dtype, g, ld, c0, z); break;
-    case 4: k_prep<4><<<grid, kBlock, 0, ctx->stream>>>(n, wcols, nch, sp[0], sp[1], sp[2], sp[3], in_dtype, g, ld, c0, z); break;
+    case 1: k_prep<1><<<grid, kBlock, 0, ctx->stream>>>(p); break;
+    case 2: k_prep<2><<<grid, kBlock, 0, ctx->stream>>>(p); break;
+    case 4: k_prep<4><<<grid, kBlock, 0, ctx->stream>>>(p); break;
     default: throw_error(GIFT_ERR_VALUE, "F must be 1, 2 or 4");
   }
   GIFT_LAUNCH_CHECK(ctx);
@@ -896,6 +1035,8 @@ static bool bank_graph(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, i
   if (ctx->profiling || c->n <= 0 || c->n >= kGraphMaxRows || ncols <= 0 || !ctx->opt.graphs)
     return false;
   if (bmt_possible(ctx, c)) return false;  // a tiled-copy build cannot run inside a capture
+  // the fused cooperative kernel (bank_fp32) is a single launch already
+  if (ctx->opt.fused && c->nnz <= kFusedMaxNnz && !c->hf.nets && bank_ops(groups, ncols) <= kMaxFusedOps) return false;
   const int64_t n = c->n;
   const size_t in_b = (size_t)(n * ncols) * (in_dtype == GIFT_DTYPE_F64 ? 8 : 4);
   const size_t out_b = (size_t)(n * ncols) * (out_dtype == GIFT_DTYPE_F64 ? 8 : 4);

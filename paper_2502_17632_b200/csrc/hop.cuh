@@ -188,6 +188,21 @@ __device__ __forceinline__ void row_epilogue(const HopArgs& a, int64_t row, floa
     reinterpret_cast<double2*>(a.out)[row] = make_double2(v0, v1);
     return;
   }
+  if (a.wcols == 2 && a.out_ld == 2 && a.out_dtype == GIFT_DTYPE_F32 && ((uintptr_t)a.out & 7) == 0) {
+    // N x 2 fp32 placement: one 8-byte store per row
+    double v0 = (double)o[0], v1 = (double)o[1];
+    if (a.fixed_mask) {
+      if (a.fixed_mask[row]) {
+        v0 = a.fixed_pos[row * 2];
+        v1 = a.fixed_pos[row * 2 + 1];
+      } else {
+        v0 = np_clip(v0, a.reg.v[0], a.reg.v[2]);
+        v1 = np_clip(v1, a.reg.v[1], a.reg.v[3]);
+      }
+    }
+    reinterpret_cast<float2*>(a.out)[row] = make_float2(__double2float_rn(v0), __double2float_rn(v1));
+    return;
+  }
   for (int cc = 0; cc < a.wcols; ++cc) {
     double v = (double)o[cc];
     if (a.fixed_mask) v = a.fixed_mask[row] ? a.fixed_pos[row * 2 + cc] : np_clip(v, a.reg.v[cc], a.reg.v[cc + 2]);

@@ -178,9 +178,10 @@ class SparseSymMatrix:
         of rows left to the row kernel."""
         out = {}
         for which, name in ((0, "f4"), (1, "f2")):
-            info = (ctypes.c_int64 * 8)()
+            info = (ctypes.c_int64 * 10)()
             _lib.check(self._lib.gift_csr_tiled_info(self._h, which, info))
-            keys = ("built", "usable", "tile_rows", "block_cols", "segments", "slices", "slots", "wide_rows")
+            keys = ("built", "usable", "tile_rows", "block_cols", "segments", "slices", "slots", "wide_rows",
+                    "coded", "code_values")
             out[name] = dict(zip(keys, [int(v) for v in info]))
         return out
 

@@ -290,6 +290,7 @@ def test_full_size_bench_config_matches_oracle(gb, orc, config):
     for key, shape in zip(("f4", "f2"), FULL_SHAPES[config]):
         assert info[key]["built"] and info[key]["usable"], (key, info)
         assert (info[key]["tile_rows"], info[key]["block_cols"]) == shape, (key, info)
+    assert not info["f2"]["coded"] and not info["f4"]["coded"]  # fp32 weights (codes are a tuning experiment)
     for got in (first, second):
         assert rel_l2(got, want) <= FP32_TOL
         assert rel_l2(got - centre, want - centre) <= FP32_TOL
@@ -549,6 +550,11 @@ def test_bmt_hop_matches_oracle_and_row_kernel(gb, orc, opts, tiled_always, conf
     assert info["f4"]["built"] or info["f2"]["built"], info
     assert rel_l2(tiled, want) <= FP32_TOL
     assert rel_l2(tiled, row_kernel) <= 1e-6
+    # the L2 prefetch of each warp's next slice changes no result
+    opts(prefetch=0)
+    no_pf = gb.gift_filter(gb.build_clique_graph(fd, max_clique_pins=cap), g32)
+    opts(prefetch=1)
+    assert np.array_equal(no_pf.view(np.int64), tiled.view(np.int64))
     again = gb.gift_filter(adj, g32)
     assert np.array_equal(tiled.view(np.int64), again.view(np.int64))
     placed, _ = gb.gift_place(fd, adj, gb.GiftConfig(seed=3, jitter_scale=10.0))
@@ -804,33 +810,40 @@ def test_implicit_high_fanout_matches_uncapped_oracle(gb, orc, golden, opts, con
 
 
 def test_small_graph_bank_replays_as_cuda_graph(gb, opts):
-    """Below the tiled-hop threshold the fp32 bank is captured once per
-    (graph, terms, widths, dtypes, epilogue) and replayed as a CUDA graph; the
-    replay runs the same kernels in the same order, so results are bit-identical
-    to direct launches, for every key (signal width, terms, epilogue region)."""
+    """Small graphs: the fp32 bank runs as ONE cooperative kernel (grid-wide
+    barrier between prep / hop ops), or -- when that is off or the bank has
+    too many ops -- is captured once per (graph, terms, widths, dtypes,
+    epilogue) and replayed as a CUDA graph.  Both run the same per-row code in
+    the same order as direct launches, so results are bit-identical, for every
+    key (signal width, terms, epilogue region) and across graph lifetimes."""
     from paper_2502_17632_b200 import _lib, synth
 
     fd = synth.generate("c0", seed=8, scale=0.5)
     g32 = synth.signal_fp32(fd, seed=4)
     cfg = gb.GiftConfig(seed=4, jitter_scale=10.0)
     terms = (gb.FilterTerm(1.0, 3, 0.5), gb.FilterTerm(3.0, 1, 0.5))
+    many = tuple(gb.FilterTerm(float(s_), 4, 0.1) for s_ in (1, 2, 3, 4, 5))  # > 10 ops: not fused
 
     def runs():
         adj = gb.build_clique_graph(fd)
         out = [gb.gift_filter(adj, g32), gb.gift_filter(adj, g32[:, :1].copy()),
-               gb.gift_filter(adj, g32, gb.GiftConfig(terms=terms)), gb.gift_place(fd, adj, cfg)[0]]
+               gb.gift_filter(adj, g32, gb.GiftConfig(terms=terms)), gb.gift_place(fd, adj, cfg)[0],
+               gb.gift_filter(adj, g32, gb.GiftConfig(terms=many))]
         out.append(gb.gift_filter(adj, g32))  # replay of the first key
         del adj
         adj = gb.build_clique_graph(fd)  # a new graph (possibly at the same address) captures anew
         out.append(gb.gift_place(fd, adj, cfg)[0])
         return out
 
-    opts(graphs=0)
+    opts(fused=0, graphs=0)
     direct = runs()
     opts(graphs=1)
-    n0 = _lib.launch_count()
     graphed = runs()
-    assert _lib.launch_count() > n0  # replayed kernels are counted
-    for a, b in zip(direct, graphed):
+    opts(fused=1)
+    n0 = _lib.launch_count()
+    fused = runs()
+    assert _lib.launch_count() > n0  # replayed / fused kernels are counted
+    for a, b, c in zip(direct, graphed, fused):
         assert np.array_equal(np.asarray(a).view(np.int64), np.asarray(b).view(np.int64))
-    assert np.array_equal(graphed[0], graphed[4])
+        assert np.array_equal(np.asarray(a).view(np.int64), np.asarray(c).view(np.int64))
+    assert np.array_equal(fused[0], fused[5])
