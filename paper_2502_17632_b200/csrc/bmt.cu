@@ -54,12 +54,21 @@
 #ifndef GIFT_BMT_DEPTH4_512
 #define GIFT_BMT_DEPTH4_512 4
 #endif
+#ifndef GIFT_BMT_DEPTH4_768
+#define GIFT_BMT_DEPTH4_768 5
+#endif
 #ifndef GIFT_BMT_DEPTH2
 #define GIFT_BMT_DEPTH2 5
 #endif
+// threads per CTA of the F = 4 barrier kernel (compile-time; 768 leaves 85
+// registers per thread for a deeper record pipeline)
+#ifndef GIFT_BMT_THREADS4
+#define GIFT_BMT_THREADS4 1024
+#endif
 template <int FIN, int kThreads>
 __host__ __device__ constexpr int bmt_depth() {
-  return FIN == 4 ? (kThreads == 512 ? GIFT_BMT_DEPTH4_512 : GIFT_BMT_DEPTH4) : GIFT_BMT_DEPTH2;
+  return FIN == 4 ? (kThreads == 512 ? GIFT_BMT_DEPTH4_512 : kThreads == 768 ? GIFT_BMT_DEPTH4_768 : GIFT_BMT_DEPTH4)
+                  : GIFT_BMT_DEPTH2;
 }
 
 namespace gift {
@@ -643,15 +652,14 @@ __host__ __device__ constexpr int rec_bytes() {
   return CODED ? 384 : 768;
 }
 
+// p = the lane's weight slot of a record: +256+16l (f32) or +256+4l (codes)
 template <bool CODED>
-__device__ __forceinline__ RecW<CODED> ld_w(const uint8_t* rec, int lane, uint64_t pol) {
+__device__ __forceinline__ RecW<CODED> ld_w(const uint8_t* p, uint64_t pol) {
   RecW<CODED> r;
   if constexpr (CODED) {
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
-                 : "=r"(r.v)
-                 : "l"(rec + 256 + 4 * lane), "l"(pol));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r.v) : "l"(p), "l"(pol));
   } else {
-    r.v = ld_stream_v4f32(reinterpret_cast<const float*>(rec + 256 + 16 * lane), pol);
+    r.v = ld_stream_v4f32(reinterpret_cast<const float*>(p), pol);
   }
   return r;
 }
@@ -677,14 +685,15 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int ste
   float acc[FIN];
 #pragma unroll
   for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
-  const uint8_t* rp = b.data + (off / 128) * RB;
+  const uint8_t* cp = b.data + (off / 128) * RB + 8 * lane;              // the lane's 4 columns
+  const uint8_t* wp = cp - 8 * lane + 256 + (CODED ? 4 : 16) * lane;     // its 4 weights / codes
   uint2 cq[D];
   RecW<CODED> wq[D];
 #pragma unroll
   for (int d = 0; d < D; ++d)
     if (d < steps) {
-      cq[d] = ld_stream_v2u32(rp + d * RB + 8 * lane, pol_s);
-      wq[d] = ld_w<CODED>(rp + d * RB, lane, pol_s);
+      cq[d] = ld_stream_v2u32(cp + d * RB, pol_s);
+      wq[d] = ld_w<CODED>(wp + d * RB, pol_s);
     }
   int rem = steps;
   // steady state: D steps consumed, D reloaded, no predicates
@@ -692,10 +701,11 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int ste
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       step_fma<FIN>(acc, cq[d], weights<CODED>(wq[d], tbl, lane), zs);
-      cq[d] = ld_stream_v2u32(rp + (d + D) * RB + 8 * lane, pol_s);
-      wq[d] = ld_w<CODED>(rp + (d + D) * RB, lane, pol_s);
+      cq[d] = ld_stream_v2u32(cp + (d + D) * RB, pol_s);
+      wq[d] = ld_w<CODED>(wp + (d + D) * RB, pol_s);
     }
-    rp += D * RB;
+    cp += D * RB;
+    wp += D * RB;
     rem -= D;
   }
   // tail: fewer than 2D steps left
@@ -704,8 +714,8 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int ste
     for (int d = 0; d < D; ++d) {
       step_fma<FIN>(acc, cq[d], weights<CODED>(wq[d], tbl, lane), zs);
       if (d + D < rem) {
-        cq[d] = ld_stream_v2u32(rp + (d + D) * RB + 8 * lane, pol_s);
-        wq[d] = ld_w<CODED>(rp + (d + D) * RB, lane, pol_s);
+        cq[d] = ld_stream_v2u32(cp + (d + D) * RB, pol_s);
+        wq[d] = ld_w<CODED>(wp + (d + D) * RB, pol_s);
       }
     }
     rem -= D;
@@ -1099,11 +1109,13 @@ size_t bmt_smem_db(int fin, int kR, int kC, bool coded) {
 
 template <int FIN, int FOUT, bool DB, bool CODED>
 void launch_bmt_k(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles, int tpb, size_t smem) {
+  constexpr int kBig = FIN == 4 ? GIFT_BMT_THREADS4 : 1024;  // the one-CTA-per-SM shape
 #ifdef GIFT_TUNING
-  auto kern = tpb == 1024 ? k_hop_bmt<FIN, FOUT, 1024, DB, CODED> : k_hop_bmt<FIN, FOUT, 512, DB, CODED>;
+  auto kern = tpb == 1024 ? k_hop_bmt<FIN, FOUT, kBig, DB, CODED> : k_hop_bmt<FIN, FOUT, 512, DB, CODED>;
+  if (tpb == 1024) tpb = kBig;
 #else
-  auto kern = k_hop_bmt<FIN, FOUT, 1024, DB, CODED>;  // default shapes are >= 4096 rows: 1 CTA x 1024 per SM
-  (void)tpb;
+  auto kern = k_hop_bmt<FIN, FOUT, kBig, DB, CODED>;  // default shapes are >= 4096 rows: 1 CTA per SM
+  tpb = kBig;
 #endif
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, int> occ;  // resident CTAs per SM per (instance, device)

@@ -6,20 +6,24 @@
 # Outputs in gpurun_out/ (copy what is judged to profiles/).
 set -u
 mkdir -p gpurun_out
-timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 1200 > gpurun_out/pytest_all.log 2>&1
-echo "pytest exit $?"; grep -E "passed|failed" gpurun_out/pytest_all.log | tail -3
-timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
-echo "smoke exit $?"; tail -1 gpurun_out/smoke.log
+if [ "${SKIP_TESTS:-0}" != 1 ]; then
+  timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 1200 > gpurun_out/pytest_all.log 2>&1
+  echo "pytest exit $?"; grep -E "passed|failed" gpurun_out/pytest_all.log | tail -3
+  timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
+  echo "smoke exit $?"; tail -1 gpurun_out/smoke.log
+fi
 for c in c3 c4; do
   timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_hop -s 8 -c 8 \
     -o /tmp/r02_$c python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --no-oneshot > gpurun_out/r02_ncu_$c.log 2>&1
   echo "ncu full $c exit $?"
-  python tools/ncu_summary.py kernels /tmp/r02_$c.ncu-rep > gpurun_out/r02_hop_kernels_$c.txt 2>&1
-  python tools/ncu_stalls.py /tmp/r02_$c.ncu-rep >> gpurun_out/r02_hop_kernels_$c.txt 2>&1
+  # (the reports stay in /tmp: gpurun_out/ must stay under 64 MiB)
+  ncu -i /tmp/r02_$c.ncu-rep --page raw --csv > /tmp/r02_${c}_raw.csv 2>/dev/null
+  python tools/ncu_stalls.py /tmp/r02_${c}_raw.csv > gpurun_out/r02_hop_kernels_$c.txt 2>&1
+  ncu -i /tmp/r02_$c.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > gpurun_out/r02_${c}_sass.csv.gz
+  gzip -c /tmp/r02_${c}_raw.csv > gpurun_out/r02_${c}_raw.csv.gz
   python tools/ncu_traffic.py /tmp/r02_$c.ncu-rep \
     "ncu --set full --clock-control none -k regex:k_hop -s 8 -c 8, bench.py --config $c (tools/evidence_r02.sh)" \
     > gpurun_out/r02_traffic_$c.json
-  cp /tmp/r02_$c.ncu-rep gpurun_out/ 2>/dev/null
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
   --log-file gpurun_out/r02_launches_c3.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-oneshot > gpurun_out/ncu_l.log 2>&1

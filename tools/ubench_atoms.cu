@@ -6,24 +6,26 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-constexpr int kSlots = 8192 * 4;  // F = 4 x 8192 columns
+constexpr int kSlots = 8192 * 4;    // 32-bit tables: F = 4 x 8192 columns (128 KB)
+constexpr int kSlots64 = 8192 * 2;  // 64-bit tables: F = 2 x 8192 columns (128 KB)
 
 template <int MODE>
 __global__ void __launch_bounds__(1024, 1) k_scatter(int iters, float v, unsigned long long* out) {
   extern __shared__ unsigned char smem[];
   unsigned x = 2463534242u ^ (threadIdx.x * 747796405u + blockIdx.x * 2891336453u);
+  constexpr int slots = (MODE == 0 || MODE == 3) ? kSlots64 : kSlots;
   if (MODE == 0 || MODE == 3) {
     unsigned long long* t = reinterpret_cast<unsigned long long*>(smem);
-    for (int i = threadIdx.x; i < kSlots; i += blockDim.x) t[i] = 0;
+    for (int i = threadIdx.x; i < slots; i += blockDim.x) t[i] = 0;
   } else {
     unsigned* t = reinterpret_cast<unsigned*>(smem);
-    for (int i = threadIdx.x; i < kSlots; i += blockDim.x) t[i] = 0;
+    for (int i = threadIdx.x; i < slots; i += blockDim.x) t[i] = 0;
   }
   __syncthreads();
   float acc = v;
   for (int it = 0; it < iters; ++it) {
     x ^= x << 13; x ^= x >> 17; x ^= x << 5;
-    const int slot = x & (kSlots - 1);
+    const int slot = x & (slots - 1);
     acc = acc * 1.0000001f + 0.5f;
     if (MODE == 0) {  // int64 fixed point: float -> int64 conversion + 64-bit shared atomic
       atomicAdd(reinterpret_cast<unsigned long long*>(smem) + slot, (unsigned long long)__float2ll_rn(acc * 4096.f));
@@ -50,7 +52,7 @@ int main() {
   const int iters = 4096;
   const char* names[4] = {"int64 atomics + F2I.S64", "fp32 atomics", "int32 atomics + magic", "int64 atomics + magic"};
   for (int mode = 0; mode < 4; ++mode) {
-    const size_t smem = (mode == 0 || mode == 3) ? kSlots * 8 : kSlots * 4;
+    const size_t smem = (mode == 0 || mode == 3) ? kSlots64 * 8 : kSlots * 4;
     void (*k)(int, float, unsigned long long*) =
         mode == 0 ? k_scatter<0> : mode == 1 ? k_scatter<1> : mode == 2 ? k_scatter<2> : k_scatter<3>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
