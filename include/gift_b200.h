@@ -85,7 +85,8 @@ int gift_ctx_set_tiled_policy(gift_ctx* ctx, int policy);
  *   "zero_copy" 0/1 (pinned host buffers used in place), "schedule" 0/1,
  *   "row_lanes" 0/8/16/32, "codes" 0 (1 only in -DGIFT_TUNING builds: u8
  *   weight codes in the F <= 2 tiled copy, an experiment that measured slower),
- *   "prefetch" 0/1 (tiled hop: L2 bulk prefetch of each warp's next slice; off).
+ *   "prefetch" 0 (1 only in tuning builds: L2 bulk prefetch of each warp's
+ *   next slice, measured slower on long-slice graphs).
  *   Unknown names or values: GIFT_ERR_VALUE. */
 int gift_ctx_set_option(gift_ctx* ctx, const char* name, int64_t value);
 /* Number of kernels this library launched on ctx since creation (for the bench's gpu_launches). */

@@ -133,14 +133,21 @@ void set_option(Ctx* ctx, const std::string& name, int64_t v) {
     if (v != 0 && (v < 11 || v > 14)) bad();
     o.col_bits = v;
   } else if (name == "barrier_free" || name == "graphs" || name == "zero_copy" || name == "schedule" ||
-             name == "fused" || name == "prefetch") {
+             name == "fused" || name == "stream") {
     if (v != 0 && v != 1) bad();
     (name == "barrier_free" ? o.barrier_free
      : name == "graphs"     ? o.graphs
      : name == "zero_copy"  ? o.zero_copy
      : name == "fused"      ? o.fused
-     : name == "prefetch"   ? o.prefetch
+     : name == "stream"     ? o.stream
                             : o.schedule) = v;
+  } else if (name == "prefetch") {
+#ifdef GIFT_TUNING
+    if (v != 0 && v != 1) bad();
+#else
+    if (v != 0) throw_error(GIFT_ERR_VALUE, "option prefetch: only in -DGIFT_TUNING builds");
+#endif
+    o.prefetch = v;
   } else if (name == "codes") {
 #ifdef GIFT_TUNING
     if (v != 0 && v != 1) bad();

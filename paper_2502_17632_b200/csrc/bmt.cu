@@ -580,6 +580,7 @@ struct BmtArgs {
   const int64_t* tile_res;    // [ntiles + 1] range of res_rows per tile
   const float* code_tbl;      // CODED copies: [256] weight of each code (255 = padding, 0)
   int prefetch;               // L2 bulk prefetch of each warp's next slice (option "prefetch")
+  int stream;                 // cross-slice record stream (option "stream")
 };
 
 // CODED kernels: the code table, 16 copies interleaved (see RecW), after the
@@ -742,11 +743,11 @@ __device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, cons
     return __shfl_sync(0xffffffffu, j, 0);
   };
   // the next slice's index and metadata are fetched before the current one
-  // runs, so their latency hides behind its stream.  Option "prefetch" also
-  // bulk-prefetches its records into L2 (off by default: c4, whose slices are
-  // ~2 record steps, gains 1-2 %; c3's long slices lose 20-40 % to the extra
-  // L2 traffic)
-  constexpr int RB = rec_bytes<CODED>();
+  // runs, so their latency hides behind its stream.  Tuning builds' option
+  // "prefetch" also bulk-prefetches its records into L2 (c4, whose slices
+  // are ~2 record steps, gained 1-2 %; c3's long slices lost 20-40 % to the
+  // extra L2 traffic)
+  [[maybe_unused]] constexpr int RB = rec_bytes<CODED>();
   int j = grab();
   int64_t off = 0, end = 0;
   int row = 0xffff;
@@ -763,10 +764,12 @@ __device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, cons
       off_n = b.slice_off[sl0 + jn];
       end_n = b.slice_off[sl0 + jn + 1];
       row_n = b.slice_rows[(sl0 + jn) * 32 + lane];
+#ifdef GIFT_TUNING
       if (b.prefetch && lane == 0)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b.data + (off_n / 128) * RB),
                      "r"((unsigned)((end_n - off_n) / 128 * RB))
                      : "memory");
+#endif
     }
     run_slice<FIN, D, CODED>(b, off, (int)((end - off) / 128), row, zs, accs, tbl, lane, pol_s);
     j = jn;
@@ -774,6 +777,122 @@ __device__ __forceinline__ void segment_slices(const BmtArgs& b, int64_t s, cons
     end = end_n;
     row = row_n;
   }
+}
+
+// Cross-slice record stream (option "stream"): the warp's D-record pipeline
+// runs through every slice the warp takes in a segment instead of restarting
+// per slice.  Each pipeline slot carries its record, the lane's row of the
+// record's slice and whether the record is that slice's last step; consuming
+// a last step flushes the lane's sum into the row accumulator.  The load
+// cursor walks the current slice's records and moves to the next slice
+// (grabbed, with its metadata, one slice ahead) when it runs out, so a slice
+// of 2 record steps (c4) no longer pays a full memory latency of its own.
+// Same per-row entry order as segment_slices: results are bit-identical.
+template <int FIN, int D, bool CODED>
+__device__ __forceinline__ void segment_stream(const BmtArgs& b, int64_t s, const float* zs, float* accs, int* ctr,
+                                               const float* tbl, int lane, uint64_t pol_s) {
+  constexpr int RB = rec_bytes<CODED>();
+  const int64_t sl0 = b.seg_slice[s];
+  const int nsl = (int)(b.seg_slice[s + 1] - sl0);
+  auto grab = [&]() {
+    int j = 0;
+    if (lane == 0) j = atomicAdd(ctr, 1);
+    return __shfl_sync(0xffffffffu, j, 0);
+  };
+  // next slice (metadata fetched one slice ahead)
+  int nx_steps = 0, nx_row = 0xffff;
+  const uint8_t* nx_rec = nullptr;
+  auto fetch_next = [&]() {
+    const int j = grab();
+    nx_steps = 0;
+    nx_row = 0xffff;
+    if (j < nsl) {
+      const int64_t off = b.slice_off[sl0 + j], end = b.slice_off[sl0 + j + 1];
+      nx_steps = (int)((end - off) / 128);
+      nx_row = b.slice_rows[(sl0 + j) * 32 + lane];
+      nx_rec = b.data + (off / 128) * RB;
+    }
+  };
+  // load cursor
+  int cur_left = 0, cur_row = 0xffff;
+  const uint8_t* cur_cp = nullptr;
+  const uint8_t* cur_wp = nullptr;
+  auto advance = [&]() {  // make the cursor point at a record, if any is left
+    while (cur_left == 0 && nx_steps > 0) {
+      cur_left = nx_steps;
+      cur_row = nx_row;
+      cur_cp = nx_rec + 8 * lane;
+      cur_wp = nx_rec + 256 + (CODED ? 4 : 16) * lane;
+      fetch_next();
+    }
+  };
+  uint2 cq[D];
+  RecW<CODED> wq[D];
+  int srow[D];  // lane's row of the slot's slice; bit 16: last step of that slice
+  bool sval[D];
+  fetch_next();
+  advance();
+  int inflight = 0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    sval[d] = cur_left > 0;
+    if (sval[d]) {
+      cq[d] = ld_stream_v2u32(cur_cp, pol_s);
+      wq[d] = ld_w<CODED>(cur_wp, pol_s);
+      srow[d] = cur_row | (cur_left == 1 ? 0x10000 : 0);
+      cur_cp += RB;
+      cur_wp += RB;
+      --cur_left;
+      ++inflight;
+      advance();
+    }
+  }
+  float acc[FIN];
+#pragma unroll
+  for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
+  while (inflight > 0) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      if (sval[d]) {
+        step_fma<FIN>(acc, cq[d], weights<CODED>(wq[d], tbl, lane), zs);
+        --inflight;
+        if (srow[d] & 0x10000) {  // the slice's last step: flush the lane's run sum
+          const int row = srow[d] & 0xffff;
+          if (row != 0xffff) {
+#pragma unroll
+            for (int f = 0; f < FIN; ++f) accs[row * FIN + f] += acc[f];
+          }
+#pragma unroll
+          for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
+        }
+        sval[d] = cur_left > 0;
+        if (sval[d]) {
+          cq[d] = ld_stream_v2u32(cur_cp, pol_s);
+          wq[d] = ld_w<CODED>(cur_wp, pol_s);
+          srow[d] = cur_row | (cur_left == 1 ? 0x10000 : 0);
+          cur_cp += RB;
+          cur_wp += RB;
+          --cur_left;
+          ++inflight;
+          advance();
+        }
+      }
+    }
+  }
+}
+
+// segment processor: per-slice pipelines or the cross-slice stream
+// (compile-time: both in one kernel would share its register budget)
+#ifndef GIFT_BMT_STREAM
+#define GIFT_BMT_STREAM 0
+#endif
+template <int FIN, int D, bool CODED>
+__device__ __forceinline__ void segment_run(const BmtArgs& b, int64_t s, const float* zs, float* accs, int* ctr,
+                                            const float* tbl, int lane, uint64_t pol_s) {
+  if constexpr (GIFT_BMT_STREAM)
+    segment_stream<FIN, D, CODED>(b, s, zs, accs, ctr, tbl, lane, pol_s);
+  else
+    segment_slices<FIN, D, CODED>(b, s, zs, accs, ctr, tbl, lane, pol_s);
 }
 
 // after the segments: residual entries, then the fused row epilogue
@@ -851,7 +970,7 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
     for (int i = nf + tid; i < (kC + kPadRows) * FIN; i += kThreads) zs[i] = 0.f;  // short block + padding rows
     if (tid == 0) slice_ctr = 0;
     __syncthreads();
-    segment_slices<FIN, bmt_depth<FIN, kThreads>(), CODED>(b, s, zs, accs, &slice_ctr, tbl, lane, pol_s);
+    segment_run<FIN, bmt_depth<FIN, kThreads>(), CODED>(b, s, zs, accs, &slice_ctr, tbl, lane, pol_s);
   }
   bmt_tile_finish<FIN, FOUT, kThreads>(a, b, tile, r0, nrows, accs, tid, lane, pol_z);
 }
@@ -908,7 +1027,7 @@ __device__ __forceinline__ void bmt_tile_db(const HopArgs& a, const BmtArgs& b, 
       stage_async<FIN, kThreads>(a, b, s + 1, buf ? zs0 : zs1, tid, pol_z);
       if (tid == 0) slice_ctr2[buf ^ 1] = 0;
     }
-    segment_slices<FIN, bmt_depth<FIN, kThreads>(), CODED>(b, s, buf ? zs1 : zs0, accs, &slice_ctr2[buf], tbl, lane,
+    segment_run<FIN, bmt_depth<FIN, kThreads>(), CODED>(b, s, buf ? zs1 : zs0, accs, &slice_ctr2[buf], tbl, lane,
                                                            pol_s);
   }
   bmt_tile_finish<FIN, FOUT, kThreads>(a, b, tile, r0, nrows, accs, tid, lane, pol_z);
@@ -1073,7 +1192,7 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt_nb(HopArg
   for (int i = 0; i < nseg; ++i) {
     const int buf = i & 1;
     mbar_wait(&full[buf], (unsigned)(i >> 1) & 1u);
-    segment_slices<FIN, bmt_depth<FIN, kThreads>(), CODED>(b, s0 + i, zs[buf], acc[buf], &slice_ctr[buf], tbl, lane,
+    segment_run<FIN, bmt_depth<FIN, kThreads>(), CODED>(b, s0 + i, zs[buf], acc[buf], &slice_ctr[buf], tbl, lane,
                                                            pol_s);
     __syncwarp();
     if (lane == 0) {
@@ -1691,7 +1810,8 @@ bool bmt_hop(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
 #endif
   BmtArgs b{c->n,         B.tile_rows,  B.kC,         B.data,      B.wide,      B.res_rowptr, B.res_col,     B.res_w,
             B.tile_seg,   B.seg_code,   B.seg_slice, B.slice_off, B.slice_rows, order,         ctr,
-            B.ntiles,     B.res_rows,   B.tile_res,  B.code_tbl,  (int)ctx->opt.prefetch};
+            B.ntiles,     B.res_rows,   B.tile_res,  B.code_tbl,  (int)ctx->opt.prefetch,
+            (int)ctx->opt.stream};
   switch (fin) {
     case 1: launch_bmt_out<1>(ctx, a, b, B.ntiles, fout, B.coded); break;
     case 2: launch_bmt_out<2>(ctx, a, b, B.ntiles, fout, B.coded); break;

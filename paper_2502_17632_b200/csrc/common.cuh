@@ -68,6 +68,7 @@ struct Ctx {
     int64_t row_lanes = 0;          // "row_lanes": force lanes per row of the row kernel (8 / 16 / 32)
     int64_t codes = 0;              // "codes" (tuning builds): u8 weight codes in the F <= 2 tiled copy
     int64_t prefetch = 0;           // "prefetch": tiled hop prefetches each warp's next slice into L2
+    int64_t stream = 0;             // "stream": tiled hop pipelines records across a warp's slices
   } opt;
   std::recursive_mutex mu;        // entry points serialise on the context (scratch, stream, logs)
   // persistent BMT tile scheduler counters [next tile, finished CTAs], one
