@@ -46,10 +46,11 @@
 
 
 // records in flight per warp (software-pipeline depth), per signal width; at
-// F = 4, 4 on 512-thread CTAs (c3 F=4 pass 1.138 -> 1.117 ms) and 3 on
-// 1024-thread ones (c4: 4 was 1.5 % slower)
+// F = 4, 4 on 512-thread CTAs (c3 F=4 pass 1.138 -> 1.117 ms) and 4 on
+// 1024-thread ones (round 2, same-box A/B: c3 F=4 pass 1.050 -> 1.035 ms,
+// c4 2.149 -> 2.144; round 1 had measured 3 ahead on c4)
 #ifndef GIFT_BMT_DEPTH4
-#define GIFT_BMT_DEPTH4 3
+#define GIFT_BMT_DEPTH4 4
 #endif
 #ifndef GIFT_BMT_DEPTH4_512
 #define GIFT_BMT_DEPTH4_512 4

@@ -133,3 +133,56 @@ def test_design_validation():
     with pytest.raises(gb.GiftPlaceError):
         gb.Design([gb.Cell(id=0, name="a", width=1, height=1)], [gb.Net(0, "n", [gb.Pin(3)])],
                   gb.Region(0, 0, 1, 1)).validate()
+
+
+def test_kernel_options_are_validated_and_restored():
+    """_lib.set_option / options(): unknown names fail; values are kept for
+    contexts created later and restored by the context manager."""
+    from paper_2502_17632_b200 import _lib
+
+    with pytest.raises(ValueError):
+        _lib.set_option("no_such_option", 1)
+    before = dict(_lib._options)
+    with _lib.options(tile_rows=4096, graphs=0):
+        assert _lib._options["tile_rows"] == 4096 and _lib._options["graphs"] == 0
+    assert _lib._options == before
+    assert set(_lib.DEFAULT_OPTIONS) >= {"tiled", "tile_rows", "col_bits", "fused", "graphs", "zero_copy"}
+
+
+def test_gift_config_output_dtype():
+    assert gb.GiftConfig().output_dtype == "float64"
+    assert gb.GiftConfig(output_dtype="float32").output_dtype == "float32"
+    with pytest.raises(ValueError):
+        gb.GiftConfig(output_dtype="float16")
+
+
+def test_exchange_plan_groups_ghosts_by_owner():
+    """shard.exchange_plan: ghosts are requested from the rank owning them,
+    and the rows a rank is asked for come back as local row ids."""
+    from paper_2502_17632_b200 import shard
+
+    bounds = np.array([0, 10, 25, 40])
+    asked_of = {}
+
+    def fake_ids(requests):  # rank 1's all-to-all: echo what others would ask of it
+        asked_of["req"] = requests
+        return [np.array([10, 12]), np.zeros(0, np.int64), np.array([24])]
+
+    plan = shard.exchange_plan(bounds, 1, np.array([3, 9, 30, 31]), fake_ids)
+    assert (plan.r0, plan.r1) == (10, 25)
+    assert plan.recv_counts == [2, 0, 2]
+    assert [list(r) for r in asked_of["req"]] == [[3, 9], [], [30, 31]]
+    assert plan.send_counts == [2, 0, 1] and list(plan.send_rows) == [0, 2, 14]
+    assert plan.n_local == 15 and plan.n_ghost == 4
+
+
+def test_split_block_host_restatement():
+    from paper_2502_17632_b200 import shard
+
+    # 4 x 4 symmetric pattern; rows [1, 3) own columns 1, 2
+    indptr = np.array([0, 2, 5, 7, 8])
+    indices = np.array([1, 3, 0, 2, 3, 1, 3, 0])
+    ghosts, loc, gh = shard.split_block(indptr, indices, 1, 3)
+    assert list(ghosts) == [0, 3]
+    assert list(loc[0]) == [0, 1, 2] and list(loc[1]) == [1, 0] and list(loc[2]) == [3, 5]
+    assert list(gh[0]) == [0, 2, 3] and list(gh[1]) == [2, 3, 3] and list(gh[2]) == [2, 4, 6]

@@ -187,3 +187,15 @@ def test_config_samples_match_reference_hashes(orc, name):
     placed = orc.place_epilogue(orc.gift_filter(A, g0, DEFAULT, deg), fd.fixed_mask(), fd.fixed_positions(),
                                 [r.xmin, r.ymin, r.xmax, r.ymax])
     assert sha(placed) == meta["place_sha"]
+
+
+@pytest.mark.parametrize("cap", [0, 1, -2])
+def test_caps_below_two_skip_every_net(orc, cap):
+    """graph.py:136: nets with m > max_clique_pins are skipped, so a cap below 2
+    (0 is a cap, not "no cap") leaves an empty graph."""
+    ns = np.array([0, 2, 5, 9])
+    pc = np.array([0, 1, 1, 2, 3, 0, 1, 2, 3])
+    A = orc.build_clique_graph(4, ns, pc, cap)
+    assert A.nnz == 0
+    assert orc.build_clique_graph(4, ns, pc, 2).nnz == 2
+    assert orc.build_clique_graph(4, ns, pc, None).nnz > 2
