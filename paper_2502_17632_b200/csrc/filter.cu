@@ -719,6 +719,18 @@ static int pick_group_lanes(double mean_row) {
 // c0 (0.66M entries) 0.052 -> 0.042 ms per bank, c1 (13.6M) 0.28 -> 0.32 ms
 constexpr int64_t kFusedMaxNnz = 1LL << 21;
 
+// lanes per row of the fp32 bank's row-kernel hops.  Small graphs (the fused
+// regime) are latency-bound: a lane streams about one 4-entry chunk, so a hop
+// is one load round trip (c0, mean row 64: 16 lanes; 8 lanes took 54 us per
+// fused bank, 16 take 39 us).  Larger graphs keep the throughput-tuned
+// choice.  The same rule serves fused, graph-replayed and direct launches, so
+// they agree bit for bit.
+static int bank_lanes(Ctx* ctx, const Csr* c) {
+  if (ctx->opt.row_lanes) return (int)ctx->opt.row_lanes;
+  if (c->nnz <= kFusedMaxNnz) return std::min(32, std::max(8, pow2_ceil((int)(c->mean_row / 4.0 + 0.5))));
+  return pick_group_lanes(c->mean_row);
+}
+
 static bool launch_fused(Ctx* ctx, Csr* c, const std::vector<BankOp>& ops, int G) {
   if ((int)ops.size() > kMaxFusedOps || !ctx->opt.fused || c->nnz > kFusedMaxNnz || c->hf.nets ||
       bmt_possible(ctx, c) || ctx->profiling)
@@ -726,7 +738,7 @@ static bool launch_fused(Ctx* ctx, Csr* c, const std::vector<BankOp>& ops, int G
   FusedBank fb{};
   fb.nops = (int)ops.size();
   for (size_t i = 0; i < ops.size(); ++i) fb.op[i] = ops[i];
-  void* kern = G == 16 ? (void*)k_bank_fused<16> : (void*)k_bank_fused<8>;
+  void* kern = G == 32 ? (void*)k_bank_fused<32> : G == 16 ? (void*)k_bank_fused<16> : (void*)k_bank_fused<8>;
   static std::mutex mu;
   static std::map<std::pair<void*, int>, int> grid_of;  // co-resident CTAs (x SMs) per (kernel, device)
   int grid = 0;
@@ -772,7 +784,7 @@ static void bank_fp32(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, in
   for (auto& grp : groups) csr_scale(ctx, c, grp.sigma);
   if (n == 0 || ncols == 0) return;
   const float* w = csr_w32(ctx, c);
-  const int G = pick_group_lanes(c->mean_row);
+  const int G = bank_lanes(ctx, c);
   Region4 reg{};
   if (region) memcpy(reg.v, region, sizeof(reg.v));
   float* zA = static_cast<float*>(scratch(ctx, 0, n * 4 * sizeof(float) + 64));
