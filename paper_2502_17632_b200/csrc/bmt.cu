@@ -61,6 +61,10 @@
 #ifndef GIFT_BMT_DEPTH2
 #define GIFT_BMT_DEPTH2 5
 #endif
+// segment blocks staged by one bulk async copy (1) or by all threads (0)
+#ifndef GIFT_BMT_BULK
+#define GIFT_BMT_BULK 1
+#endif
 // threads per CTA of the F = 4 barrier kernel (compile-time; 768 leaves 85
 // registers per thread for a deeper record pipeline)
 #ifndef GIFT_BMT_THREADS4
@@ -940,18 +944,75 @@ __device__ __forceinline__ void bmt_tile_finish(const HopArgs& a, const BmtArgs&
   }
 }
 
-// one staging buffer: stage, barrier, slices, barrier
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(m)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* m, unsigned bytes) {
+  uint64_t state;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+               : "=l"(state)
+               : "r"(smem_addr(m)), "r"(bytes)
+               : "memory");
+  asm volatile("" ::"l"(state));  // the phase token is not needed
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_addr(m)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+// segment s's signal block -> dst: one bulk copy of the 16-byte-aligned part,
+// the ragged tail (last block of an odd-sized signal) by this thread's own
+// stores, which the arrive (release) publishes together with the copy
+template <int FIN>
+__device__ __forceinline__ void stage_bulk(const HopArgs& a, const BmtArgs& b, int64_t s, float* dst, uint64_t* full,
+                                           uint64_t pol) {
+  const int64_t cbase = (int64_t)b.seg_code[s] * b.kC;
+  const int64_t cend = min(cbase + b.kC, b.ncols);
+  const unsigned nf = (unsigned)((cend - cbase) * FIN);
+  const unsigned bytes = (nf * 4u) & ~15u;
+  const float* src = a.zin + cbase * FIN;
+  for (unsigned i = bytes / 4; i < nf; ++i) dst[i] = src[i];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of dst before the async write
+  mbar_arrive_expect_tx(full, bytes);
+  if (bytes)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(full)), "l"(pol)
+        : "memory");
+}
+
+// one staging buffer: stage, barrier, slices, barrier.  The block is staged
+// by ONE bulk async copy (cp.async.bulk global -> shared, completion on an
+// mbarrier) issued by thread 0 -- the warps spend no load / store issue on
+// it -- or, for a signal that is not 16-byte aligned, by all threads.
 template <int FIN, int FOUT, int kThreads, bool CODED>
 __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int64_t tile, int kR, int tid, int lane,
                                          uint64_t pol_s, uint64_t pol_z) {
   extern __shared__ float4 smem_f4[];
   __shared__ int slice_ctr;
+  __shared__ uint64_t full;
   const int kC = b.kC;
   float* zs = reinterpret_cast<float*>(smem_f4);  // [(kC + kPadRows) * FIN], rows >= kC stay zero
   float* accs = zs + (kC + kPadRows) * FIN;         // [kR * FIN]
   const float* tbl = accs + kR * FIN;               // CODED: [256 * 16] code table
   const int64_t r0 = tile * kR;
   const int nrows = (int)min((int64_t)kR, a.n - r0);
+  const bool bulk = GIFT_BMT_BULK && (reinterpret_cast<uintptr_t>(a.zin) & 15) == 0;
+  if (bulk && tid == 0) {  // visible after the first segment's barrier
+    mbar_init(&full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  unsigned parity = 0;
   for (int i = tid; i < nrows * FIN; i += kThreads) accs[i] = 0.f;
   const int64_t s_end = b.tile_seg[tile + 1];
   for (int64_t s = b.tile_seg[tile]; s < s_end; ++s) {
@@ -962,15 +1023,23 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
     __syncthreads();
     const int64_t cend = min(cbase + kC, b.ncols);
     const int nf = (int)((cend - cbase) * FIN);
-    const int nv = nf / 4;
-    const float4* src = reinterpret_cast<const float4*>(zg);
-    float4* dst = reinterpret_cast<float4*>(zs);
+    if (bulk) {
+      if (tid == 0) stage_bulk<FIN>(a, b, s, zs, &full, pol_z);
+    } else {
+      const int nv = nf / 4;
+      const float4* src = reinterpret_cast<const float4*>(zg);
+      float4* dst = reinterpret_cast<float4*>(zs);
 #pragma unroll 4
-    for (int i = tid; i < nv; i += kThreads) dst[i] = src[i];
-    for (int i = nv * 4 + tid; i < nf; i += kThreads) zs[i] = zg[i];
+      for (int i = tid; i < nv; i += kThreads) dst[i] = src[i];
+      for (int i = nv * 4 + tid; i < nf; i += kThreads) zs[i] = zg[i];
+    }
     for (int i = nf + tid; i < (kC + kPadRows) * FIN; i += kThreads) zs[i] = 0.f;  // short block + padding rows
     if (tid == 0) slice_ctr = 0;
     __syncthreads();
+    if (bulk) {
+      mbar_wait(&full, parity);
+      parity ^= 1u;
+    }
     segment_run<FIN, bmt_depth<FIN, kThreads>(), CODED>(b, s, zs, accs, &slice_ctr, tbl, lane, pol_s);
   }
   bmt_tile_finish<FIN, FOUT, kThreads>(a, b, tile, r0, nrows, accs, tid, lane, pol_z);
@@ -1100,53 +1169,6 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt(HopArgs a
 // order, so the result stays deterministic (it is a different, equally valid
 // fp32 association than the single-bank kernels).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* m, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(m)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* m, unsigned bytes) {
-  uint64_t state;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
-               : "=l"(state)
-               : "r"(smem_addr(m)), "r"(bytes)
-               : "memory");
-  asm volatile("" ::"l"(state));  // the phase token is not needed
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(smem_addr(m)), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-
-// segment s's signal block -> dst: one bulk copy of the 16-byte-aligned part,
-// the ragged tail (last block of an odd-sized signal) by this thread's own
-// stores, which the arrive (release) publishes together with the copy
-template <int FIN>
-__device__ __forceinline__ void stage_bulk(const HopArgs& a, const BmtArgs& b, int64_t s, float* dst, uint64_t* full,
-                                           uint64_t pol) {
-  const int64_t cbase = (int64_t)b.seg_code[s] * b.kC;
-  const int64_t cend = min(cbase + b.kC, b.ncols);
-  const unsigned nf = (unsigned)((cend - cbase) * FIN);
-  const unsigned bytes = (nf * 4u) & ~15u;
-  const float* src = a.zin + cbase * FIN;
-  for (unsigned i = bytes / 4; i < nf; ++i) dst[i] = src[i];
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of dst before the async write
-  mbar_arrive_expect_tx(full, bytes);
-  if (bytes)
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-        ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(full)), "l"(pol)
-        : "memory");
-}
-
 template <int FIN, int FOUT, int kThreads, bool CODED>
 __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_hop_bmt_nb(HopArgs a, BmtArgs b) {
   extern __shared__ float4 smem_f4[];
