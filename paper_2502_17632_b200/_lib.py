@@ -197,13 +197,13 @@ def set_tiled_policy(policy: str) -> None:
 
 DEFAULT_OPTIONS = {"tiled": 1, "tiled_min_rows": 262144, "tiled_min_mean": 32, "tile_rows": 0, "col_bits": 0,
                    "barrier_free": 1, "graphs": 1, "fused": 1, "zero_copy": 1, "schedule": 1, "row_lanes": 0,
-                   "codes": 0, "prefetch": 0, "stream": 0}
+                   "codes": 0, "prefetch": 0, "stream": 0, "balance": 1}
 
 
 def set_option(name: str, value: int) -> None:
     """Kernel-selection option (gift_ctx_set_option) for every context, present
     and future: tiled, tiled_min_rows, tiled_min_mean, tile_rows, col_bits,
-    barrier_free, graphs, zero_copy, schedule, row_lanes."""
+    barrier_free, graphs, zero_copy, schedule, row_lanes, balance."""
     if name not in DEFAULT_OPTIONS:
         raise ValueError(f"unknown option {name!r}")
     lib = load_library()

@@ -122,20 +122,21 @@ void set_option(Ctx* ctx, const std::string& name, int64_t v) {
     if (v < 0) bad();
     o.tiled_min_mean = v;
   } else if (name == "tile_rows") {
-    if (v != 0 && v != 4096 && v != 8192 && v != 16384
 #ifdef GIFT_TUNING
-        && v != 1024 && v != 2048
+    const int64_t lo = 1024;
+#else
+    const int64_t lo = 2048;
 #endif
-    )
-      bad();
+    if (v != 0 && (v < lo || v > 16384 || v % 32 != 0)) bad();
     o.tile_rows = v;
   } else if (name == "col_bits") {
     if (v != 0 && (v < 11 || v > 14)) bad();
     o.col_bits = v;
   } else if (name == "barrier_free" || name == "graphs" || name == "zero_copy" || name == "schedule" ||
-             name == "fused" || name == "stream") {
+             name == "fused" || name == "stream" || name == "balance") {
     if (v != 0 && v != 1) bad();
     (name == "barrier_free" ? o.barrier_free
+     : name == "balance"    ? o.balance
      : name == "graphs"     ? o.graphs
      : name == "zero_copy"  ? o.zero_copy
      : name == "fused"      ? o.fused

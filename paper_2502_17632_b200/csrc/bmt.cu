@@ -97,10 +97,26 @@ namespace {
 struct BmtShape {
   int kR, cb;
 };
-BmtShape bmt_shape_for(const Ctx* ctx, double mean_row, bool wide_blocks) {
+BmtShape bmt_shape_for(const Ctx* ctx, int64_t n, double mean_row, bool wide_blocks) {
   BmtShape s = wide_blocks ? BmtShape{8192, 14} : (mean_row >= 160.0 ? BmtShape{8192, 12} : BmtShape{4096, 13});
   if (ctx->opt.tile_rows) s.kR = (int)ctx->opt.tile_rows;  // forced shape (option "tile_rows")
   if (ctx->opt.col_bits) s.cb = (int)ctx->opt.col_bits;    // option "col_bits"
+  // Even waves (option "balance").  The default shapes run one CTA per SM and
+  // one CTA per tile, so ceil(n / kR) tiles take ceil(tiles / SMs) waves: c3's
+  // 269 tiles of 8192 rows on 148 SMs are 2 waves of which the second is 82 %
+  // full, and the F = 4 pass -- bound per SM by the shared-memory pipe, not by
+  // DRAM -- loses that idle time (the DRAM-bound F = 2 pass does not: fewer
+  // SMs share the same bandwidth).  The tile height shrinks to the smallest
+  // multiple of 32 that keeps the wave count: 7424 rows = 296 tiles = 2 x 148.
+  // Graphs with fewer tiles than SMs get shorter tiles (down to 2048 rows) so
+  // every SM has one.
+  if (!ctx->opt.tile_rows && ctx->opt.balance && n > 0) {
+    const int64_t sms = ctx->num_sms > 0 ? ctx->num_sms : 148;
+    const int64_t waves = (n + (int64_t)s.kR * sms - 1) / ((int64_t)s.kR * sms);
+    int64_t kr = (n + waves * sms - 1) / (waves * sms);
+    kr = (kr + 31) / 32 * 32;
+    s.kR = (int)std::min<int64_t>(s.kR, std::max<int64_t>(kr, 2048));
+  }
   return s;
 }
 constexpr int kPadRows = 16;      // one zero row per bank residue mod 16 (padding never conflicts)
@@ -1452,7 +1468,7 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32, Csr::Bmt& B, bool wide_blocks
   cudaStream_t st = ctx->stream;
   const bool coded = wide_blocks && ctx->opt.codes;  // tuning builds only (see launch_bmt_out)
   const int64_t n = c->n, nnz_all = c->nnz;
-  const BmtShape shape = bmt_shape_for(ctx, c->mean_row, wide_blocks);
+  const BmtShape shape = bmt_shape_for(ctx, c->n, c->mean_row, wide_blocks);
   const int kR = shape.kR, cb = shape.cb, kC = 1 << cb;
   const int64_t ntiles = (n + kR - 1) / kR;
   const int64_t nblocks = (n + kC - 1) / kC;

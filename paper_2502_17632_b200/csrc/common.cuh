@@ -58,7 +58,8 @@ struct Ctx {
     int64_t tiled = 1;              // "tiled": 0 = row kernel only
     int64_t tiled_min_rows = 262144;  // "tiled_min_rows": smaller graphs stay on the row kernel
     int64_t tiled_min_mean = 32;    // "tiled_min_mean": mean row length below which too
-    int64_t tile_rows = 0;          // "tile_rows": force the tile height (4096 / 8192 / 16384), 0 = per graph
+    int64_t tile_rows = 0;          // "tile_rows": force the tile height (multiple of 32 in 2048..16384), 0 = per graph
+    int64_t balance = 1;            // "balance": shrink the default tile height to fill whole waves of SMs
     int64_t col_bits = 0;           // "col_bits": force log2 of the block width (11..14), 0 = per graph
     int64_t barrier_free = 1;       // "barrier_free": the bulk-copy pipeline where it fits
     int64_t graphs = 1;             // "graphs": replay small-graph banks as CUDA graphs

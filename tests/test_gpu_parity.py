@@ -253,8 +253,15 @@ def test_heavy_tail_configs_scaled_match_oracle(gb, orc, config, scale, cap):
 
 # Default tiled-copy shapes (csrc/bmt.cu bmt_shape_for): F = 4 copy 8192 x 4096
 # on long-row graphs (c3), 4096 x 8192 on short-row ones (c4); F <= 2 copy
-# 8192 x 16384 on both.
+# 8192 x 16384 on both -- the tile height then shrunk to fill whole waves of
+# SMs (option "balance": c3 on 148 SMs runs 7424-row tiles, 296 = 2 x 148).
 FULL_SHAPES = {"c3": ((8192, 4096), (8192, 16384)), "c4": ((4096, 8192), (8192, 16384))}
+
+
+def _balanced_rows(n, rows, sms):
+    waves = -(-n // (rows * sms))
+    kr = -(-n // (waves * sms))
+    return min(rows, max(-(-kr // 32) * 32, 2048))
 
 
 @pytest.mark.parametrize("config", ["c3", "c4"])
@@ -262,8 +269,8 @@ def test_full_size_bench_config_matches_oracle(gb, orc, config):
     """The exact workload bench.py times (full-size config, seed 1, fp32
     seed of synth.signal_fp32, default bank) on the default kernel selection:
     the first bank on the graph runs the row kernel, the second builds and
-    runs the tiled copies (8192-row tiles, 1024-thread CTAs, wide rows on the
-    side stream).  CSR + degrees bit-exact against the oracle, both banks and
+    runs the tiled copies (wave-balanced tiles of up to 8192 rows, 1024-thread
+    CTAs, wide rows on the side stream).  CSR + degrees bit-exact against the oracle, both banks and
     the fused placement within 1e-5 relative L2."""
     from paper_2502_17632_b200 import synth
 
@@ -287,9 +294,13 @@ def test_full_size_bench_config_matches_oracle(gb, orc, config):
     assert not adj.tiled_info()["f4"]["built"]
     second = gb.gift_filter(adj, g32)  # graph reused: tiled copies built and used
     info = adj.tiled_info()
+    import torch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
     for key, shape in zip(("f4", "f2"), FULL_SHAPES[config]):
         assert info[key]["built"] and info[key]["usable"], (key, info)
-        assert (info[key]["tile_rows"], info[key]["block_cols"]) == shape, (key, info)
+        want_shape = (_balanced_rows(adj.n, shape[0], sms), shape[1])
+        assert (info[key]["tile_rows"], info[key]["block_cols"]) == want_shape, (key, info)
     assert not info["f2"]["coded"] and not info["f4"]["coded"]  # fp32 weights (codes are a tuning experiment)
     for got in (first, second):
         assert rel_l2(got, want) <= FP32_TOL
