@@ -38,8 +38,11 @@ Multi-GPU: `--gpus N` launches N ranks itself (torch.distributed.run, one
 process per GPU) unless WORLD_SIZE is already set.  The SAME graph is
 row-sharded over the ranks (strong scaling, paper_2502_17632_b200/shard.py):
 each rank builds the graph on its GPU, cuts its nnz-balanced row block on the
-device (no host copy of the CSR), and exchanges ghost rows per hop by NCCL
-all_to_all overlapped with the local part of the hop; `value` counts the one
+device (no host copy of the CSR), and gets its ghost rows per hop straight
+from the owners' signal buffers over NVLink peer memory (`--exchange peer`,
+the default: CUDA IPC mappings + one kernel of peer loads, csrc/peer.cu;
+falls back to the NCCL all_to_all of `--exchange nccl` if the mappings cannot
+be made), overlapped with the local part of the hop; `value` counts the one
 graph's nnz_op * 6 per step over the max-rank time.  `--config c4` is the
 north-star scaling configuration (10M cells).
 """
@@ -363,6 +366,8 @@ def main() -> None:
     ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
                     help="kernel option (gift_ctx_set_option), e.g. tile_rows=4096; repeatable")
     ap.add_argument("--oneshot", choices=["python", "abi"], default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
+                    help="N > 1: ghost rows by NVLink peer loads (CUDA IPC) or by NCCL all_to_all")
     ap.add_argument("--dry-launch", action="store_true", help="form the process group and exit (launcher test)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -426,7 +431,21 @@ def main() -> None:
     else:
         from paper_2502_17632_b200 import shard
 
-        sf = shard.cuda_sharded_filter(adj, world, rank, local)
+        exchange_used = "nccl"
+        sf = None
+        if args.exchange == "peer":
+            # every rank must take the same path: agree on whether the mappings worked
+            ok = torch.ones(1, dtype=torch.int32, device=dev)
+            try:
+                sf = shard.cuda_sharded_filter(adj, world, rank, local,
+                                               exchange=shard.PeerExchange(device=f"cuda:{local}"))
+            except Exception as e:  # no peer access / IPC on this box
+                print(f"[bench] rank {rank}: peer exchange unavailable ({e!r}); using NCCL", file=sys.stderr)
+                ok.zero_()
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            exchange_used = "peer" if int(ok.item()) else "nccl"
+        if exchange_used == "nccl":
+            sf = shard.cuda_sharded_filter(adj, world, rank, local)
         r0, r1 = sf.plan.r0, sf.plan.r1
     dg = torch.from_numpy(np.ascontiguousarray(g32[r0:r1])).to(dev)
     dmask = torch.from_numpy(np.ascontiguousarray(mask[r0:r1])).to(dev)
@@ -630,7 +649,9 @@ def main() -> None:
                 "n": n, "nnz": adj.nnz, "nnz_op": nnz_op, "hops": HOPS, "seed": args.seed,
                 "bytes_per_hop_unit": unit_bytes,
                 "l2": "inputs larger than L2 (CSR col+w32 = %.2f GB per pass)" % (8 * adj.nnz / 1e9),
-                "parallelism": f"row-sharded x{world} (NCCL ghost all_to_all per hop)" if world > 1
+                "parallelism": (f"row-sharded x{world} (ghost rows pulled over NVLink peer memory per hop)"
+                                if exchange_used == "peer" else
+                                f"row-sharded x{world} (NCCL ghost all_to_all per hop)") if world > 1
                 else "single GPU",
                 "kernel_times": "per-launch CUDA events in the timed region" if not graph_replay else
                 "per-launch CUDA events in a profiled pass after the timed region (the timed steps replay the "

@@ -248,6 +248,25 @@ int gift_csr_ext_ids(const gift_csr* ghost, const int64_t** d_ids, int64_t* n_id
 /* dst[r, :] = src[idx[r], :] for F floats per row (halo send buffers). */
 int gift_gather_rows_f32(gift_ctx* ctx, int64_t n_idx, int F, const int64_t* d_idx, const float* d_src,
                          float* d_dst);
+/* Ghost rows over NVLink peer memory instead of a collective (csrc/peer.cu;
+ * the reference has no distributed code -- this shards gift.py:73-95 over
+ * GPUs).  A rank's signal buffers live in plain device allocations
+ * (gift_peer_alloc, zero-filled) whose CUDA IPC handle (64 bytes) the other
+ * ranks' processes open once (gift_peer_open: peer access over NVLink).
+ * gift_pull_rows_f32 copies, for every ghost row i,
+ *   dst[i, :F] = peers[src_rank[i]][src_row[i], :F]
+ * (d_peers: device array of one base pointer per rank) on a stream forked
+ * from the context's stream; gift_pull_join makes the context's stream wait
+ * for it, so work enqueued in between (the local part of the hop) overlaps
+ * the transfer.  The caller orders ranks with a per-hop barrier (shard.py). */
+#define GIFT_PEER_HANDLE_BYTES 64
+int gift_peer_alloc(gift_ctx* ctx, int64_t bytes, void** d_ptr, unsigned char* h_handle);
+int gift_peer_open(gift_ctx* ctx, const unsigned char* h_handle, void** d_ptr);
+int gift_peer_close(gift_ctx* ctx, void* d_ptr);
+int gift_peer_free(gift_ctx* ctx, void* d_ptr);
+int gift_pull_rows_f32(gift_ctx* ctx, int64_t n_rows, int F, const void* const* d_peers, const int32_t* d_src_rank,
+                       const int64_t* d_src_row, float* d_dst);
+int gift_pull_join(gift_ctx* ctx);
 
 /* ---- placement metrics: consumers of the filter output --
  * fp64, fixed reduction trees (deterministic; numpy's pairwise / BLAS order

@@ -85,6 +85,12 @@ SIGNATURES = [
     ("gift_hop_fp32", c_int, [c_vp, c_vp, c_vp]),
     ("gift_pack_fp32", c_int, [c_vp, c_i64, c_int, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_int, c_vp]),
     ("gift_gather_rows_f32", c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp]),
+    ("gift_peer_alloc", c_int, [c_vp, c_i64, ctypes.POINTER(c_vp), c_vp]),
+    ("gift_peer_open", c_int, [c_vp, c_vp, ctypes.POINTER(c_vp)]),
+    ("gift_peer_close", c_int, [c_vp, c_vp]),
+    ("gift_peer_free", c_int, [c_vp, c_vp]),
+    ("gift_pull_rows_f32", c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp]),
+    ("gift_pull_join", c_int, [c_vp]),
     ("gift_csr_row_bounds", c_int, [c_vp, c_vp, c_int, c_i64p]),
     ("gift_csr_attach_high_fanout", c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64p]),
     ("gift_csr_split_rows", c_int, [c_vp, c_vp, c_i64, c_i64, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),

@@ -37,6 +37,11 @@ void free_bank_graphs(Ctx* ctx);
 int64_t csr_attach_high_fanout(Ctx* ctx, Csr* c, int64_t n_nets, const int64_t* d_net_start, const int32_t* d_pin_cell,
                                int64_t cap);
 void csr_split_rows(Ctx* ctx, const Csr* c, int64_t r0, int64_t r1, Csr** local, Csr** ghost);
+void* peer_alloc(Ctx* ctx, size_t bytes, cudaIpcMemHandle_t* handle);
+void* peer_open(Ctx* ctx, const cudaIpcMemHandle_t& handle);
+void pull_rows_f32(Ctx* ctx, int64_t n, int F, const void* const* d_peers, const int32_t* d_src_rank,
+                   const int64_t* d_src_row, float* d_dst);
+void pull_join(Ctx* ctx);
 
 double quadratic_wirelength(Ctx* ctx, const Csr* c, const double* g);
 double hpwl(Ctx* ctx, int64_t n_nets, const int64_t* net_start, const int32_t* pin_cell, const double* pdx,
@@ -132,6 +137,8 @@ void set_option(Ctx* ctx, const std::string& name, int64_t v) {
   } else if (name == "col_bits") {
     if (v != 0 && (v < 11 || v > 14)) bad();
     o.col_bits = v;
+  } else if (name == "barrier_free" && v == 2) {
+    o.barrier_free = 2;  // also on tiles of <= 2048 rows at one 1024-thread CTA per SM
   } else if (name == "barrier_free" || name == "graphs" || name == "zero_copy" || name == "schedule" ||
              name == "fused" || name == "stream" || name == "balance") {
     if (v != 0 && v != 1) bad();
@@ -321,6 +328,12 @@ int gift_ctx_destroy(gift_ctx* ctx) {
   for (auto& kv : ctx->tile_ctr) cudaFree(kv.second);
   gift::free_bank_graphs(ctx);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  if (ctx->pull) {
+    cudaStreamSynchronize(ctx->pull);
+    cudaStreamDestroy(ctx->pull);
+    cudaEventDestroy(ctx->pull_fork);
+    cudaEventDestroy(ctx->pull_done);
+  }
   if (ctx->side) {
     cudaStreamSynchronize(ctx->side);
     cudaStreamDestroy(ctx->side);
@@ -612,6 +625,66 @@ int gift_gather_rows_f32(gift_ctx* ctx, int64_t n_idx, int F, const int64_t* d_i
   require(ctx, GIFT_ERR_VALUE, "null argument");
   ApiScope g(ctx, nullptr);
   gift::gather_rows_f32(ctx, n_idx, F, d_idx, d_src, d_dst);
+  GIFT_API_END
+}
+
+static_assert(sizeof(cudaIpcMemHandle_t) == GIFT_PEER_HANDLE_BYTES, "IPC handle size");
+
+int gift_peer_alloc(gift_ctx* ctx, int64_t bytes, void** d_ptr, unsigned char* h_handle) {
+  GIFT_API_BEGIN
+  require(ctx && d_ptr && bytes >= 0, GIFT_ERR_VALUE, "null argument");
+  ApiScope g(ctx, nullptr);
+  cudaIpcMemHandle_t h;
+  *d_ptr = gift::peer_alloc(ctx, (size_t)bytes, h_handle ? &h : nullptr);
+  if (h_handle) memcpy(h_handle, &h, sizeof(h));
+  GIFT_API_END
+}
+
+int gift_peer_open(gift_ctx* ctx, const unsigned char* h_handle, void** d_ptr) {
+  GIFT_API_BEGIN
+  require(ctx && d_ptr && h_handle, GIFT_ERR_VALUE, "null argument");
+  ApiScope g(ctx, nullptr);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, h_handle, sizeof(h));
+  *d_ptr = gift::peer_open(ctx, h);
+  GIFT_API_END
+}
+
+int gift_peer_close(gift_ctx* ctx, void* d_ptr) {
+  GIFT_API_BEGIN
+  require(ctx != nullptr, GIFT_ERR_VALUE, "null argument");
+  ApiScope g(ctx, nullptr);
+  if (d_ptr) GIFT_CUDA(cudaIpcCloseMemHandle(d_ptr));
+  GIFT_API_END
+}
+
+int gift_peer_free(gift_ctx* ctx, void* d_ptr) {
+  GIFT_API_BEGIN
+  require(ctx != nullptr, GIFT_ERR_VALUE, "null argument");
+  ApiScope g(ctx, nullptr);
+  if (d_ptr) {
+    GIFT_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->pull) GIFT_CUDA(cudaStreamSynchronize(ctx->pull));
+    GIFT_CUDA(cudaFree(d_ptr));
+  }
+  GIFT_API_END
+}
+
+int gift_pull_rows_f32(gift_ctx* ctx, int64_t n_rows, int F, const void* const* d_peers, const int32_t* d_src_rank,
+                       const int64_t* d_src_row, float* d_dst) {
+  GIFT_API_BEGIN
+  require(ctx != nullptr && n_rows >= 0, GIFT_ERR_VALUE, "null argument");
+  require(n_rows == 0 || (d_peers && d_src_rank && d_src_row && d_dst), GIFT_ERR_VALUE, "null argument");
+  ApiScope g(ctx, nullptr);
+  gift::pull_rows_f32(ctx, n_rows, F, d_peers, d_src_rank, d_src_row, d_dst);
+  GIFT_API_END
+}
+
+int gift_pull_join(gift_ctx* ctx) {
+  GIFT_API_BEGIN
+  require(ctx != nullptr, GIFT_ERR_VALUE, "null argument");
+  ApiScope g(ctx, nullptr);
+  gift::pull_join(ctx);
   GIFT_API_END
 }
 

@@ -65,6 +65,10 @@
 #ifndef GIFT_BMT_BULK
 #define GIFT_BMT_BULK 1
 #endif
+// segment hand-off pipelining in the barrier kernel (see FirstSlice)
+#ifndef GIFT_BMT_PRE
+#define GIFT_BMT_PRE 1
+#endif
 // threads per CTA of the F = 4 barrier kernel (compile-time; 768 leaves 85
 // registers per thread for a deeper record pipeline)
 #ifndef GIFT_BMT_THREADS4
@@ -699,32 +703,45 @@ __device__ __forceinline__ float4 weights(RecW<CODED> r, const float* tbl, int l
   }
 }
 
-// one slice (dynamic mode): lane = one row's run, summed in its (conflict-scheduled) order
+// D record steps in flight (the registers of the software pipeline)
+template <int D, bool CODED>
+struct RecPipe {
+  uint2 cq[D];
+  RecW<CODED> wq[D];
+};
+
+// first D record loads of a slice (cp / wp: the lane's column / weight slots of
+// the slice's first record)
+template <int D, bool CODED>
+__device__ __forceinline__ void pipe_issue(RecPipe<D, CODED>& p, const uint8_t* cp, const uint8_t* wp, int steps,
+                                           uint64_t pol_s) {
+  constexpr int RB = rec_bytes<CODED>();
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+    if (d < steps) {
+      p.cq[d] = ld_stream_v2u32(cp + d * RB, pol_s);
+      p.wq[d] = ld_w<CODED>(wp + d * RB, pol_s);
+    }
+}
+
+// the rest of the slice: lane = one row's run, summed in its (conflict-
+// scheduled) order, then added to the row's accumulator
 template <int FIN, int D, bool CODED>
-__device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int steps, int row, const float* zs,
-                                          float* accs, const float* tbl, int lane, uint64_t pol_s) {
+__device__ __forceinline__ void pipe_consume(RecPipe<D, CODED>& p, const uint8_t* cp, const uint8_t* wp, int steps,
+                                             int row, const float* zs, float* accs, const float* tbl, int lane,
+                                             uint64_t pol_s) {
   constexpr int RB = rec_bytes<CODED>();
   float acc[FIN];
 #pragma unroll
   for (int f = 0; f < FIN; ++f) acc[f] = 0.f;
-  const uint8_t* cp = b.data + (off / 128) * RB + 8 * lane;              // the lane's 4 columns
-  const uint8_t* wp = cp - 8 * lane + 256 + (CODED ? 4 : 16) * lane;     // its 4 weights / codes
-  uint2 cq[D];
-  RecW<CODED> wq[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d)
-    if (d < steps) {
-      cq[d] = ld_stream_v2u32(cp + d * RB, pol_s);
-      wq[d] = ld_w<CODED>(wp + d * RB, pol_s);
-    }
   int rem = steps;
   // steady state: D steps consumed, D reloaded, no predicates
   while (rem >= 2 * D) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      step_fma<FIN>(acc, cq[d], weights<CODED>(wq[d], tbl, lane), zs);
-      cq[d] = ld_stream_v2u32(cp + (d + D) * RB, pol_s);
-      wq[d] = ld_w<CODED>(wp + (d + D) * RB, pol_s);
+      step_fma<FIN>(acc, p.cq[d], weights<CODED>(p.wq[d], tbl, lane), zs);
+      p.cq[d] = ld_stream_v2u32(cp + (d + D) * RB, pol_s);
+      p.wq[d] = ld_w<CODED>(wp + (d + D) * RB, pol_s);
     }
     cp += D * RB;
     wp += D * RB;
@@ -734,20 +751,109 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int ste
   if (rem > D) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      step_fma<FIN>(acc, cq[d], weights<CODED>(wq[d], tbl, lane), zs);
+      step_fma<FIN>(acc, p.cq[d], weights<CODED>(p.wq[d], tbl, lane), zs);
       if (d + D < rem) {
-        cq[d] = ld_stream_v2u32(cp + (d + D) * RB, pol_s);
-        wq[d] = ld_w<CODED>(wp + (d + D) * RB, pol_s);
+        p.cq[d] = ld_stream_v2u32(cp + (d + D) * RB, pol_s);
+        p.wq[d] = ld_w<CODED>(wp + (d + D) * RB, pol_s);
       }
     }
     rem -= D;
   }
 #pragma unroll
   for (int d = 0; d < D; ++d)
-    if (d < rem) step_fma<FIN>(acc, cq[d], weights<CODED>(wq[d], tbl, lane), zs);
+    if (d < rem) step_fma<FIN>(acc, p.cq[d], weights<CODED>(p.wq[d], tbl, lane), zs);
   if (row != 0xffff) {
+    // one run per row per segment: no other lane touches this row now
+    if constexpr (FIN == 4) {
+      float4* ap = reinterpret_cast<float4*>(accs) + row;
+      float4 v = *ap;
+      v.x += acc[0]; v.y += acc[1]; v.z += acc[2]; v.w += acc[3];
+      *ap = v;
+    } else if constexpr (FIN == 2) {
+      float2* ap = reinterpret_cast<float2*>(accs) + row;
+      float2 v = *ap;
+      v.x += acc[0]; v.y += acc[1];
+      *ap = v;
+    } else {
 #pragma unroll
-    for (int f = 0; f < FIN; ++f) accs[row * FIN + f] += acc[f];
+      for (int f = 0; f < FIN; ++f) accs[row * FIN + f] += acc[f];
+    }
+  }
+}
+
+// one slice (dynamic mode)
+template <int FIN, int D, bool CODED>
+__device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int steps, int row, const float* zs,
+                                          float* accs, const float* tbl, int lane, uint64_t pol_s) {
+  constexpr int RB = rec_bytes<CODED>();
+  const uint8_t* cp = b.data + (off / 128) * RB + 8 * lane;              // the lane's 4 columns
+  const uint8_t* wp = cp - 8 * lane + 256 + (CODED ? 4 : 16) * lane;     // its 4 weights / codes
+  RecPipe<D, CODED> p;
+  pipe_issue<D, CODED>(p, cp, wp, steps, pol_s);
+  pipe_consume<FIN, D, CODED>(p, cp, wp, steps, row, zs, accs, tbl, lane, pol_s);
+}
+
+// Segment hand-off pipelining (the barrier kernel).  A warp's FIRST slice of a
+// segment is fixed (slice index = warp index; the shared counter hands out
+// the rest from kThreads / 32 on), so everything that slice needs from global
+// memory is requested while the segment's signal block is being staged:
+// right after the barrier that ends the previous segment the warp loads the
+// slice's metadata (offsets, the lanes' rows; the segment's slice range was
+// loaded a segment ahead) and issues its first D records; both latencies run
+// under the bulk copy of the block, which every warp has to wait for anyway.
+// Without this a segment started with three dependent memory latencies
+// AFTER the staging (slice range -> slice offsets -> records), ~2.5 us of the
+// ~12 us a config-4 segment takes.
+struct FirstSlice {
+  int64_t off = 0, end = 0;  // slot range (raw loads: converted where they are used)
+  int row = 0xffff;
+};
+
+__device__ __forceinline__ FirstSlice load_first(const BmtArgs& b, int sl0, int nsl, int warp, int lane) {
+  FirstSlice f;
+  if (warp < nsl) {
+    f.off = b.slice_off[sl0 + warp];
+    f.end = b.slice_off[sl0 + warp + 1];
+    f.row = b.slice_rows[(int64_t)(sl0 + warp) * 32 + lane];
+  }
+  return f;
+}
+
+// segment [sl0, sl0 + nsl) with the warp's first slice `first` already issued into p
+template <int FIN, int D, bool CODED>
+__device__ __forceinline__ void segment_slices_pre(const BmtArgs& b, int sl0, int nsl, int warp,
+                                                   const FirstSlice& first, RecPipe<D, CODED>& p, const float* zs,
+                                                   float* accs, int* ctr, const float* tbl, int lane,
+                                                   uint64_t pol_s) {
+  constexpr int RB = rec_bytes<CODED>();
+  auto grab = [&]() {
+    int j = 0;
+    if (lane == 0) j = atomicAdd(ctr, 1);
+    return __shfl_sync(0xffffffffu, j, 0);
+  };
+  if (warp >= nsl) return;
+  int64_t off = first.off, end = first.end;
+  int row = first.row;
+  bool pre = true;
+  for (;;) {
+    const int jn = grab();
+    int64_t off_n = 0, end_n = 0;
+    int row_n = 0xffff;
+    if (jn < nsl) {
+      off_n = b.slice_off[sl0 + jn];
+      end_n = b.slice_off[sl0 + jn + 1];
+      row_n = b.slice_rows[(int64_t)(sl0 + jn) * 32 + lane];
+    }
+    const int steps = (int)((end - off) / 128);
+    const uint8_t* cp = b.data + (off / 128) * RB + 8 * lane;
+    const uint8_t* wp = cp - 8 * lane + 256 + (CODED ? 4 : 16) * lane;
+    if (!pre) pipe_issue<D, CODED>(p, cp, wp, steps, pol_s);
+    pre = false;
+    pipe_consume<FIN, D, CODED>(p, cp, wp, steps, row, zs, accs, tbl, lane, pol_s);
+    if (jn >= nsl) break;
+    off = off_n;
+    end = end_n;
+    row = row_n;
   }
 }
 
@@ -1030,8 +1136,20 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
   }
   unsigned parity = 0;
   for (int i = tid; i < nrows * FIN; i += kThreads) accs[i] = 0.f;
-  const int64_t s_end = b.tile_seg[tile + 1];
-  for (int64_t s = b.tile_seg[tile]; s < s_end; ++s) {
+  const int64_t s_beg = b.tile_seg[tile], s_end = b.tile_seg[tile + 1];
+  constexpr int D = bmt_depth<FIN, kThreads>();
+  constexpr int RB = rec_bytes<CODED>();
+  constexpr bool kPre = !GIFT_BMT_STREAM && GIFT_BMT_PRE;
+  const int warp = tid >> 5;
+  // slice ranges of this segment [sl0, sl1), the next [sl1, sl2) and the one after
+  // (loaded a segment ahead of the addresses they feed)
+  int sl0 = 0, sl1 = 0, sl2 = 0;
+  if (kPre && s_beg < s_end) {
+    sl0 = (int)b.seg_slice[s_beg];
+    sl1 = (int)b.seg_slice[s_beg + 1];
+    sl2 = s_beg + 2 <= s_end ? (int)b.seg_slice[s_beg + 2] : sl1;
+  }
+  for (int64_t s = s_beg; s < s_end; ++s) {
     const int64_t cbase = (int64_t)b.seg_code[s] * kC;
     const float* zg = a.zin + cbase * FIN;
     // finish the previous segment: its lanes may still read zs and update the
@@ -1049,14 +1167,35 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
       for (int i = tid; i < nv; i += kThreads) dst[i] = src[i];
       for (int i = nv * 4 + tid; i < nf; i += kThreads) zs[i] = zg[i];
     }
+    // the warp's first slice: metadata, then its first records, in flight
+    // while the block is staged
+    RecPipe<D, CODED> pipe;
+    FirstSlice cur;
+    int sl3 = sl2;
+    if constexpr (kPre) {
+      cur = load_first(b, sl0, sl1 - sl0, warp, lane);
+      if (s + 3 <= s_end) sl3 = (int)b.seg_slice[s + 3];
+      if (warp < sl1 - sl0) {
+        const uint8_t* cp = b.data + (cur.off / 128) * RB + 8 * lane;
+        pipe_issue<D, CODED>(pipe, cp, cp - 8 * lane + 256 + (CODED ? 4 : 16) * lane, (int)((cur.end - cur.off) / 128),
+                             pol_s);
+      }
+    }
     for (int i = nf + tid; i < (kC + kPadRows) * FIN; i += kThreads) zs[i] = 0.f;  // short block + padding rows
-    if (tid == 0) slice_ctr = 0;
+    if (tid == 0) slice_ctr = kPre ? kThreads / 32 : 0;
     __syncthreads();
     if (bulk) {
       mbar_wait(&full, parity);
       parity ^= 1u;
     }
-    segment_run<FIN, bmt_depth<FIN, kThreads>(), CODED>(b, s, zs, accs, &slice_ctr, tbl, lane, pol_s);
+    if constexpr (kPre) {
+      segment_slices_pre<FIN, D, CODED>(b, sl0, sl1 - sl0, warp, cur, pipe, zs, accs, &slice_ctr, tbl, lane, pol_s);
+      sl0 = sl1;
+      sl1 = sl2;
+      sl2 = sl3;
+    } else {
+      segment_run<FIN, D, CODED>(b, s, zs, accs, &slice_ctr, tbl, lane, pol_s);
+    }
   }
   bmt_tile_finish<FIN, FOUT, kThreads>(a, b, tile, r0, nrows, accs, tid, lane, pol_z);
 }
@@ -1335,7 +1474,7 @@ void launch_bmt(Ctx* ctx, const HopArgs& a, const BmtArgs& b, int64_t ntiles) {
       return;
     }
 #endif
-    if (b.tile_rows > 2048 && nb + fixed <= 228 * 1024) {
+    if ((b.tile_rows > 2048 || ctx->opt.barrier_free > 1) && nb + fixed <= 228 * 1024) {
       launch_bmt_nb<FIN, FOUT, 1024, CODED>(ctx, a, b, ntiles, nb);
       return;
     }

@@ -48,6 +48,10 @@ struct Ctx {
   cudaStream_t stream = 0;
   cudaStream_t side = nullptr;    // forked work (BMT wide rows), joined back with events
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  // ghost-row pull from peer memory (peer.cu): its own forked stream
+  cudaStream_t pull = nullptr;
+  cudaEvent_t pull_fork = nullptr, pull_done = nullptr;
+  bool pull_pending = false;
   int64_t launches = 0;
   int num_sms = 148;
   int smem_optin = 0;             // max dynamic shared memory per block (opt-in), this device

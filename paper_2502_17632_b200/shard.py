@@ -8,12 +8,17 @@ netlists with index locality (every net inside a +-W window) the ghosts are a
 everywhere.
 
 Per hop, each rank
-  1. packs the rows other ranks asked for (gift_gather_rows_f32),
-  2. starts an all-to-all of those rows (NCCL over NVLink; async),
-  3. runs the LOCAL part of the hop (columns it owns) -> partial row sums,
-  4. waits for the exchange (stream-ordered; the host never blocks),
-  5. runs the GHOST part (columns owned elsewhere) plus the epilogue.
-Steps 2 and 3 overlap.  The bank schedule (chain packing, term accumulation,
+  1. gets its ghost rows moving:
+     * PeerExchange (NVLink peer memory, the default on GPUs): a stream-ordered
+       barrier, then ONE kernel of peer loads pulls the ghost rows straight
+       out of the owners' signal buffers (CUDA IPC mappings, csrc/peer.cu) on
+       a forked stream -- no pack kernel, no staging, no collective;
+     * TorchExchange (NCCL / gloo): packs the rows other ranks asked for
+       (gift_gather_rows_f32) and starts an async all_to_all_single;
+  2. runs the LOCAL part of the hop (columns it owns) -> partial row sums,
+     overlapping the transfer,
+  3. waits for the transfer (stream-ordered; the host never blocks),
+  4. runs the GHOST part (columns owned elsewhere) plus the epilogue.  The bank schedule (chain packing, term accumulation,
 fused re-pin/clamp) is `plan_bank`, the host mirror of bank_fp32 in
 csrc/filter.cu; the numeric kernels are the same k_hop instances.
 
@@ -297,6 +302,196 @@ class _ThreadRankExchange:
         return None
 
 
+class _DevArray:
+    """A raw device allocation as a __cuda_array_interface__ object (torch
+    wraps it without a copy)."""
+
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4", "data": (int(ptr), False),
+                                         "version": 2, "strides": None}
+
+
+class _PullWork:
+    def __init__(self, be):
+        self.be = be
+
+    def wait(self):
+        self.be.pull_join()
+
+
+class PeerExchange:
+    """Ghost rows over NVLink peer memory (csrc/peer.cu), one process per GPU.
+
+    Each rank's two signal buffers are plain device allocations published by
+    CUDA IPC handle; every rank opens its peers' buffers once.  Per hop:
+    `barrier()` (every rank has written the rows others will read, and has
+    finished reading what is about to be overwritten), then `pull()` copies
+    the ghost rows with peer loads on a forked stream while the local part of
+    the hop runs.  The barrier is stream-ordered on NCCL groups (a one-element
+    all_reduce: the host never blocks); on a gloo control group (tests: two
+    processes sharing one GPU) it is a device synchronise + host barrier.
+
+    Setup traffic (ghost ids, IPC handles) goes through torch.distributed."""
+
+    pull_mode = True
+
+    def __init__(self, group=None, device="cuda:0"):
+        import torch.distributed as dist
+
+        self.group = group
+        self.device = device
+        self.plan = None
+        self.nccl = dist.get_backend(group) == "nccl"
+        self._ids = TorchExchange(group=group, device=device if self.nccl else "cpu")
+        self._flag = None
+        self._own: list[int] = []
+        self._opened: list[int] = []
+        self._keep: list = []
+        self.tables: list = []
+
+    def ids(self, requests):
+        return self._ids.ids(requests)
+
+    # -- setup: allocate, publish, open, build the pull tables
+    def alloc_signal(self, be, rows: int, plan: ShardPlan):
+        import torch
+        import torch.distributed as dist
+
+        lib, _lib = be.lib, be._lib
+        ctx = be.ctx()
+        world, rank = plan.world, plan.rank
+        nbytes = max(rows, 1) * 4 * 4
+        bufs, handles, err = [], [], None
+        try:
+            for _ in range(2):
+                ptr = ctypes.c_void_p()
+                h = (ctypes.c_ubyte * 64)()
+                _lib.check(lib.gift_peer_alloc(ctx, nbytes, ctypes.byref(ptr), ctypes.cast(h, ctypes.c_void_p)))
+                self._own.append(ptr.value)
+                handles.append(bytes(h))
+                holder = _DevArray(ptr.value, (max(rows, 1), 4))
+                self._keep.append(holder)
+                bufs.append(torch.as_tensor(holder, device=self.device))
+        except Exception as e:  # keep the collective below matched on every rank
+            handles, err = None, e
+        everyone = [None] * world
+        dist.all_gather_object(everyone, handles, group=self.group)
+        if any(h is None for h in everyone):
+            raise RuntimeError(f"peer memory unavailable on rank(s) "
+                               f"{[q for q, h in enumerate(everyone) if h is None]}: {err!r}")
+        for which in range(2):
+            ptrs = np.zeros(world, dtype=np.int64)
+            for q in range(world):
+                if q == rank:
+                    ptrs[q] = self._own[which]
+                elif plan.recv_counts[q] > 0:  # map only the ranks this one reads from
+                    p = ctypes.c_void_p()
+                    hb = (ctypes.c_ubyte * 64).from_buffer_copy(everyone[q][which])
+                    _lib.check(lib.gift_peer_open(ctx, ctypes.cast(hb, ctypes.c_void_p), ctypes.byref(p)))
+                    self._opened.append(p.value)
+                    ptrs[q] = p.value
+            self.tables.append(be.upload(ptrs))
+        self._finish_tables(be, plan)
+        self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        return bufs[0], bufs[1]
+
+    def _finish_tables(self, be, plan: ShardPlan):
+        owner = np.searchsorted(plan.bounds, plan.ghosts, side="right") - 1
+        self.src_rank = be.upload(owner.astype(np.int32))
+        self.src_row = be.upload((plan.ghosts - plan.bounds[owner]).astype(np.int64))
+
+    def barrier(self):
+        import torch
+        import torch.distributed as dist
+
+        if self.plan is not None and self.plan.world == 1:
+            return
+        if self.nccl:
+            dist.all_reduce(self._flag, group=self.group)  # ordered on the current stream
+        else:
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+
+    def pull(self, be, which: int, F: int, dst):
+        be.pull(self.plan.n_ghost, F, self.tables[which], self.src_rank, self.src_row, dst)
+        return _PullWork(be)
+
+    def close(self, be):
+        """Unmap the peers' buffers and free this rank's (collective)."""
+        lib, _lib = be.lib, be._lib
+        self.barrier()
+        if self.nccl:
+            be.torch.cuda.synchronize()
+        for p in self._opened:
+            _lib.check(lib.gift_peer_close(be.ctx(), ctypes.c_void_p(p)))
+        self._opened = []
+        self.barrier()
+        if self.nccl:
+            be.torch.cuda.synchronize()
+        for p in self._own:
+            _lib.check(lib.gift_peer_free(be.ctx(), ctypes.c_void_p(p)))
+        self._own = []
+
+
+class ThreadPeerExchange:
+    """PeerExchange for P virtual ranks as threads of one process on one GPU
+    (tests): the "peers" are allocations of the same process, shared by
+    pointer instead of IPC handle (a process cannot open its own handles),
+    and the barrier is a host barrier -- every thread enqueues on the same
+    stream, so work enqueued after the barrier runs after what the other
+    ranks enqueued before it; no kernel ever waits on another."""
+
+    def __init__(self, world: int):
+        import threading
+
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.box: dict = {}
+
+    def for_rank(self, rank: int):
+        return _ThreadPeerRank(self, rank)
+
+
+class _ThreadPeerRank(PeerExchange):
+    def __init__(self, hub: ThreadPeerExchange, rank: int):
+        self.hub, self.rank, self.plan = hub, rank, None
+        self.device = "cuda:0"
+        self._own, self._opened, self._keep, self.tables = [], [], [], []
+
+    def ids(self, requests):
+        return _ThreadRankExchange.ids(self, requests)
+
+    def alloc_signal(self, be, rows: int, plan: ShardPlan):
+        import torch
+
+        lib, _lib = be.lib, be._lib
+        bufs = []
+        for _ in range(2):
+            ptr = ctypes.c_void_p()
+            _lib.check(lib.gift_peer_alloc(be.ctx(), max(rows, 1) * 16, ctypes.byref(ptr), None))
+            self._own.append(ptr.value)
+            holder = _DevArray(ptr.value, (max(rows, 1), 4))
+            self._keep.append(holder)
+            bufs.append(torch.as_tensor(holder, device=self.device))
+        self.hub.box[("ptrs", self.rank)] = list(self._own)
+        self.hub.barrier.wait()
+        for which in range(2):
+            ptrs = np.array([self.hub.box[("ptrs", q)][which] for q in range(plan.world)], dtype=np.int64)
+            self.tables.append(be.upload(ptrs))
+        self._finish_tables(be, plan)
+        return bufs[0], bufs[1]
+
+    def barrier(self):
+        self.hub.barrier.wait()
+
+    def close(self, be):
+        be.torch.cuda.synchronize()
+        self.hub.barrier.wait()
+        for p in self._own:
+            be._lib.check(be.lib.gift_peer_free(be.ctx(), ctypes.c_void_p(p)))
+        self._own = []
+
+
 # ------------------------------------------------------------------ backends
 
 
@@ -336,6 +531,14 @@ class CudaBackend:
     def hop(self, block, desc: dict):
         d = _hop_desc(desc)
         self._lib.check(self.lib.gift_hop_fp32(self.ctx(), block.h, ctypes.addressof(d)))
+
+    def pull(self, n_rows, F, peers, src_rank, src_row, dst):
+        self._lib.check(self.lib.gift_pull_rows_f32(self.ctx(), n_rows, F, self._lib.dptr(peers),
+                                                    self._lib.dptr(src_rank), self._lib.dptr(src_row),
+                                                    self._lib.dptr(dst)))
+
+    def pull_join(self):
+        self._lib.check(self.lib.gift_pull_join(self.ctx()))
 
 
 class _Handle:
@@ -409,8 +612,12 @@ class ShardedFilter:
         self.local = local
         self.ghost = ghost
         n, ng = plan.n_local, plan.n_ghost
-        self.zA = backend.empty(n + ng, 4)
-        self.zB = backend.empty(n + ng, 4)
+        self.pull_mode = bool(getattr(exchange, "pull_mode", False))
+        if self.pull_mode:  # signal buffers the other ranks read through peer mappings
+            self.zA, self.zB = exchange.alloc_signal(backend, n + ng, plan)
+        else:
+            self.zA = backend.empty(n + ng, 4)
+            self.zB = backend.empty(n + ng, 4)
         self.acc = backend.empty(n, 4)
         self.part = backend.empty(n, 4)
         self.sendbuf = backend.empty(len(plan.send_rows), 4)
@@ -431,6 +638,13 @@ class ShardedFilter:
         p = self.plan
         n, ng = p.n_local, p.n_ghost
         flat = z.view(-1)
+        if self.pull_mode:
+            # every rank's rows of z are complete (and nobody still reads the
+            # buffer this hop will overwrite): pull the ghosts from the owners
+            self.ex.barrier()
+            if ng == 0:
+                return None
+            return self.ex.pull(self.be, 0 if z is self.zA else 1, F, flat[n * F: (n + ng) * F])
         send = self.sendbuf.view(-1)[: len(p.send_rows) * F]
         if len(p.send_rows):
             self.be.gather(self.send_idx, F, flat, send)
@@ -449,6 +663,8 @@ class ShardedFilter:
         for st in bank.steps:
             if isinstance(st, PackStep):
                 F = st.F
+                if self.pull_mode:  # a slow peer may still pull its last ghosts of the previous bank from zA
+                    self.ex.barrier()
                 self.be.pack(n, st.wcols, [self.s_of(bank.sigmas[j]) for j in st.groups], g, ncols, st.c0, F,
                              self.zA.view(-1))
                 zin, zout = self.zA, self.zB

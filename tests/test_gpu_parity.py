@@ -467,14 +467,19 @@ def _flat(nets):
 
 # ---------------------------------------------------------- sharded path --
 
-@pytest.mark.parametrize("world,tiled", [(2, False), (4, False), (2, True), (3, True)])
-def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, opts, world, tiled):
+@pytest.mark.parametrize("world,tiled,mode", [(2, False, "a2a"), (4, False, "a2a"), (2, True, "a2a"),
+                                              (3, True, "a2a"), (2, False, "pull"), (4, False, "pull"),
+                                              (3, True, "pull")])
+def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, opts, world, tiled, mode):
     """The multi-GPU code path (partition, ghost pack, split local/ghost hops,
     fused epilogue) with `world` virtual ranks as threads on one device; the
     all-to-all is replaced by stream-ordered device copies (ThreadExchange),
     so no kernel ever waits on another.  `tiled`: the local blocks take the
     block-major tiled hop (forced below its size threshold), writing partial
-    sums that the ghost hop completes."""
+    sums that the ghost hop completes.  mode "pull": the ghost rows come
+    through the peer-memory path (csrc/peer.cu: gift_pull_rows_f32 reading the
+    owners' signal buffers by pointer on a forked stream, per-hop barriers);
+    two banks back to back on the same buffers must agree bit for bit."""
     import threading
 
     import torch
@@ -488,7 +493,7 @@ def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, opts, world, tiled)
     fd = synth.generate("c2", seed=4, scale=0.02, window=600)
     adj = gb.build_clique_graph(fd, max_clique_pins=200)
     g32 = synth.signal_fp32(fd, seed=2)
-    hub = shard.ThreadExchange(world)
+    hub = shard.ThreadExchange(world) if mode == "a2a" else shard.ThreadPeerExchange(world)
     blocks = [None] * world
     errors = []
 
@@ -502,8 +507,14 @@ def test_sharded_path_on_one_gpu_matches_single_gpu(gb, orc, opts, world, tiled)
             mask = torch.from_numpy(fd.fixed_mask()[r0:r1].astype(np.uint8)).cuda()
             pos = torch.from_numpy(np.nan_to_num(fd.fixed_positions()[r0:r1], nan=0.0)).cuda()
             sf.run(g, gb.DEFAULT_TERMS, out, fixed_mask=mask, fixed_pos=pos, region=fd.region.bounds())
+            if mode == "pull":
+                first = out.clone()
+                sf.run(g, gb.DEFAULT_TERMS, out, fixed_mask=mask, fixed_pos=pos, region=fd.region.bounds())
+                assert torch.equal(first, out)
             torch.cuda.synchronize()
             blocks[rank] = (r0, out.cpu().numpy(), sf.plan.n_ghost)
+            if mode == "pull":
+                sf.ex.close(sf.be)
         except Exception as e:  # surfaced below
             errors.append(repr(e))
             hub.barrier.abort()

@@ -53,6 +53,17 @@ class NumpyBackend:
         s = src.numpy().reshape(-1, F)
         dst.numpy()[: len(idx) * F] = s[idx.numpy()].reshape(-1)
 
+    def pull(self, n_rows, F, peers, src_rank, src_row, dst):
+        """gift_pull_rows_f32 (csrc/peer.cu): dst[i] = peers[src_rank[i]][src_row[i]], rows of F floats."""
+        rk, rw = src_rank.numpy(), src_row.numpy()
+        d = dst.numpy()[: n_rows * F].reshape(n_rows, F)
+        for q in np.unique(rk):
+            sel = rk == q
+            d[sel] = np.asarray(peers[q]).reshape(-1)[: (len(peers[q].reshape(-1)) // F) * F].reshape(-1, F)[rw[sel]]
+
+    def pull_join(self):
+        pass
+
     def hop(self, A, d):
         n, fin = d["row_end"], d["fin"]
         zin = d["zin"].numpy().reshape(-1, fin)
@@ -100,13 +111,53 @@ class NumpyBackend:
         out[:, d["out_c0"]:d["out_c0"] + wcols] = v
 
 
+class MemmapPeerExchange(shard.PeerExchange):
+    """CPU stand-in for NVLink peer memory: every rank's two signal buffers
+    are files mapped by all ranks (one-sided reads, like CUDA IPC mappings);
+    the per-hop barrier is a gloo barrier.  Runs PeerExchange's own schedule
+    (barrier placement, pull tables) with the numpy backend."""
+
+    def __init__(self, tmpdir):
+        self.tmpdir = tmpdir
+        self.plan = None
+        self._ids = shard.TorchExchange(device="cpu")
+        self.tables = []
+        self.barriers = 0
+
+    def alloc_signal(self, be, rows, plan):
+        import torch
+        import torch.distributed as dist
+
+        rows = max(rows, 1)
+        sizes = [None] * plan.world
+        dist.all_gather_object(sizes, rows)
+        mine = [np.lib.format.open_memmap(os.path.join(self.tmpdir, f"z{w}_{plan.rank}.npy"), mode="w+",
+                                          dtype=np.float32, shape=(rows, 4)) for w in range(2)]
+        for m in mine:
+            m[:] = 0
+            m.flush()
+        dist.barrier()
+        for w in range(2):
+            self.tables.append([mine[w] if q == plan.rank else
+                                np.lib.format.open_memmap(os.path.join(self.tmpdir, f"z{w}_{q}.npy"), mode="r")
+                                for q in range(plan.world)])
+        self._finish_tables(be, plan)
+        return torch.from_numpy(mine[0]), torch.from_numpy(mine[1])
+
+    def barrier(self):
+        import torch.distributed as dist
+
+        self.barriers += 1
+        dist.barrier()
+
+
 def _free_port() -> int:
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, results, scale, window):
+def _worker(rank, world, port, results, scale, window, mode="a2a", tmpdir=None):
     import torch
     import torch.distributed as dist
 
@@ -120,7 +171,7 @@ def _worker(rank, world, port, results, scale, window):
         fd = synth.generate("c2", seed=3, scale=scale, window=window)
         A = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, 200)
         deg = orc.degrees(A)
-        ex = shard.TorchExchange(device="cpu")
+        ex = shard.TorchExchange(device="cpu") if mode == "a2a" else MemmapPeerExchange(tmpdir)
         bounds = shard.nnz_balanced_bounds(A.indptr, world)
         ghosts, loc, gh = shard.split_block(A.indptr, A.indices, int(bounds[rank]), int(bounds[rank + 1]))
         plan = shard.exchange_plan(bounds, rank, ghosts, ex.ids)
@@ -135,6 +186,11 @@ def _worker(rank, world, port, results, scale, window):
         mask = torch.from_numpy(fd.fixed_mask()[r0:r1].astype(np.uint8))
         pos = torch.from_numpy(np.nan_to_num(fd.fixed_positions()[r0:r1], nan=0.0))
         sf.run(g, DEFAULT, out, fixed_mask=mask, fixed_pos=pos, region=fd.region.bounds())
+        if mode == "pull":  # a second bank on the same buffers (the barrier before the pack protects them)
+            first = out.clone()
+            sf.run(g, DEFAULT, out, fixed_mask=mask, fixed_pos=pos, region=fd.region.bounds())
+            assert torch.equal(first, out)
+            assert ex.barriers == 2 * (1 + 4)  # one per pack, one per hop of the 4-pass default bank
         # plan invariants
         inv = {
             "recv": int(sum(plan.recv_counts)) == plan.n_ghost,
@@ -161,14 +217,18 @@ def _worker(rank, world, port, results, scale, window):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_bank_over_gloo_matches_oracle(world):
+@pytest.mark.parametrize("world,mode", [(2, "a2a"), (3, "a2a"), (2, "pull"), (3, "pull")])
+def test_sharded_bank_over_gloo_matches_oracle(world, mode, tmp_path):
+    """mode "a2a": packed rows through all_to_all_single (TorchExchange);
+    mode "pull": one-sided reads of the owners' buffers between per-hop
+    barriers (PeerExchange's schedule; mapped files stand in for peer memory)."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, 0.01, 300)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, 0.01, 300, mode, str(tmp_path)))
+             for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:

@@ -12,14 +12,14 @@ cd "$(dirname "$0")/.."
 mkdir -p _variants/obj
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wno-deprecated-declarations -DGIFT_TUNING"
 S=paper_2502_17632_b200/csrc
-for f in abi build filter metrics plio bookshelf shard hf; do
+for f in abi build filter metrics plio bookshelf shard hf peer; do
   [ _variants/obj/$f.o -nt $S/$f.cu ] && [ _variants/obj/$f.o -nt $S/common.cuh ] || nvcc $F -c $S/$f.cu -o _variants/obj/$f.o &
 done
 wait
 for spec in "$@"; do
   name=${spec%%:*}; defs=${spec#*:}
   ( nvcc $F $defs -c $S/bmt.cu -o _variants/obj/bmt_$name.o &&
-    nvcc -gencode arch=compute_100a,code=sm_100a -shared -o _variants/lib_$name.so _variants/obj/{abi,build,filter,metrics,plio,bookshelf,shard,hf}.o _variants/obj/bmt_$name.o &&
+    nvcc -gencode arch=compute_100a,code=sm_100a -shared -o _variants/lib_$name.so _variants/obj/{abi,build,filter,metrics,plio,bookshelf,shard,hf,peer}.o _variants/obj/bmt_$name.o &&
     echo "built _variants/lib_$name.so" ) &
 done
 wait
