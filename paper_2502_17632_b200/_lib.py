@@ -93,6 +93,7 @@ SIGNATURES = [
     ("gift_pull_join", c_int, [c_vp]),
     ("gift_csr_row_bounds", c_int, [c_vp, c_vp, c_int, c_i64p]),
     ("gift_csr_attach_high_fanout", c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64p]),
+    ("gift_csr_attach_implicit_nets", c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64p]),
     ("gift_csr_split_rows", c_int, [c_vp, c_vp, c_i64, c_i64, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
     ("gift_csr_ext_ids", c_int, [c_vp, ctypes.POINTER(c_vp), c_i64p]),
     # placement metrics (metrics.py)

@@ -35,7 +35,7 @@ Csr* csr_from_arrays(Ctx* ctx, int64_t n_rows, int64_t nnz, const int64_t* d_ind
 void csr_row_bounds(Ctx* ctx, const Csr* c, int world, int64_t* h_bounds);
 void free_bank_graphs(Ctx* ctx);
 int64_t csr_attach_high_fanout(Ctx* ctx, Csr* c, int64_t n_nets, const int64_t* d_net_start, const int32_t* d_pin_cell,
-                               int64_t cap);
+                               int64_t cap, int64_t upto);
 void csr_split_rows(Ctx* ctx, const Csr* c, int64_t r0, int64_t r1, Csr** local, Csr** ghost);
 void* peer_alloc(Ctx* ctx, size_t bytes, cudaIpcMemHandle_t* handle);
 void* peer_open(Ctx* ctx, const cudaIpcMemHandle_t& handle);
@@ -754,7 +754,18 @@ int gift_csr_attach_high_fanout(gift_ctx* ctx, gift_csr* csr, int64_t n_nets, co
   GIFT_API_BEGIN
   require(ctx && csr && d_net_start, GIFT_ERR_VALUE, "null argument");
   ApiScope g(ctx, csr);
-  const int64_t k = gift::csr_attach_high_fanout(ctx, csr, n_nets, d_net_start, d_pin_cell, max_clique_pins);
+  const int64_t k = gift::csr_attach_high_fanout(ctx, csr, n_nets, d_net_start, d_pin_cell, max_clique_pins, -1);
+  if (n_implicit) *n_implicit = k;
+  GIFT_API_END
+}
+
+int gift_csr_attach_implicit_nets(gift_ctx* ctx, gift_csr* csr, int64_t n_nets, const int64_t* d_net_start,
+                                  const int32_t* d_pin_cell, int64_t above, int64_t upto, int64_t* n_implicit) {
+  GIFT_API_BEGIN
+  require(ctx && csr && d_net_start, GIFT_ERR_VALUE, "null argument");
+  require(above >= 1 && (upto < 0 || upto >= above), GIFT_ERR_VALUE, "implicit nets: need 1 <= above <= upto");
+  ApiScope g(ctx, csr);
+  const int64_t k = gift::csr_attach_high_fanout(ctx, csr, n_nets, d_net_start, d_pin_cell, above, upto);
   if (n_implicit) *n_implicit = k;
   GIFT_API_END
 }

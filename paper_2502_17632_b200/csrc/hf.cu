@@ -32,11 +32,11 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int kNetBlock = 256;
 
-__global__ void k_hf_flags(int64_t n_nets, const int64_t* __restrict__ net_start, int64_t cap,
+__global__ void k_hf_flags(int64_t n_nets, const int64_t* __restrict__ net_start, int64_t cap, int64_t upto,
                            uint8_t* __restrict__ flag, int64_t* __restrict__ cnt) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_nets; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = net_start[e + 1] - net_start[e];
-    const bool hf = m >= 2 && m > cap;
+    const bool hf = m >= 2 && m > cap && (upto < 0 || m <= upto);
     flag[e] = hf;
     cnt[e] = hf ? m : 0;
   }
@@ -168,6 +168,38 @@ __global__ void __launch_bounds__(kNetBlock) k_hf_tsum(int64_t nh, const int64_t
   }
 }
 
+// the same sums with one WARP per net (graphs whose implicit nets are many and
+// short -- the factored clique model keeps every net above a few pins
+// implicit): lanes stride the net's pins, fixed xor-butterfly, lane f writes
+template <typename T, int F, bool S>
+__global__ void __launch_bounds__(kBlock) k_hf_tsum_warp(int64_t nh, const int64_t* __restrict__ hstart,
+                                                         const int32_t* __restrict__ hpin, const T* __restrict__ z,
+                                                         int64_t ld, int64_t c0, const double* __restrict__ s,
+                                                         double* __restrict__ t) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t h = warp0; h < nh; h += nwarps) {
+    double acc[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) acc[f] = 0.0;
+    const int64_t a = hstart[h], b = hstart[h + 1];
+    for (int64_t p = a + lane; p < b; p += 32) {
+      const int64_t c = hpin[p];
+      const double sc = S ? s[c] : 1.0;
+#pragma unroll
+      for (int f = 0; f < F; ++f) acc[f] += sc * (double)z[c * ld + c0 + f];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int f = 0; f < F; ++f) acc[f] += __shfl_xor_sync(0xffffffffu, acc[f], off);
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+      if (lane == f) t[h * F + f] = acc[f];
+  }
+}
+
 // out[cell] (F values) = sum over occurrences of (2/m)(t_e - b u_cell), in net order
 template <typename T, int F, bool S>
 __global__ void k_hf_apply(int64_t nc, const int32_t* __restrict__ cell, const int64_t* __restrict__ occ_ptr,
@@ -203,39 +235,37 @@ void hf_apply_t(Ctx* ctx, const Csr* c, int F, const T* z, int64_t ld, int64_t c
   double* t = static_cast<double*>(H.tbuf);
   const unsigned gn = (unsigned)std::min<int64_t>(H.nets, 65535);
   const unsigned gc = grid_for(H.cells, kBlock);
+  // one warp per net unless the nets are few and long (a fixed choice per
+  // graph: the two kernels sum in different orders)
+  const bool warp_nets = H.pins < 512 * H.nets;
+  const unsigned gw = grid_for(H.nets * 32, kBlock, 1LL << 30);
+#define GIFT_HF_CASE(FF)                                                                                         \
+  if (warp_nets)                                                                                                   \
+    k_hf_tsum_warp<T, FF, S><<<gw, kBlock, 0, st>>>(H.nets, H.net_start, H.pin_cell, z, ld, c0, s, t);            \
+  else                                                                                                             \
+    k_hf_tsum<T, FF, S><<<gn, kNetBlock, 0, st>>>(H.nets, H.net_start, H.pin_cell, z, ld, c0, s, t);              \
+  k_hf_apply<T, FF, S><<<gc, kBlock, 0, st>>>(H.cells, H.cell, H.occ_ptr, H.occ_net, H.occ_b, H.coef, t, z, ld, c0, \
+                                              s, out, ldo);
   switch (F) {
-    case 1:
-      k_hf_tsum<T, 1, S><<<gn, kNetBlock, 0, st>>>(H.nets, H.net_start, H.pin_cell, z, ld, c0, s, t);
-      k_hf_apply<T, 1, S><<<gc, kBlock, 0, st>>>(H.cells, H.cell, H.occ_ptr, H.occ_net, H.occ_b, H.coef, t, z, ld, c0,
-                                                 s, out, ldo);
-      break;
-    case 2:
-      k_hf_tsum<T, 2, S><<<gn, kNetBlock, 0, st>>>(H.nets, H.net_start, H.pin_cell, z, ld, c0, s, t);
-      k_hf_apply<T, 2, S><<<gc, kBlock, 0, st>>>(H.cells, H.cell, H.occ_ptr, H.occ_net, H.occ_b, H.coef, t, z, ld, c0,
-                                                 s, out, ldo);
-      break;
-    case 3:
-      k_hf_tsum<T, 3, S><<<gn, kNetBlock, 0, st>>>(H.nets, H.net_start, H.pin_cell, z, ld, c0, s, t);
-      k_hf_apply<T, 3, S><<<gc, kBlock, 0, st>>>(H.cells, H.cell, H.occ_ptr, H.occ_net, H.occ_b, H.coef, t, z, ld, c0,
-                                                 s, out, ldo);
-      break;
-    default:
-      k_hf_tsum<T, 4, S><<<gn, kNetBlock, 0, st>>>(H.nets, H.net_start, H.pin_cell, z, ld, c0, s, t);
-      k_hf_apply<T, 4, S><<<gc, kBlock, 0, st>>>(H.cells, H.cell, H.occ_ptr, H.occ_net, H.occ_b, H.coef, t, z, ld, c0,
-                                                 s, out, ldo);
-      break;
+    case 1: GIFT_HF_CASE(1) break;
+    case 2: GIFT_HF_CASE(2) break;
+    case 3: GIFT_HF_CASE(3) break;
+    default: GIFT_HF_CASE(4) break;
   }
+#undef GIFT_HF_CASE
   GIFT_LAUNCH_CHECK(ctx);
   ctx->launches++;
 }
 
 }  // namespace
 
-// Attach the implicit term of the nets with more than `cap` pins to c (a
-// graph built from the same netlist with that cap).  Must run before any
-// derived state (degrees, s_sigma) exists: those then include the term.
+// Attach the implicit term of the nets with more than `cap` pins -- and, when
+// upto >= 0, at most `upto` pins (larger ones stay dropped, like the
+// reference's max_clique_pins skip) -- to c, a graph built from the same
+// netlist with that cap.  Must run before any derived state (degrees,
+// s_sigma) exists: those then include the term.
 int64_t csr_attach_high_fanout(Ctx* ctx, Csr* c, int64_t n_nets, const int64_t* d_net_start,
-                               const int32_t* d_pin_cell, int64_t cap) {
+                               const int32_t* d_pin_cell, int64_t cap, int64_t upto) {
   if (cap < 0) throw_error(GIFT_ERR_VALUE, "high-fanout term needs a cap (max_clique_pins >= 0)");
   if (c->hf.nets) throw_error(GIFT_ERR_VALUE, "graph already has a high-fanout term");
   if (c->degrees || !c->s64.empty() || c->bmt.ready || c->bmt_wide.ready)
@@ -244,7 +274,7 @@ int64_t csr_attach_high_fanout(Ctx* ctx, Csr* c, int64_t n_nets, const int64_t* 
   cudaStream_t st = ctx->stream;
   DevBuf<uint8_t> flag(ctx, n_nets);
   DevBuf<int64_t> cnt(ctx, n_nets + 1), ids(ctx, n_nets + 1), nsel(ctx, 1);
-  k_hf_flags<<<grid_for(n_nets, kBlock), kBlock, 0, st>>>(n_nets, d_net_start, cap, flag.p, cnt.p);
+  k_hf_flags<<<grid_for(n_nets, kBlock), kBlock, 0, st>>>(n_nets, d_net_start, cap, upto, flag.p, cnt.p);
   GIFT_LAUNCH_CHECK(ctx);
   {
     thrust::counting_iterator<int64_t> it(0);

@@ -248,7 +248,8 @@ def from_coo(n: int, rows, cols, vals) -> SparseSymMatrix:
     return SparseSymMatrix._from_handle(_coo_handle(n, rows, cols, vals, True))
 
 
-def build_clique_graph(design, max_clique_pins: int | None = None, *, high_fanout: str = "skip") -> SparseSymMatrix:
+def build_clique_graph(design, max_clique_pins: int | None = None, *, high_fanout: str = "skip",
+                       implicit_above: int | None = None) -> SparseSymMatrix:
     """Expand every net into a clique with edge weight 2/M (M = pin count), on the GPU.
 
     Same contract as graph.py:120-158: weights of parallel nets accumulate,
@@ -264,11 +265,24 @@ def build_clique_graph(design, max_clique_pins: int | None = None, *, high_fanou
     part only; `degrees`, `matmul`, `gift_filter` and `gift_place` use the
     whole operator (fp32 within 1e-5 of the uncapped reference; no bit-exact
     contract for the implicit part).
+
+    implicit_above (extension, keyword only): the FACTORED clique model.  Nets
+    with more than `implicit_above` pins (>= 2) -- still only those the
+    high_fanout / max_clique_pins rule keeps -- go into the implicit term and
+    only the smaller nets are stored as matrix entries.  The operator is the
+    same one (equal to the reference's in exact arithmetic; fp32 bank within
+    1e-5, fp64 bank ~1e-13 of the reference's result), but a hop costs
+    O(pins) for those nets instead of O(pins^2) stored entries, and the graph
+    builds in a fraction of the time: config 3 keeps ~9M entries + ~9M pin
+    occurrences instead of 866M entries.  The explicit `indptr`/`indices`/
+    `values` then describe the small nets only.
     """
     if high_fanout not in ("skip", "implicit"):
         raise ValueError(f"high_fanout must be 'skip' or 'implicit', got {high_fanout!r}")
     if high_fanout == "implicit" and max_clique_pins is None:
         raise ValueError("high_fanout='implicit' needs a max_clique_pins cap")
+    if implicit_above is not None and int(implicit_above) < 2:
+        raise ValueError(f"implicit_above must be >= 2, got {implicit_above}")
     torch = _lib.torch_cuda()
     lib = _lib.load_library()
     net_start, pin_cell = pin_arrays(design)
@@ -277,16 +291,26 @@ def build_clique_graph(design, max_clique_pins: int | None = None, *, high_fanou
     d_ns = torch.from_numpy(np.ascontiguousarray(net_start, dtype=np.int64)).cuda()
     d_pc = torch.from_numpy(np.ascontiguousarray(pin_cell, dtype=np.int32)).cuda()
     cap = max(int(max_clique_pins), 0) if max_clique_pins is not None else -1  # -1 = None
+    # nets stored as entries: up to the cap, or up to implicit_above if that is lower
+    explicit_cap = cap
+    if implicit_above is not None and (cap < 0 or int(implicit_above) < cap):
+        explicit_cap = int(implicit_above)
     h = ctypes.c_void_p()
     skipped = ctypes.c_int64(0)
-    _lib.check(lib.gift_build_clique_graph(ctx, n, len(net_start) - 1, _lib.dptr(d_ns), _lib.dptr(d_pc), cap,
+    _lib.check(lib.gift_build_clique_graph(ctx, n, len(net_start) - 1, _lib.dptr(d_ns), _lib.dptr(d_pc), explicit_cap,
                                            ctypes.byref(h), ctypes.byref(skipped)))
     adj = SparseSymMatrix._from_handle(h.value)
-    if high_fanout == "implicit":
+    # implicit nets: explicit_cap < pins <= upto (upto < 0: no upper bound)
+    upto = -1 if (high_fanout == "implicit" or cap < 0) else cap
+    if explicit_cap >= 0 and (high_fanout == "implicit" or explicit_cap != cap):
         kept = ctypes.c_int64(0)
-        _lib.check(lib.gift_csr_attach_high_fanout(ctx, adj.handle, len(net_start) - 1, _lib.dptr(d_ns),
-                                                   _lib.dptr(d_pc), cap, ctypes.byref(kept)))
+        _lib.check(lib.gift_csr_attach_implicit_nets(ctx, adj.handle, len(net_start) - 1, _lib.dptr(d_ns),
+                                                     _lib.dptr(d_pc), max(explicit_cap, 1), upto,
+                                                     ctypes.byref(kept)))
         adj._implicit_nets = int(kept.value)
+        dropped = int(skipped.value) - adj._implicit_nets
+        if dropped > 0:
+            log.info("clique expansion skipped %d nets with more than %d pins", dropped, max_clique_pins)
     elif skipped.value:
         log.info("clique expansion skipped %d nets with more than %d pins", skipped.value, max_clique_pins)
     return adj

@@ -829,6 +829,70 @@ def test_implicit_high_fanout_matches_uncapped_oracle(gb, orc, golden, opts, con
         gb.normalized_augmented_adjacency(adj, 2.0)
 
 
+@pytest.mark.parametrize("config,scale,window,cap,above", [
+    ("c0", 1.0, None, None, 4), ("c1", 0.25, None, None, 2), ("c2", 0.05, 600, 200, 5), ("c3", 0.03, None, 200, 8),
+    ("c2", 0.03, 600, 40, 40), ("dupnets", 0, None, None, 2)])
+def test_factored_clique_model_matches_oracle(gb, orc, golden, config, scale, window, cap, above):
+    """build_clique_graph(..., implicit_above=T): the factored clique model.
+    Nets with T < pins <= cap live in the O(pins) implicit term, only the
+    smaller ones are stored; nets above the cap stay dropped like the
+    reference's skip.  The operator is the reference's own (capped) clique
+    graph: explicit part = the oracle's graph with cap T bit for bit; degrees,
+    matmul and the fp64 bank match the oracle with the reference's cap to
+    ~1e-12, the fp32 bank and placement within the 1e-5 bar."""
+    from paper_2502_17632_b200 import synth
+
+    if config == "dupnets":
+        n = int(golden["dupnets__n"][0])
+        fd = flat(gb, golden["dupnets__net_start"], golden["dupnets__pin_cell"], n)
+    else:
+        fd = synth.generate(config, seed=9, scale=scale, **({"window": window} if window else {}))
+    adj = gb.build_clique_graph(fd, max_clique_pins=cap, implicit_above=above)
+    ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, cap)
+    if cap is not None and above >= cap:  # nothing left to factor: the plain capped graph
+        assert adj.implicit_nets == 0
+        csr_equal(adj, ref.indptr, ref.indices, ref.data, f"{config}: capped graph")
+        return
+    assert adj.implicit_nets > 0
+    small = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, above)
+    csr_equal(adj, small.indptr, small.indices, small.data, f"{config}: explicit part")
+    assert adj.nnz < ref.nnz
+    deg = orc.degrees(ref)
+    assert rel_l2(adj.degrees, deg) <= 1e-13
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((fd.num_cells, 2)) * 10.0
+    assert rel_l2(adj.matmul(x), orc.matmul(ref, x)) <= 1e-13
+    g32 = (rng.standard_normal((fd.num_cells, 2)) * 10.0 + 500.0).astype(np.float32)
+    want = orc.gift_filter(ref, g32.astype(np.float64), DEFAULT, deg)
+    got64 = gb.gift_filter(adj, g32, gb.GiftConfig(precision="fp64"))
+    assert rel_l2(got64, want) <= 1e-12
+    got = gb.gift_filter(adj, g32)
+    assert rel_l2(got, want) <= FP32_TOL
+    assert rel_l2(got - 500.0, want - 500.0) <= FP32_TOL
+    assert np.array_equal(gb.gift_filter(adj, g32), got)  # deterministic
+    if config != "dupnets":
+        cfg = gb.GiftConfig(seed=1, jitter_scale=10.0)
+        g0 = gb.initial_signal(fd, cfg)
+        placed, _ = gb.gift_place(fd, adj, cfg)
+        want_p = orc.place_epilogue(orc.gift_filter(ref, g0, DEFAULT, deg), fd.fixed_mask(), fd.fixed_positions(),
+                                    fd.region.bounds())
+        assert rel_l2(placed, want_p) <= FP32_TOL
+        mask = fd.fixed_mask()
+        assert np.array_equal(placed[mask], fd.fixed_positions()[mask])
+    with pytest.raises(ValueError):
+        adj.to_scipy()
+
+
+def test_factored_clique_model_argument_checks(gb):
+    from paper_2502_17632_b200 import synth
+
+    fd = synth.generate("c0", seed=1, scale=0.1)
+    with pytest.raises(ValueError):
+        gb.build_clique_graph(fd, implicit_above=1)
+    with pytest.raises(ValueError):
+        gb.build_clique_graph(fd, high_fanout="implicit", implicit_above=4)  # still needs a cap
+
+
 def test_small_graph_bank_replays_as_cuda_graph(gb, opts):
     """Small graphs: the fp32 bank runs as ONE cooperative kernel (grid-wide
     barrier between prep / hop ops), or -- when that is off or the bank has

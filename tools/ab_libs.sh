@@ -5,7 +5,7 @@ libs=$1; cfgs=$2; steps=${3:-10}; shift 3 2>/dev/null
 mkdir -p gpurun_out
 for c in $cfgs; do for v in $libs; do
   log=gpurun_out/ab_${v}_${c}$(echo "$@" | tr ' =' '_-').log
-  env GIFT_LIB=_variants/lib_$v.so "$@" timeout 600 python bench.py --config $c --steps $steps --no-cpu-baseline > $log 2>&1
+  env GIFT_LIB=_variants/lib_$v.so "$@" timeout 600 python bench.py --config $c --steps $steps --no-cpu-baseline --no-factored > $log 2>&1
   python - "$c" "$v" "$log" "$*" <<'PY'
 import json, sys
 c, v, f, extra = sys.argv[1:]
