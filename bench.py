@@ -279,8 +279,9 @@ def run_oneshot(args) -> None:
     _lib.load_library()
     _lib.context(0)
     t1 = time.perf_counter()
-    if args.oneshot == "python":
-        adj = gb.build_clique_graph(fd, max_clique_pins=cap)
+    if args.oneshot in ("python", "python_factored"):
+        adj = gb.build_clique_graph(fd, max_clique_pins=cap,
+                                    implicit_above=FACTOR_ABOVE if args.oneshot == "python_factored" else None)
         t_b = time.perf_counter()
         placed, _ = gb.gift_place(fd, adj, cfg)
         nnz = adj.nnz
@@ -290,7 +291,9 @@ def run_oneshot(args) -> None:
                                            fd.fixed_positions(), fd.region.bounds(), max_clique_pins=cap)
     t2 = time.perf_counter()
     assert placed.shape == (fd.num_cells, 2) and np.isfinite(placed).all()
-    out = {"api": "build_clique_graph + gift_place" if args.oneshot == "python" else "gift_place_host (C ABI)",
+    out = {"api": {"python": "build_clique_graph + gift_place",
+                   "python_factored": f"build_clique_graph(implicit_above={FACTOR_ABOVE}) + gift_place",
+                   "abi": "gift_place_host (C ABI)"}[args.oneshot],
            "config": args.config, "nnz": int(nnz), "place_s": round(t2 - t1, 4),
            "cuda_init_s": round(t1 - t0, 4), "import_s": round(import_s, 3),
            "netlist_to_positions_s": round(t2 - t0, 4)}
@@ -303,7 +306,7 @@ def run_oneshot(args) -> None:
 def oneshot_e2e(config: str, seed: int) -> dict:
     """Both one-shot paths, each in its own fresh process."""
     res = {}
-    for mode in ("python", "abi"):
+    for mode in ("python", "abi", "python_factored"):
         try:
             p = subprocess.run([sys.executable, os.path.abspath(__file__), "--oneshot", mode, "--config", config,
                                 "--seed", str(seed)], capture_output=True, text=True, timeout=600)
@@ -368,7 +371,8 @@ def main() -> None:
     ap.add_argument("--e2e-out", choices=["f32", "f64"], default="f32", help="placement dtype of the e2e leg")
     ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
                     help="kernel option (gift_ctx_set_option), e.g. tile_rows=4096; repeatable")
-    ap.add_argument("--oneshot", choices=["python", "abi"], default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--oneshot", choices=["python", "abi", "python_factored"], default=None,
+                    help=argparse.SUPPRESS)
     ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
                     help="N > 1: ghost rows by NVLink peer loads (CUDA IPC) or by NCCL all_to_all")
     ap.add_argument("--dry-launch", action="store_true", help="form the process group and exit (launcher test)")
@@ -671,11 +675,21 @@ def main() -> None:
             torch.cuda.synchronize()
             f_ms = fe0.elapsed_time(fe1) / args.steps
             f_out = dout.cpu().numpy()
+            _lib.set_profiling(True, local)
+            for _ in range(3):
+                step_f()
+            torch.cuda.synchronize()
+            f_recs = _lib.drain_profile(local)
+            _lib.set_profiling(False, local)
+            f_pass = {}
+            for kind, _units, t in f_recs:
+                f_pass.setdefault(kind, []).append(t)
             dev_l2 = float(np.linalg.norm(f_out - explicit_out) / np.linalg.norm(explicit_out))
             factored = {
                 "implicit_above": FACTOR_ABOVE, "ms_per_step": round(f_ms, 4),
                 "value": nnz_op * HOPS / (f_ms / 1e3), "unit": UNIT + " (of the explicit graph it replaces)",
                 "graph_build_s": round(fbuild_s, 3), "explicit_nnz": adj_f.nnz, "implicit_nets": adj_f.implicit_nets,
+                "pass_ms": {(f"F{k}" if k else "prep"): round(sum(v) / len(v), 5) for k, v in f_pass.items()},
                 "rel_l2_vs_explicit_path": dev_l2,
                 "note": "opt-in: build_clique_graph(..., implicit_above=T); same operator as the reference's capped "
                         "clique graph in exact arithmetic, parity-tested against the oracle "

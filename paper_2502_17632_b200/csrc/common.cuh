@@ -219,6 +219,11 @@ struct Csr {
     int32_t* occ_net = nullptr;    // [pins] net of each occurrence
     double* occ_b = nullptr;       // [pins] multiplicity of the cell in that net
     void* tbuf = nullptr;          // [nets * 4] fp64 per-hop net sums
+    // fp32 hop of the factored clique model (hf.cu k_fact_*)
+    float* coef32 = nullptr;       // [nets] 2/m
+    float* occ_b32 = nullptr;      // [pins] multiplicities
+    int32_t* row_occ = nullptr;    // [n + 1] occurrence range of every row (cells without any: empty)
+    double* row_d = nullptr;       // [n] sum over the row's occurrences of (2/m) b
   } hf;
   int64_t ext_n = 0;              // ghost block of a row shard: its columns >= n index these
   int64_t* ext_ids = nullptr;     // [ext_n] global ids of the ghost columns, ascending

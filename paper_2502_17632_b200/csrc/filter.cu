@@ -41,6 +41,8 @@ namespace gift {
 // hf.cu: implicit clique term of the nets above the cap (opt-in)
 void hf_add_degrees(Ctx* ctx, const Csr* c, double* deg);
 void hf_apply_f32(Ctx* ctx, const Csr* c, int F, const float* z, float* out);
+bool fact_hop_applies(const Ctx* ctx, const Csr* c, const HopArgs& a, int fin);
+bool fact_hop_f32(Ctx* ctx, const Csr* c, const HopArgs& a, int fin, int fout);
 void hf_apply_f64(Ctx* ctx, const Csr* c, int nc, const double* x, int64_t ld, int64_t c0, const double* s,
                   double* out);
 
@@ -883,6 +885,12 @@ static void bank_fp32(Ctx* ctx, Csr* c, const std::vector<TermGroup>& groups, in
       continue;
     }
     if (c->hf.nets) {
+      if (fact_hop_applies(ctx, c, op.a, op.fin)) {  // factored clique model: two O(pins) kernels
+        ProfScope prof(ctx, op.fin, op.a.nch);
+        fact_hop_f32(ctx, c, op.a, op.fin, op.fout);
+        c->fp32_hops++;
+        continue;
+      }
       // implicit high-fanout term: its row sums enter the hop as partial sums
       float* part = static_cast<float*>(scratch(ctx, 3, n * 4 * sizeof(float) + 64));
       GIFT_CUDA(cudaMemsetAsync(part, 0, n * op.fin * sizeof(float), ctx->stream));

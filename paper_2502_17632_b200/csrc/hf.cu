@@ -22,6 +22,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include "common.cuh"
+#include "hop.cuh"
 
 namespace gift {
 
@@ -226,6 +227,128 @@ __global__ void k_hf_apply(int64_t nc, const int32_t* __restrict__ cell, const i
   }
 }
 
+// ---- fp32 hop of the FACTORED clique model ---------------------------------
+// When every net above a few pins is implicit the stored matrix is tiny (rows
+// of ~5 entries) and the hop is two kernels over O(pins) data:
+//   k_fact_tsum: t'_e = (2/m) * sum of the net's pins' signal rows, 8 lanes
+//                per net (fp64, fixed butterfly);
+//   k_fact_hop : one thread per row: the row's few stored entries (fp32),
+//                then sum over its occurrences in implicit nets of t'_e, in
+//                net order, minus D_i z_i with D_i = sum (2/m) b over those
+//                occurrences (a per-row constant, computed at attach) -- the
+//                same sum of (2/m)(t_e - b z_i), but one 32-byte gather per
+//                occurrence and nothing else; fp64 (t_e is ~m signal values:
+//                rounding it to fp32 would cost the row sum several ulps);
+//                then the shared fused epilogue (hop.cuh).
+// Fixed orders everywhere: deterministic.
+struct FactArgs {
+  int64_t nets;
+  const int64_t* net_start;
+  const int32_t* pin_cell;
+  double* t;  // [nets, F] (2/m) * net sums
+  const int32_t* row_occ;
+  const int32_t* occ_net;
+  const double* row_d;  // [n] D_i
+  const double* coef;
+};
+
+template <int F>
+__global__ void __launch_bounds__(kBlock) k_fact_tsum(FactArgs h, const float* __restrict__ z) {
+  constexpr int G = 8;
+  const int lane = threadIdx.x & 31, sub = lane & (G - 1);
+  const unsigned gmask = 0xffu << (lane & ~(G - 1));
+  const uint64_t pol_z = policy_evict_last();
+  const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t e = g0; e < h.nets; e += ng) {
+    double acc[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) acc[f] = 0.0;
+    const int64_t a = h.net_start[e], b = h.net_start[e + 1];
+    for (int64_t p = a + sub; p < b; p += G) {
+      const VecF<F> zq = ld_z<F>(z + (int64_t)h.pin_cell[p] * F, pol_z);
+#pragma unroll
+      for (int f = 0; f < F; ++f) acc[f] += (double)zq.v[f];
+    }
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1)
+#pragma unroll
+      for (int f = 0; f < F; ++f) acc[f] += __shfl_xor_sync(gmask, acc[f], off, G);
+    if (sub == 0)
+#pragma unroll
+      for (int f = 0; f < F; ++f) h.t[e * F + f] = h.coef[e] * acc[f];
+  }
+}
+
+template <int F, int FOUT>
+__global__ void __launch_bounds__(kBlock) k_fact_hop(HopArgs a, FactArgs h) {
+  const uint64_t pol_z = policy_evict_last();
+  for (int64_t row = a.row_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < a.n;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    float acc[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) acc[f] = 0.f;
+    const int64_t k1 = a.rowptr[row + 1];
+    for (int64_t k = a.rowptr[row]; k < k1; ++k) {
+      const VecF<F> zq = ld_z<F>(a.zin + (int64_t)a.col[k] * F, pol_z);
+      const float w = a.w[k];
+#pragma unroll
+      for (int f = 0; f < F; ++f) acc[f] = fmaf(w, zq.v[f], acc[f]);
+    }
+    const int o1 = h.row_occ[row + 1];
+    int o = h.row_occ[row];
+    if (o < o1) {
+      const VecF<F> zi = ld_z<F>(a.zin + row * F, pol_z);
+      double imp[F];
+#pragma unroll
+      for (int f = 0; f < F; ++f) imp[f] = 0.0;
+      for (; o < o1; ++o) {
+        const double* tp = h.t + (int64_t)h.occ_net[o] * F;
+#pragma unroll
+        for (int f = 0; f < F; ++f) imp[f] += tp[f];
+      }
+      const double d = h.row_d[row];
+#pragma unroll
+      for (int f = 0; f < F; ++f) imp[f] = fma(-d, (double)zi.v[f], imp[f]);
+#pragma unroll
+      for (int f = 0; f < F; ++f) acc[f] += (float)imp[f];
+    }
+    row_epilogue<F, FOUT>(a, row, acc, pol_z);
+  }
+}
+
+template <int F>
+void launch_fact(Ctx* ctx, const HopArgs& a, const FactArgs& h, int fout) {
+  cudaStream_t st = ctx->stream;
+  k_fact_tsum<F><<<grid_for(h.nets * 8, kBlock, 1LL << 30), kBlock, 0, st>>>(h, a.zin);
+  GIFT_LAUNCH_CHECK(ctx);
+  const unsigned grid = grid_for(a.n - a.row_begin, kBlock, 1LL << 30);
+  switch (fout) {
+    case 0: k_fact_hop<F, 0><<<grid, kBlock, 0, st>>>(a, h); break;
+    case 1: k_fact_hop<F, 1><<<grid, kBlock, 0, st>>>(a, h); break;
+    case 2: k_fact_hop<F, 2><<<grid, kBlock, 0, st>>>(a, h); break;
+    default: k_fact_hop<F, 4><<<grid, kBlock, 0, st>>>(a, h); break;
+  }
+  GIFT_LAUNCH_CHECK(ctx);
+}
+
+// D_i = sum over the row's occurrences of (2/m) b, in net order
+__global__ void k_hf_row_d(int64_t n, const int32_t* __restrict__ row_occ, const int32_t* __restrict__ occ_net,
+                           const double* __restrict__ b64, const double* __restrict__ coef64,
+                           double* __restrict__ row_d) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    double d = 0.0;
+    for (int o = row_occ[r]; o < row_occ[r + 1]; ++o) d = fma(coef64[occ_net[o]], b64[o], d);
+    row_d[r] = d;
+  }
+}
+
+__global__ void k_hf_row_counts(int64_t nc, const int32_t* __restrict__ cell, const int64_t* __restrict__ occ_ptr,
+                                int32_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x)
+    cnt[cell[i]] = (int32_t)(occ_ptr[i + 1] - occ_ptr[i]);
+}
+
 template <typename T, bool S>
 void hf_apply_t(Ctx* ctx, const Csr* c, int F, const T* z, int64_t ld, int64_t c0, const double* s, T* out,
                 int64_t ldo) {
@@ -357,11 +480,27 @@ int64_t csr_attach_high_fanout(Ctx* ctx, Csr* c, int64_t n_nets, const int64_t* 
   k_hf_cells<<<grid_for(nc + 1, kBlock), kBlock, 0, st>>>(nc, P, starts.p, cell_s.p, H.cell, H.occ_ptr);
   GIFT_LAUNCH_CHECK(ctx);
   H.tbuf = csr_alloc(ctx, c, nh * 4 * sizeof(double));
+  H.coef32 = coef32;
+  H.occ_b32 = b32;
+  {  // occurrence range of every row (occurrences are grouped by cell, cells ascending)
+    DevBuf<int32_t> cnt(ctx, c->n + 1);
+    GIFT_CUDA(cudaMemsetAsync(cnt.p, 0, (c->n + 1) * sizeof(int32_t), st));
+    k_hf_row_counts<<<grid_for(nc, kBlock), kBlock, 0, st>>>(nc, H.cell, H.occ_ptr, cnt.p);
+    GIFT_LAUNCH_CHECK(ctx);
+    H.row_occ = static_cast<int32_t*>(csr_alloc(ctx, c, (c->n + 1) * sizeof(int32_t)));
+    size_t bytes = 0;
+    GIFT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, H.row_occ, c->n + 1, st));
+    DevBuf<char> tmp(ctx, bytes);
+    GIFT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, H.row_occ, c->n + 1, st));
+    ctx->launches += 2;
+    H.row_d = static_cast<double*>(csr_alloc(ctx, c, (c->n + 1) * sizeof(double)));
+    k_hf_row_d<<<grid_for(c->n, kBlock), kBlock, 0, st>>>(c->n, H.row_occ, H.occ_net, H.occ_b, H.coef, H.row_d);
+    GIFT_LAUNCH_CHECK(ctx);
+    GIFT_CUDA(cudaStreamSynchronize(st));
+  }
   H.nets = nh;
   H.pins = P;
   H.cells = nc;
-  (void)coef32;
-  (void)b32;
   c->hf = H;
   return nh;
 }
@@ -379,6 +518,31 @@ void hf_add_degrees(Ctx* ctx, const Csr* c, double* deg) {
 // hop: z has F floats per row, ld = F); other rows of out are left untouched
 void hf_apply_f32(Ctx* ctx, const Csr* c, int F, const float* z, float* out) {
   hf_apply_t<float, false>(ctx, c, F, z, F, 0, nullptr, out, F);
+}
+
+// The whole fp32 hop (explicit rows + implicit nets + epilogue) as the two
+// factored-model kernels; false when the graph is not a factored one (its
+// stored rows are long: the tiled / row kernels serve those with part_in)
+bool fact_hop_applies(const Ctx* ctx, const Csr* c, const HopArgs& a, int fin) {
+  const Csr::Hf& H = c->hf;
+  if (!H.nets || !H.row_occ || a.part_in || a.part_out || a.row_list) return false;
+  if (fin != 1 && fin != 2 && fin != 4) return false;
+  // stored rows long enough for the tiled / row kernels (option "tiled_min_mean",
+  // default 32): not the factored regime, the term enters those as partial sums
+  return c->mean_row < (double)ctx->opt.tiled_min_mean;
+}
+
+bool fact_hop_f32(Ctx* ctx, const Csr* c, const HopArgs& a, int fin, int fout) {
+  const Csr::Hf& H = c->hf;
+  if (!fact_hop_applies(ctx, c, a, fin)) return false;
+  FactArgs h{H.nets, H.net_start, H.pin_cell, static_cast<double*>(H.tbuf), H.row_occ, H.occ_net, H.row_d, H.coef};
+  switch (fin) {
+    case 1: launch_fact<1>(ctx, a, h, fout); break;
+    case 2: launch_fact<2>(ctx, a, h, fout); break;
+    case 4: launch_fact<4>(ctx, a, h, fout); break;
+    default: return false;
+  }
+  return true;
 }
 
 // out[cell, :nc] = (A_hf (s o x))[cell] over columns c0 .. c0 + nc of x
