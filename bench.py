@@ -271,7 +271,7 @@ def run_oneshot(args) -> None:
     fd = synth.generate(args.config, seed=args.seed)
     cap = fd.meta["max_clique_pins"]
     cfg = gb.GiftConfig(seed=0, jitter_scale=10.0)
-    g32 = synth.signal_fp32(fd, seed=0) if args.oneshot == "abi" else None
+    g32 = synth.signal_fp32(fd, seed=0) if args.oneshot.startswith("abi") else None
     t0 = time.perf_counter()
     torch.cuda.init()
     from paper_2502_17632_b200 import _lib
@@ -288,12 +288,14 @@ def run_oneshot(args) -> None:
     else:
         t_b = None
         placed, nnz = gb.gift_place_arrays(fd.net_start, fd.pin_cell, g32, fd.fixed_mask(),
-                                           fd.fixed_positions(), fd.region.bounds(), max_clique_pins=cap)
+                                           fd.fixed_positions(), fd.region.bounds(), max_clique_pins=cap,
+                                           implicit_above=FACTOR_ABOVE if args.oneshot == "abi_factored" else None)
     t2 = time.perf_counter()
     assert placed.shape == (fd.num_cells, 2) and np.isfinite(placed).all()
     out = {"api": {"python": "build_clique_graph + gift_place",
                    "python_factored": f"build_clique_graph(implicit_above={FACTOR_ABOVE}) + gift_place",
-                   "abi": "gift_place_host (C ABI)"}[args.oneshot],
+                   "abi": "gift_place_host (C ABI)",
+                   "abi_factored": f"gift_place_host (C ABI, option implicit_above={FACTOR_ABOVE})"}[args.oneshot],
            "config": args.config, "nnz": int(nnz), "place_s": round(t2 - t1, 4),
            "cuda_init_s": round(t1 - t0, 4), "import_s": round(import_s, 3),
            "netlist_to_positions_s": round(t2 - t0, 4)}
@@ -306,7 +308,7 @@ def run_oneshot(args) -> None:
 def oneshot_e2e(config: str, seed: int) -> dict:
     """Both one-shot paths, each in its own fresh process."""
     res = {}
-    for mode in ("python", "abi", "python_factored"):
+    for mode in ("python", "abi", "python_factored", "abi_factored"):
         try:
             p = subprocess.run([sys.executable, os.path.abspath(__file__), "--oneshot", mode, "--config", config,
                                 "--seed", str(seed)], capture_output=True, text=True, timeout=600)
@@ -368,16 +370,20 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-oneshot", action="store_true")
     ap.add_argument("--no-factored", action="store_true", help="skip the factored-clique-model leg")
+    ap.add_argument("--factor-above", type=int, default=None, help="implicit_above of the factored leg")
     ap.add_argument("--e2e-out", choices=["f32", "f64"], default="f32", help="placement dtype of the e2e leg")
     ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
                     help="kernel option (gift_ctx_set_option), e.g. tile_rows=4096; repeatable")
-    ap.add_argument("--oneshot", choices=["python", "abi", "python_factored"], default=None,
+    ap.add_argument("--oneshot", choices=["python", "abi", "python_factored", "abi_factored"], default=None,
                     help=argparse.SUPPRESS)
     ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
                     help="N > 1: ghost rows by NVLink peer loads (CUDA IPC) or by NCCL all_to_all")
     ap.add_argument("--dry-launch", action="store_true", help="form the process group and exit (launcher test)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.factor_above:
+        global FACTOR_ABOVE
+        FACTOR_ABOVE = args.factor_above
     if args.oneshot:
         run_oneshot(args)
         return

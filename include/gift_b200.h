@@ -81,7 +81,9 @@ int gift_ctx_set_tiled_policy(gift_ctx* ctx, int policy);
  *   "tiled" 0/1, "tiled_min_rows", "tiled_min_mean" (when the tiled hop applies),
  *   "tile_rows" 0 or a multiple of 32 in 2048..16384 and "col_bits" 0/11..14
  *   (force a tile shape), "balance" 0/1 (default tile heights shrink so the
- *   tiles fill whole waves of SMs),
+ *   tiles fill whole waves of SMs), "implicit_above" 0 / T >= 2 (gift_place_host
+ *   builds the factored clique model: nets with T < pins <= max_clique_pins
+ *   as the implicit term, see gift_csr_attach_implicit_nets),
  *   "barrier_free" 0/1, "fused" 0/1 (small banks as one cooperative kernel),
  *   "graphs" 0/1 (CUDA-graph replay of small banks the fused kernel does not take),
  *   "zero_copy" 0/1 (pinned host buffers used in place), "schedule" 0/1,

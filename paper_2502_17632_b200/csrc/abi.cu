@@ -163,6 +163,9 @@ void set_option(Ctx* ctx, const std::string& name, int64_t v) {
     if (v != 0) throw_error(GIFT_ERR_VALUE, "option codes: u8 weight codes exist only in -DGIFT_TUNING builds");
 #endif
     o.codes = v;
+  } else if (name == "implicit_above") {
+    if (v != 0 && v < 2) bad();
+    o.implicit_above = v;
   } else if (name == "row_lanes") {
     if (v != 0 && v != 8 && v != 16 && v != 32) bad();
     o.row_lanes = v;
@@ -539,7 +542,19 @@ int gift_place_host(gift_ctx* ctx, int64_t n_cells, int64_t n_nets, const int64_
   gift::DevBuf<int32_t> dpc(ctx, n_pins);
   GIFT_CUDA(cudaMemcpyAsync(dns.p, h_net_start, (n_nets + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   if (n_pins) GIFT_CUDA(cudaMemcpyAsync(dpc.p, h_pin_cell, n_pins * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-  gift::Csr* c = gift::build_clique_graph(ctx, n_cells, n_nets, dns.p, dpc.p, max_clique_pins, nullptr);
+  // option "implicit_above" = T > 0: the factored clique model -- nets with
+  // T < pins <= max_clique_pins are applied as the O(pins) implicit term and
+  // only the smaller ones are expanded into matrix entries (same operator)
+  const int64_t T = ctx->opt.implicit_above;
+  const bool factored = T >= 2 && (max_clique_pins < 0 || T < max_clique_pins);
+  gift::Csr* c = gift::build_clique_graph(ctx, n_cells, n_nets, dns.p, dpc.p, factored ? T : max_clique_pins, nullptr);
+  try {
+    if (factored) gift::csr_attach_high_fanout(ctx, c, n_nets, dns.p, dpc.p, T, max_clique_pins < 0 ? -1 : max_clique_pins);
+  } catch (...) {
+    gift::csr_touch(ctx, c);
+    gift::csr_destroy(c);
+    throw;
+  }
   dns.reset();
   dpc.reset();
   try {

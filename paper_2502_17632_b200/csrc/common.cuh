@@ -70,6 +70,7 @@ struct Ctx {
     int64_t fused = 1;              // "fused": small-graph banks as one cooperative kernel
     int64_t zero_copy = 1;          // "zero_copy": *_host calls use pinned buffers in place
     int64_t schedule = 1;           // "schedule": bank-conflict-aware entry order in the tiled copy
+    int64_t implicit_above = 0;     // "implicit_above": gift_place_host builds the factored clique model (0 = off)
     int64_t row_lanes = 0;          // "row_lanes": force lanes per row of the row kernel (8 / 16 / 32)
     int64_t codes = 0;              // "codes" (tuning builds): u8 weight codes in the F <= 2 tiled copy
     int64_t prefetch = 0;           // "prefetch": tiled hop prefetches each warp's next slice into L2
@@ -224,6 +225,7 @@ struct Csr {
     float* occ_b32 = nullptr;      // [pins] multiplicities
     int32_t* row_occ = nullptr;    // [n + 1] occurrence range of every row (cells without any: empty)
     double* row_d = nullptr;       // [n] sum over the row's occurrences of (2/m) b
+    void* cw = nullptr;            // [nnz] (column, fp32 weight) pairs of the stored entries (lazy)
   } hf;
   int64_t ext_n = 0;              // ghost block of a row shard: its columns >= n index these
   int64_t* ext_ids = nullptr;     // [ext_n] global ids of the ghost columns, ascending

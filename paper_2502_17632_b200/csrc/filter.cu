@@ -42,7 +42,7 @@ namespace gift {
 void hf_add_degrees(Ctx* ctx, const Csr* c, double* deg);
 void hf_apply_f32(Ctx* ctx, const Csr* c, int F, const float* z, float* out);
 bool fact_hop_applies(const Ctx* ctx, const Csr* c, const HopArgs& a, int fin);
-bool fact_hop_f32(Ctx* ctx, const Csr* c, const HopArgs& a, int fin, int fout);
+bool fact_hop_f32(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout);
 void hf_apply_f64(Ctx* ctx, const Csr* c, int nc, const double* x, int64_t ld, int64_t c0, const double* s,
                   double* out);
 

@@ -250,6 +250,7 @@ struct FactArgs {
   const int32_t* occ_net;
   const double* row_d;  // [n] D_i
   const double* coef;
+  const int2* cw;       // [nnz] stored entries as (column, fp32 weight bits): one 8-byte load each
 };
 
 template <int F>
@@ -265,7 +266,15 @@ __global__ void __launch_bounds__(kBlock) k_fact_tsum(FactArgs h, const float* _
 #pragma unroll
     for (int f = 0; f < F; ++f) acc[f] = 0.0;
     const int64_t a = h.net_start[e], b = h.net_start[e + 1];
-    for (int64_t p = a + sub; p < b; p += G) {
+    int64_t p = a + sub;
+    for (; p + 3 * G < b; p += 4 * G) {  // four gathers in flight per lane (same summation order)
+      const int c0 = h.pin_cell[p], c1 = h.pin_cell[p + G], c2 = h.pin_cell[p + 2 * G], c3 = h.pin_cell[p + 3 * G];
+      const VecF<F> q0 = ld_z<F>(z + (int64_t)c0 * F, pol_z), q1 = ld_z<F>(z + (int64_t)c1 * F, pol_z);
+      const VecF<F> q2 = ld_z<F>(z + (int64_t)c2 * F, pol_z), q3 = ld_z<F>(z + (int64_t)c3 * F, pol_z);
+#pragma unroll
+      for (int f = 0; f < F; ++f) acc[f] = (((acc[f] + (double)q0.v[f]) + (double)q1.v[f]) + (double)q2.v[f]) + (double)q3.v[f];
+    }
+    for (; p < b; p += G) {
       const VecF<F> zq = ld_z<F>(z + (int64_t)h.pin_cell[p] * F, pol_z);
 #pragma unroll
       for (int f = 0; f < F; ++f) acc[f] += (double)zq.v[f];
@@ -290,8 +299,9 @@ __global__ void __launch_bounds__(kBlock) k_fact_hop(HopArgs a, FactArgs h) {
     for (int f = 0; f < F; ++f) acc[f] = 0.f;
     const int64_t k1 = a.rowptr[row + 1];
     for (int64_t k = a.rowptr[row]; k < k1; ++k) {
-      const VecF<F> zq = ld_z<F>(a.zin + (int64_t)a.col[k] * F, pol_z);
-      const float w = a.w[k];
+      const int2 e = __ldg(h.cw + k);
+      const VecF<F> zq = ld_z<F>(a.zin + (int64_t)e.x * F, pol_z);
+      const float w = __int_as_float(e.y);
 #pragma unroll
       for (int f = 0; f < F; ++f) acc[f] = fmaf(w, zq.v[f], acc[f]);
     }
@@ -330,6 +340,13 @@ void launch_fact(Ctx* ctx, const HopArgs& a, const FactArgs& h, int fout) {
     default: k_fact_hop<F, 4><<<grid, kBlock, 0, st>>>(a, h); break;
   }
   GIFT_LAUNCH_CHECK(ctx);
+}
+
+// stored entries as (column, fp32 weight) pairs (the weights rounded like the hop's w32)
+__global__ void k_fact_pack(int64_t nnz, const int32_t* __restrict__ col, const double* __restrict__ v,
+                            int2* __restrict__ cw) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x)
+    cw[k] = make_int2(col[k], __float_as_int((float)v[k]));
 }
 
 // D_i = sum over the row's occurrences of (2/m) b, in net order
@@ -493,6 +510,13 @@ int64_t csr_attach_high_fanout(Ctx* ctx, Csr* c, int64_t n_nets, const int64_t* 
     DevBuf<char> tmp(ctx, bytes);
     GIFT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, H.row_occ, c->n + 1, st));
     ctx->launches += 2;
+    if (c->nnz <= 64 * c->n) {  // short stored rows: the factored hop's (column, weight) pairs
+      H.cw = csr_alloc(ctx, c, (c->nnz > 0 ? c->nnz : 1) * sizeof(int2));
+      if (c->nnz > 0) {
+        k_fact_pack<<<grid_for(c->nnz, kBlock), kBlock, 0, st>>>(c->nnz, c->indices, c->values, static_cast<int2*>(H.cw));
+        GIFT_LAUNCH_CHECK(ctx);
+      }
+    }
     H.row_d = static_cast<double*>(csr_alloc(ctx, c, (c->n + 1) * sizeof(double)));
     k_hf_row_d<<<grid_for(c->n, kBlock), kBlock, 0, st>>>(c->n, H.row_occ, H.occ_net, H.occ_b, H.coef, H.row_d);
     GIFT_LAUNCH_CHECK(ctx);
@@ -525,17 +549,19 @@ void hf_apply_f32(Ctx* ctx, const Csr* c, int F, const float* z, float* out) {
 // stored rows are long: the tiled / row kernels serve those with part_in)
 bool fact_hop_applies(const Ctx* ctx, const Csr* c, const HopArgs& a, int fin) {
   const Csr::Hf& H = c->hf;
-  if (!H.nets || !H.row_occ || a.part_in || a.part_out || a.row_list) return false;
+  if (!H.nets || !H.row_occ || !H.cw || a.part_in || a.part_out || a.row_list) return false;
   if (fin != 1 && fin != 2 && fin != 4) return false;
   // stored rows long enough for the tiled / row kernels (option "tiled_min_mean",
   // default 32): not the factored regime, the term enters those as partial sums
   return c->mean_row < (double)ctx->opt.tiled_min_mean;
 }
 
-bool fact_hop_f32(Ctx* ctx, const Csr* c, const HopArgs& a, int fin, int fout) {
+
+bool fact_hop_f32(Ctx* ctx, Csr* c, const HopArgs& a, int fin, int fout) {
   const Csr::Hf& H = c->hf;
   if (!fact_hop_applies(ctx, c, a, fin)) return false;
-  FactArgs h{H.nets, H.net_start, H.pin_cell, static_cast<double*>(H.tbuf), H.row_occ, H.occ_net, H.row_d, H.coef};
+  FactArgs h{H.nets, H.net_start, H.pin_cell, static_cast<double*>(H.tbuf), H.row_occ, H.occ_net, H.row_d, H.coef,
+             static_cast<const int2*>(H.cw)};
   switch (fin) {
     case 1: launch_fact<1>(ctx, a, h, fout); break;
     case 2: launch_fact<2>(ctx, a, h, fout); break;

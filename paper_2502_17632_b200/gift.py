@@ -160,10 +160,18 @@ def gift_place(design, adj, config: GiftConfig | None = None) -> tuple[np.ndarra
 
 def gift_place_arrays(net_start, pin_cell, g0, fixed_mask, fixed_pos, region, terms=DEFAULT_TERMS,
                       max_clique_pins: int | None = None, precision: str = "fp32",
-                      out_dtype=np.float64) -> tuple[np.ndarray, int]:
+                      out_dtype=np.float64, implicit_above: int | None = None) -> tuple[np.ndarray, int]:
     """Netlist in, positions out, through the single host-buffer C ABI call
     `gift_place_host` (H2D, clique build, bank, epilogue, D2H).
-    Returns (positions [N, 2], nnz of the clique graph)."""
+    Returns (positions [N, 2], nnz of the clique graph).  implicit_above=T:
+    the factored clique model (see build_clique_graph) -- nets above T pins
+    applied as the O(pins) implicit term; nnz then counts the stored part."""
+    if implicit_above is not None:
+        if int(implicit_above) < 2:
+            raise ValueError(f"implicit_above must be >= 2, got {implicit_above}")
+        with _lib.options(implicit_above=int(implicit_above)):
+            return gift_place_arrays(net_start, pin_cell, g0, fixed_mask, fixed_pos, region, terms, max_clique_pins,
+                                     precision, out_dtype)
     lib = _lib.load_library()
     ctx = _lib.context()
     net_start = np.ascontiguousarray(net_start, dtype=np.int64)

@@ -883,6 +883,31 @@ def test_factored_clique_model_matches_oracle(gb, orc, golden, config, scale, wi
         adj.to_scipy()
 
 
+def test_factored_clique_model_through_host_abi(gb, orc):
+    """gift_place_host with the context option implicit_above (Python:
+    gift_place_arrays(..., implicit_above=T)): netlist arrays in host memory
+    -> placement, on the factored model; matches the oracle's gift_place with
+    the reference's cap; the option does not leak into later calls."""
+    from paper_2502_17632_b200 import _lib, synth
+
+    fd = synth.generate("c2", seed=5, scale=0.04, window=600)
+    cap = 200
+    ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, cap)
+    g32 = synth.signal_fp32(fd, seed=4)
+    want = orc.place_epilogue(orc.gift_filter(ref, g32.astype(np.float64), DEFAULT), fd.fixed_mask(),
+                              fd.fixed_positions(), fd.region.bounds())
+    got, nnz = gb.gift_place_arrays(fd.net_start, fd.pin_cell, g32, fd.fixed_mask(), fd.fixed_positions(),
+                                    fd.region.bounds(), max_clique_pins=cap, implicit_above=5)
+    assert 0 < nnz < ref.nnz // 10
+    assert rel_l2(got, want) <= FP32_TOL
+    mask = fd.fixed_mask()
+    assert np.array_equal(got[mask], fd.fixed_positions()[mask])
+    assert "implicit_above" not in _lib._options
+    plain, nnz2 = gb.gift_place_arrays(fd.net_start, fd.pin_cell, g32, fd.fixed_mask(), fd.fixed_positions(),
+                                       fd.region.bounds(), max_clique_pins=cap)
+    assert nnz2 == ref.nnz and rel_l2(plain, want) <= FP32_TOL
+
+
 def test_factored_clique_model_argument_checks(gb):
     from paper_2502_17632_b200 import synth
 

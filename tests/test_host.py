@@ -146,7 +146,42 @@ def test_kernel_options_are_validated_and_restored():
     with _lib.options(tile_rows=4096, graphs=0):
         assert _lib._options["tile_rows"] == 4096 and _lib._options["graphs"] == 0
     assert _lib._options == before
-    assert set(_lib.DEFAULT_OPTIONS) >= {"tiled", "tile_rows", "col_bits", "fused", "graphs", "zero_copy"}
+    assert set(_lib.DEFAULT_OPTIONS) >= {"tiled", "tile_rows", "col_bits", "fused", "graphs", "zero_copy", "balance",
+                                         "implicit_above"}
+
+
+def test_factored_model_arguments_are_checked_before_any_device_work():
+    """implicit_above below 2 (or high_fanout='implicit' without a cap) is a
+    ValueError on any machine; so is the same argument of gift_place_arrays."""
+    from paper_2502_17632_b200 import synth
+
+    fd = synth.generate("c0", seed=1, scale=0.02)
+    for bad in (1, 0, -3):
+        with pytest.raises(ValueError):
+            gb.build_clique_graph(fd, implicit_above=bad)
+        with pytest.raises(ValueError):
+            gb.gift_place_arrays(fd.net_start, fd.pin_cell, np.zeros((fd.num_cells, 2), np.float32), fd.fixed_mask(),
+                                 fd.fixed_positions(), fd.region.bounds(), implicit_above=bad)
+    with pytest.raises(ValueError):
+        gb.build_clique_graph(fd, high_fanout="implicit", implicit_above=4)
+
+
+def test_peer_exchange_pull_tables():
+    """PeerExchange._finish_tables: every ghost id maps to (owner rank, row in
+    the owner's block); owners hold contiguous row ranges."""
+    from paper_2502_17632_b200 import shard
+
+    class Be:
+        def upload(self, a):
+            return np.asarray(a)
+
+    bounds = np.array([0, 10, 25, 40])
+    ghosts = np.array([0, 9, 25, 39])
+    plan = shard.ShardPlan(3, 1, bounds, 10, 25, ghosts, [2, 0, 2], [0, 0, 0], np.zeros(0, np.int64))
+    ex = shard.PeerExchange.__new__(shard.PeerExchange)
+    ex._finish_tables(Be(), plan)
+    assert ex.src_rank.tolist() == [0, 0, 2, 2]
+    assert ex.src_row.tolist() == [0, 9, 0, 14]
 
 
 def test_gift_config_output_dtype():
