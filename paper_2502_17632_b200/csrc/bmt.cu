@@ -804,6 +804,31 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int ste
 // Without this a segment started with three dependent memory latencies
 // AFTER the staging (slice range -> slice offsets -> records), ~2.5 us of the
 // ~12 us a config-4 segment takes.
+// slice metadata loads pinned where they are written (asm volatile): as plain
+// loads the compiler sank the row id to its use after the slice's FMAs, one
+// exposed memory latency per slice (9 % of the c4 F = 4 pass's stall samples)
+#ifndef GIFT_BMT_META
+#define GIFT_BMT_META 2
+#endif
+__device__ __forceinline__ int64_t ld_meta_s64(const int64_t* p) {
+#if GIFT_BMT_META
+  int64_t v;
+  asm volatile("ld.global.nc.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ int ld_meta_u16(const uint16_t* p) {
+#if GIFT_BMT_META
+  unsigned short v;
+  asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return (int)v;
+#else
+  return (int)*p;
+#endif
+}
+
 struct FirstSlice {
   int64_t off = 0, end = 0;  // slot range (raw loads: converted where they are used)
   int row = 0xffff;
@@ -812,9 +837,9 @@ struct FirstSlice {
 __device__ __forceinline__ FirstSlice load_first(const BmtArgs& b, int sl0, int nsl, int warp, int lane) {
   FirstSlice f;
   if (warp < nsl) {
-    f.off = b.slice_off[sl0 + warp];
-    f.end = b.slice_off[sl0 + warp + 1];
-    f.row = b.slice_rows[(int64_t)(sl0 + warp) * 32 + lane];
+    f.off = ld_meta_s64(b.slice_off + sl0 + warp);
+    f.end = ld_meta_s64(b.slice_off + sl0 + warp + 1);
+    f.row = ld_meta_u16(b.slice_rows + (int64_t)(sl0 + warp) * 32 + lane);
   }
   return f;
 }
@@ -840,9 +865,9 @@ __device__ __forceinline__ void segment_slices_pre(const BmtArgs& b, int sl0, in
     int64_t off_n = 0, end_n = 0;
     int row_n = 0xffff;
     if (jn < nsl) {
-      off_n = b.slice_off[sl0 + jn];
-      end_n = b.slice_off[sl0 + jn + 1];
-      row_n = b.slice_rows[(int64_t)(sl0 + jn) * 32 + lane];
+      off_n = ld_meta_s64(b.slice_off + sl0 + jn);
+      end_n = ld_meta_s64(b.slice_off + sl0 + jn + 1);
+      row_n = ld_meta_u16(b.slice_rows + (int64_t)(sl0 + jn) * 32 + lane);
     }
     const int steps = (int)((end - off) / 128);
     const uint8_t* cp = b.data + (off / 128) * RB + 8 * lane;
@@ -1144,10 +1169,14 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
   // slice ranges of this segment [sl0, sl1), the next [sl1, sl2) and the one after
   // (loaded a segment ahead of the addresses they feed)
   int sl0 = 0, sl1 = 0, sl2 = 0;
+  FirstSlice cur;
   if (kPre && s_beg < s_end) {
     sl0 = (int)b.seg_slice[s_beg];
     sl1 = (int)b.seg_slice[s_beg + 1];
     sl2 = s_beg + 2 <= s_end ? (int)b.seg_slice[s_beg + 2] : sl1;
+#if GIFT_BMT_META >= 2
+    cur = load_first(b, sl0, sl1 - sl0, warp, lane);
+#endif
   }
   for (int64_t s = s_beg; s < s_end; ++s) {
     const int64_t cbase = (int64_t)b.seg_code[s] * kC;
@@ -1167,13 +1196,15 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
       for (int i = tid; i < nv; i += kThreads) dst[i] = src[i];
       for (int i = nv * 4 + tid; i < nf; i += kThreads) zs[i] = zg[i];
     }
-    // the warp's first slice: metadata, then its first records, in flight
-    // while the block is staged
+    // the warp's first slice: its metadata was requested when the warp left
+    // the previous segment (the latency ran under the wait for the slower
+    // warps); its first records go in flight now, while the block is staged
     RecPipe<D, CODED> pipe;
-    FirstSlice cur;
     int sl3 = sl2;
     if constexpr (kPre) {
+#if GIFT_BMT_META < 2
       cur = load_first(b, sl0, sl1 - sl0, warp, lane);
+#endif
       if (s + 3 <= s_end) sl3 = (int)b.seg_slice[s + 3];
       if (warp < sl1 - sl0) {
         const uint8_t* cp = b.data + (cur.off / 128) * RB + 8 * lane;
@@ -1190,6 +1221,9 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
     }
     if constexpr (kPre) {
       segment_slices_pre<FIN, D, CODED>(b, sl0, sl1 - sl0, warp, cur, pipe, zs, accs, &slice_ctr, tbl, lane, pol_s);
+#if GIFT_BMT_META >= 2
+      if (s + 1 < s_end) cur = load_first(b, sl1, sl2 - sl1, warp, lane);
+#endif
       sl0 = sl1;
       sl1 = sl2;
       sl2 = sl3;

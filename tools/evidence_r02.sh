@@ -13,8 +13,8 @@ if [ "${SKIP_TESTS:-0}" != 1 ]; then
   echo "smoke exit $?"; tail -1 gpurun_out/smoke.log
 fi
 for c in c3 c4; do
-  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_hop -s 8 -c 8 \
-    -o /tmp/r02_$c python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --no-oneshot > gpurun_out/r02_ncu_$c.log 2>&1
+  timeout 1500 ncu --set full --clock-control none --import-source on -f -k regex:k_hop -s 8 -c 8 \
+    -o /tmp/r02_$c python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --no-oneshot --no-factored > gpurun_out/r02_ncu_$c.log 2>&1
   echo "ncu full $c exit $?"
   # (the reports stay in /tmp: gpurun_out/ must stay under 64 MiB)
   ncu -i /tmp/r02_$c.ncu-rep --page raw --csv > /tmp/r02_${c}_raw.csv 2>/dev/null
@@ -25,8 +25,14 @@ for c in c3 c4; do
     "ncu --set full --clock-control none -k regex:k_hop -s 8 -c 8, bench.py --config $c (tools/evidence_r02.sh)" \
     > gpurun_out/r02_traffic_$c.json
 done
+# the factored clique model's two hop kernels (bench.py "factored" leg)
+timeout 1200 ncu --set full --clock-control none --import-source on -f -k regex:k_fact -s 8 -c 4 -o /tmp/fact_c3 \
+  python bench.py --config c3 --steps 2 --warmup 3 --no-cpu-baseline --no-oneshot > gpurun_out/ncu_fact.log 2>&1
+echo "ncu factored exit $?"
+ncu -i /tmp/fact_c3.ncu-rep --page raw --csv > /tmp/fact_c3_raw.csv 2>/dev/null
+python tools/ncu_stalls.py /tmp/fact_c3_raw.csv > gpurun_out/r02_fact_kernels_c3.txt 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
-  --log-file gpurun_out/r02_launches_c3.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-oneshot > gpurun_out/ncu_l.log 2>&1
+  --log-file gpurun_out/r02_launches_c3.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-oneshot --no-factored > gpurun_out/ncu_l.log 2>&1
 echo "ncu launches exit $?"
 cp gpurun_out/r02_traffic_c3.json gpurun_out/r02_traffic_c4.json profiles/ 2>/dev/null
 timeout 1500 python bench.py > gpurun_out/r02_bench_c3.log 2>&1; echo "bench exit $?"; tail -1 gpurun_out/r02_bench_c3.log | cut -c1-300
