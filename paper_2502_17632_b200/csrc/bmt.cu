@@ -804,11 +804,13 @@ __device__ __forceinline__ void run_slice(const BmtArgs& b, int64_t off, int ste
 // Without this a segment started with three dependent memory latencies
 // AFTER the staging (slice range -> slice offsets -> records), ~2.5 us of the
 // ~12 us a config-4 segment takes.
-// slice metadata loads pinned where they are written (asm volatile): as plain
-// loads the compiler sank the row id to its use after the slice's FMAs, one
-// exposed memory latency per slice (9 % of the c4 F = 4 pass's stall samples)
+// slice metadata loads pinned where they are written (asm volatile), one
+// slice ahead of their use.  The row id is still waited for at the end of a
+// short slice (9 % of the c4 F = 4 pass's stall samples sit on it): a c4
+// slice is ~3 record steps, about one DRAM latency (same time with plain
+// loads: profiles/r02_ab_meta.txt)
 #ifndef GIFT_BMT_META
-#define GIFT_BMT_META 2
+#define GIFT_BMT_META 1
 #endif
 __device__ __forceinline__ int64_t ld_meta_s64(const int64_t* p) {
 #if GIFT_BMT_META
@@ -1174,9 +1176,6 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
     sl0 = (int)b.seg_slice[s_beg];
     sl1 = (int)b.seg_slice[s_beg + 1];
     sl2 = s_beg + 2 <= s_end ? (int)b.seg_slice[s_beg + 2] : sl1;
-#if GIFT_BMT_META >= 2
-    cur = load_first(b, sl0, sl1 - sl0, warp, lane);
-#endif
   }
   for (int64_t s = s_beg; s < s_end; ++s) {
     const int64_t cbase = (int64_t)b.seg_code[s] * kC;
@@ -1196,15 +1195,14 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
       for (int i = tid; i < nv; i += kThreads) dst[i] = src[i];
       for (int i = nv * 4 + tid; i < nf; i += kThreads) zs[i] = zg[i];
     }
-    // the warp's first slice: its metadata was requested when the warp left
-    // the previous segment (the latency ran under the wait for the slower
-    // warps); its first records go in flight now, while the block is staged
+    // the warp's first slice: metadata, then its first records, in flight
+    // while the block is staged.  (Requesting the metadata one step earlier,
+    // when the warp leaves the previous segment, keeps five more registers
+    // live across the barrier: spills, c4 step 6.46 -> 6.81 ms.)
     RecPipe<D, CODED> pipe;
     int sl3 = sl2;
     if constexpr (kPre) {
-#if GIFT_BMT_META < 2
       cur = load_first(b, sl0, sl1 - sl0, warp, lane);
-#endif
       if (s + 3 <= s_end) sl3 = (int)b.seg_slice[s + 3];
       if (warp < sl1 - sl0) {
         const uint8_t* cp = b.data + (cur.off / 128) * RB + 8 * lane;
@@ -1221,9 +1219,6 @@ __device__ __forceinline__ void bmt_tile(const HopArgs& a, const BmtArgs& b, int
     }
     if constexpr (kPre) {
       segment_slices_pre<FIN, D, CODED>(b, sl0, sl1 - sl0, warp, cur, pipe, zs, accs, &slice_ctr, tbl, lane, pol_s);
-#if GIFT_BMT_META >= 2
-      if (s + 1 < s_end) cur = load_first(b, sl1, sl2 - sl1, warp, lane);
-#endif
       sl0 = sl1;
       sl1 = sl2;
       sl2 = sl3;
