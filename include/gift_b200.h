@@ -86,7 +86,9 @@ int gift_ctx_set_tiled_policy(gift_ctx* ctx, int policy);
  *   as the implicit term, see gift_csr_attach_implicit_nets),
  *   "barrier_free" 0/1, "fused" 0/1 (small banks as one cooperative kernel),
  *   "graphs" 0/1 (CUDA-graph replay of small banks the fused kernel does not take),
- *   "zero_copy" 0/1 (pinned host buffers used in place), "schedule" 0/1,
+ *   "zero_copy" 0/1 (pinned host buffers used in place), "schedule" 0/1/2
+ *   (entry order inside the tiled copies: none / greedy / greedy + the
+ *   edge-colouring optimum for the two-chain copy, the default),
  *   "row_lanes" 0/8/16/32, "codes" 0 (1 only in -DGIFT_TUNING builds: u8
  *   weight codes in the F <= 2 tiled copy, an experiment that measured slower),
  *   "prefetch" 0 (1 only in tuning builds: L2 bulk prefetch of each warp's

@@ -137,6 +137,8 @@ void set_option(Ctx* ctx, const std::string& name, int64_t v) {
   } else if (name == "col_bits") {
     if (v != 0 && (v < 11 || v > 14)) bad();
     o.col_bits = v;
+  } else if (name == "schedule" && v == 2) {
+    o.schedule = 2;  // optimal (edge-colouring) step order in the F = 4 tiled copy
   } else if (name == "barrier_free" && v == 2) {
     o.barrier_free = 2;  // also on tiles of <= 2048 rows at one 1024-thread CTA per SM
   } else if (name == "barrier_free" || name == "graphs" || name == "zero_copy" || name == "schedule" ||

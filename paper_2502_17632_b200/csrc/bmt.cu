@@ -429,6 +429,232 @@ __global__ void __launch_bounds__(256) k_slice_schedule(int64_t nslices, int kC,
   }
 }
 
+
+// Optimal step order for the F = 4 copy (option "schedule" = 2).  An LDS.128
+// wavefront serves the 8 lanes of a quarter warp, conflict-free when their
+// columns differ mod 8.  Per (slice, quarter) the entries form a bipartite
+// multigraph lanes x residues (M[i][r] = entries of lane i with column = r mod
+// 8); ordering them into L steps with distinct residues per step is an edge
+// colouring with L colours.  A residue held by more than L entries of the
+// quarter forces conflicts: its surplus entries become "fillers" like the
+// padding slots (which may sit on the zero row of any residue).  The rest is
+// made L-regular by spreading every lane's fillers over the residues with
+// slack (north-west corner rule, in closed form from two prefix sums), and an
+// L-regular bipartite multigraph splits into L perfect matchings (Birkhoff -
+// von Neumann): find a perfect matching in the support (8 x 8 bits, augmenting
+// paths), use it for as many steps as its rarest edge allows, repeat.
+// Conflicts left = the surplus entries, the lower bound; the greedy wavefront
+// schedule leaves 5-9-way conflicts in a slice's last steps.
+//
+// One warp per slice, lane = the slice's lane (it moves its own entries, as in
+// the greedy kernel).  The 8 lanes of a quarter hold one matrix row each and
+// run the matching search redundantly on the shared 64-bit support, so they
+// stay converged; all exchanges are quarter-wide shuffles.  Small per-lane
+// arrays are indexed through unrolled selects (registers, no local memory).
+__device__ __forceinline__ int sel8(const int (&v)[8], int r) {
+  int x = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x = (i == r) ? v[i] : x;
+  return x;
+}
+__device__ __forceinline__ void add8(int (&v)[8], int r, int d) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] += (i == r) ? d : 0;
+}
+__device__ __forceinline__ unsigned get4(unsigned x, int i) { return (x >> (4 * i)) & 15u; }
+__device__ __forceinline__ unsigned set4(unsigned x, int i, unsigned v) {
+  return (x & ~(15u << (4 * i))) | (v << (4 * i));
+}
+
+__global__ void __launch_bounds__(256) k_slice_schedule_bvn(int64_t nslices, int kC,
+                                                            const int64_t* __restrict__ slice_off,
+                                                            uint16_t* __restrict__ col, float* __restrict__ w,
+                                                            uint16_t* __restrict__ tcol, float* __restrict__ tw) {
+  const int lane = threadIdx.x & 31;
+  const int i = lane & 7;    // this lane's row of the quarter's matrix
+  const int qb = lane & ~7;  // first lane of the quarter
+  const unsigned qmask = 0xffu << qb;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t sl = warp0; sl < nslices; sl += nwarps) {
+    const int64_t off = slice_off[sl];
+    const int L = (int)((slice_off[sl + 1] - off) / 32);  // slots per lane
+    if (L <= 0) continue;
+    // 1. bucket this lane's real entries by residue into its scratch run
+    int cnt[8], bst[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) cnt[r] = 0;
+    int pads = 0;
+    for (int k = 0; k < L; ++k) {
+      const int cv = col[off + (k >> 2) * 128 + lane * 4 + (k & 3)];
+      if (cv >= kC) ++pads;
+      else add8(cnt, cv & 7, 1);
+    }
+    {
+      int acc = 0;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        bst[r] = acc;
+        acc += cnt[r];
+      }
+    }
+    const int64_t base = off + (int64_t)lane * L;
+    {
+      int pos[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) pos[r] = bst[r];
+      for (int k = 0; k < L; ++k) {
+        const int64_t slot = off + (k >> 2) * 128 + lane * 4 + (k & 3);
+        const int cv = col[slot];
+        if (cv >= kC) continue;
+        const int p = sel8(pos, cv & 7);
+        tcol[base + p] = (uint16_t)cv;
+        tw[base + p] = w[slot];
+        add8(pos, cv & 7, 1);
+      }
+    }
+    // 2. surplus of every residue (column sum above L), given up lane by lane;
+    //    cnt[r] keeps the entries placed as themselves, ovc[r] the surplus
+    int ovc[8], S[8];
+    int need = pads;  // fillers of this lane = padding + surplus entries
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int v = cnt[r];
+      int inc = v;
+#pragma unroll
+      for (int d = 1; d < 8; d <<= 1) {
+        const int t = __shfl_up_sync(qmask, inc, d, 8);
+        if (i >= d) inc += t;
+      }
+      const int tot = __shfl_sync(qmask, inc, 7, 8);
+      const int e = tot - L;
+      int g = 0;
+      if (e > 0) g = min(max(e - (inc - v), 0), v);
+      ovc[r] = g;
+      cnt[r] = v - g;
+      need += g;
+      S[r] = e > 0 ? L : tot;
+    }
+    // 3. A = real + fillers with every row and column sum L: this lane's
+    //    fillers are the interval [P, P + need) of the columns' slacks laid end to end
+    int A[8];
+    {
+      int inc = need;
+#pragma unroll
+      for (int d = 1; d < 8; d <<= 1) {
+        const int t = __shfl_up_sync(qmask, inc, d, 8);
+        if (i >= d) inc += t;
+      }
+      const int P = inc - need;
+      int Q = 0;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int slack = L - S[r];
+        const int lo = max(P, Q), hi = min(P + need, Q + slack);
+        A[r] = cnt[r] + max(hi - lo, 0);
+        Q += slack;
+      }
+    }
+    // 4. Birkhoff - von Neumann: perfect matchings of the support, replicated per lane
+    unsigned rowm = 0xffffffffu, colm = 0xffffffffu;  // nibble i: residue of lane i / lane of residue i (15: none)
+    int used[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) used[r] = 0;
+    int k = 0;
+    while (k < L) {
+      unsigned my = 0;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) my |= (A[r] > 0 ? 1u : 0u) << r;
+      unsigned long long sup = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sup |= (unsigned long long)__shfl_sync(qmask, my, j, 8) << (8 * j);
+      for (int i0 = 0; i0 < 8; ++i0) {
+        if (get4(rowm, i0) != 15u) continue;
+        unsigned from = 0, queue = 0, seen = 0;
+        int qh = 0, qt = 0;
+        queue = set4(queue, qt++, (unsigned)i0);
+        bool done = false;
+        while (qh < qt && !done) {
+          const int ii = (int)get4(queue, qh++);
+          unsigned cand = (unsigned)(sup >> (8 * ii)) & 0xffu & ~seen;
+          while (cand && !done) {
+            const int r = __ffs(cand) - 1;
+            cand &= cand - 1;
+            seen |= 1u << r;
+            from = set4(from, r, (unsigned)ii);
+            const unsigned cm = get4(colm, r);
+            if (cm == 15u) {  // free residue: flip the alternating path back to i0
+              int rr = r;
+              for (;;) {
+                const int i2 = (int)get4(from, rr);
+                const unsigned prev = get4(rowm, i2);
+                colm = set4(colm, rr, (unsigned)i2);
+                rowm = set4(rowm, i2, (unsigned)rr);
+                if (i2 == i0) break;
+                rr = (int)prev;
+              }
+              done = true;
+            } else {
+              queue = set4(queue, qt++, cm);
+            }
+          }
+        }
+        if (!done) {  // impossible for a regular multigraph; keep the state consistent anyway
+          for (int r = 0; r < 8; ++r)
+            if (get4(colm, r) == 15u) {
+              colm = set4(colm, r, (unsigned)i0);
+              rowm = set4(rowm, i0, (unsigned)r);
+              break;
+            }
+        }
+      }
+      const int r = (int)get4(rowm, i);  // this lane's residue for the next m steps
+      int m = min(max(sel8(A, r), 1), L - k);
+#pragma unroll
+      for (int d = 4; d > 0; d >>= 1) m = min(m, __shfl_xor_sync(qmask, m, d, 8));
+      int nreal = sel8(cnt, r) - sel8(used, r);
+      for (int t = 0; t < m; ++t) {
+        const int kk = k + t;
+        const int64_t slot = off + (kk >> 2) * 128 + lane * 4 + (kk & 3);
+        if (nreal > 0) {  // an entry of this residue
+          const int p = sel8(bst, r) + sel8(used, r);
+          add8(used, r, 1);
+          --nreal;
+          col[slot] = tcol[base + p];
+          w[slot] = tw[base + p];
+        } else if (pads > 0) {  // a padding slot, on the zero row of this residue
+          --pads;
+          col[slot] = (uint16_t)(kC + r);
+          w[slot] = 0.f;
+        } else {  // a surplus entry: it conflicts wherever it goes
+          int rs = -1;
+#pragma unroll
+          for (int r2 = 7; r2 >= 0; --r2) rs = ovc[r2] > 0 ? r2 : rs;
+          if (rs < 0) {
+            col[slot] = (uint16_t)(kC + r);
+            w[slot] = 0.f;
+          } else {
+            add8(ovc, rs, -1);
+            const int p = sel8(bst, rs) + sel8(cnt, rs) + sel8(ovc, rs);
+            col[slot] = tcol[base + p];
+            w[slot] = tw[base + p];
+          }
+        }
+      }
+      add8(A, r, -m);
+      unsigned z = (__ballot_sync(qmask, sel8(A, r) <= 0) >> qb) & 0xffu;
+      while (z) {  // used-up edges: lane and residue look for new partners
+        const int i2 = __ffs(z) - 1;
+        z &= z - 1;
+        const unsigned r2 = get4(rowm, i2);
+        rowm = set4(rowm, i2, 15u);
+        colm = set4(colm, (int)r2, 15u);
+      }
+      k += m;
+    }
+  }
+}
+
 // entries of sparse segments (fewer than kStage entries: pad / macro columns)
 __global__ void k_flag_sparse(int64_t nseg, const int64_t* __restrict__ seg_start, int64_t nnz,
                               uint8_t* __restrict__ sparse, uint8_t* __restrict__ dense) {
@@ -1879,8 +2105,12 @@ bool bmt_build(Ctx* ctx, Csr* c, const float* w32, Csr::Bmt& B, bool wide_blocks
   if (ctx->opt.schedule) {
     DevBuf<uint16_t> tcol(ctx, total + 8);
     DevBuf<float> tw(ctx, total + 8);
-    k_slice_schedule<<<grid_for(nslices * 32, 256, 1LL << 30), 256, 0, st>>>(nslices, kC, B.slice_off, bcol, bw,
-                                                                            tcol.p, tw.p);
+    if (ctx->opt.schedule == 2 && !wide_blocks && !coded)  // the F = 4 copy: optimal per quarter warp
+      k_slice_schedule_bvn<<<grid_for(nslices * 32, 256, 1LL << 30), 256, 0, st>>>(nslices, kC, B.slice_off, bcol, bw,
+                                                                                  tcol.p, tw.p);
+    else
+      k_slice_schedule<<<grid_for(nslices * 32, 256, 1LL << 30), 256, 0, st>>>(nslices, kC, B.slice_off, bcol, bw,
+                                                                              tcol.p, tw.p);
     GIFT_LAUNCH_CHECK(ctx);
   }
   if (coded) {

@@ -69,7 +69,8 @@ struct Ctx {
     int64_t graphs = 1;             // "graphs": replay small-graph banks as CUDA graphs
     int64_t fused = 1;              // "fused": small-graph banks as one cooperative kernel
     int64_t zero_copy = 1;          // "zero_copy": *_host calls use pinned buffers in place
-    int64_t schedule = 1;           // "schedule": bank-conflict-aware entry order in the tiled copy
+    int64_t schedule = 2;           // "schedule": bank-conflict-aware entry order in the tiled copy (1: greedy
+                                    // everywhere; 2: edge-colouring optimum in the F = 4 copy, greedy in the other)
     int64_t implicit_above = 0;     // "implicit_above": gift_place_host builds the factored clique model (0 = off)
     int64_t row_lanes = 0;          // "row_lanes": force lanes per row of the row kernel (8 / 16 / 32)
     int64_t codes = 0;              // "codes" (tuning builds): u8 weight codes in the F <= 2 tiled copy

@@ -582,6 +582,37 @@ def test_bmt_hop_matches_oracle_and_row_kernel(gb, orc, opts, tiled_always, conf
     assert np.array_equal(placed[mask], fd.fixed_positions()[mask])
 
 
+@pytest.mark.parametrize("config,scale,cap", [("c3", 0.03, 200), ("c4", 0.02, 100), ("c1", 0.2, None)])
+def test_bmt_optimal_schedule_keeps_every_entry(gb, orc, opts, config, scale, cap):
+    """Option schedule=2 (the default): the F = 4 tiled copy orders each quarter
+    warp's entries by an edge colouring (Birkhoff - von Neumann matchings)
+    instead of the greedy pass (schedule=1).  Same entries, another fixed order: the bank matches the
+    oracle and the row kernel within the fp32 tolerance and is deterministic;
+    it stores exactly as many slots as the greedy copy."""
+    from paper_2502_17632_b200 import synth
+
+    fd = synth.generate(config, seed=6, scale=scale, window=900)
+    ref = orc.build_clique_graph(fd.num_cells, fd.net_start, fd.pin_cell, cap)
+    g32 = synth.signal_fp32(fd, seed=3)
+    want = orc.gift_filter(ref, g32.astype(np.float64), DEFAULT)
+    opts(tiled=1, tiled_min_rows=1, tiled_min_mean=1, schedule=1)
+    gb.set_tiled_policy("always")
+    try:
+        greedy_adj = gb.build_clique_graph(fd, max_clique_pins=cap)
+        greedy = gb.gift_filter(greedy_adj, g32)
+        opts(schedule=2)
+        adj = gb.build_clique_graph(fd, max_clique_pins=cap)
+        tiled = gb.gift_filter(adj, g32)
+        again = gb.gift_filter(gb.build_clique_graph(fd, max_clique_pins=cap), g32)
+    finally:
+        gb.set_tiled_policy("on_reuse")
+    info, ginfo = adj.tiled_info(), greedy_adj.tiled_info()
+    assert info["f4"]["built"] and info["f4"]["slots"] == ginfo["f4"]["slots"]
+    assert rel_l2(tiled, want) <= FP32_TOL
+    assert rel_l2(tiled, greedy) <= 1e-6
+    assert np.array_equal(tiled.view(np.int64), again.view(np.int64))
+
+
 # ----------------------------------------------- §8(f) metrics consumers --
 
 @pytest.mark.parametrize("case", ["kat_brute", "dupnets", "rand_graph1"])
