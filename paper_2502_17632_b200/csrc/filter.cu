@@ -355,6 +355,17 @@ struct PrepArgs {
 
 template <int F>
 __device__ __forceinline__ void prep_row(const PrepArgs& p, int64_t i) {
+  if constexpr (F == 4) {
+    // the default bank's first pack (two chains of an N x 2 fp32 signal): one
+    // 8-byte load, two scale loads, one 16-byte store -- the same products
+    if (p.wcols == 2 && p.nch == 2 && p.in_dtype == GIFT_DTYPE_F32 && p.ld == 2 && p.c0 == 0 &&
+        (reinterpret_cast<uintptr_t>(p.g) & 7) == 0) {
+      const float2 x = static_cast<const float2*>(p.g)[i];
+      const float s0 = p.s[0][i], s1 = p.s[1][i];
+      *reinterpret_cast<float4*>(p.z + i * 4) = make_float4(s0 * x.x, s0 * x.y, s1 * x.x, s1 * x.y);
+      return;
+    }
+  }
   float v[F];
 #pragma unroll
   for (int f = 0; f < F; ++f) {
