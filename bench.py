@@ -371,6 +371,7 @@ def main() -> None:
     ap.add_argument("--no-oneshot", action="store_true")
     ap.add_argument("--no-factored", action="store_true", help="skip the factored-clique-model leg")
     ap.add_argument("--factor-above", type=int, default=None, help="implicit_above of the factored leg")
+    ap.add_argument("--scale", type=float, default=1.0, help=argparse.SUPPRESS)  # sweeps only: shrink the config
     ap.add_argument("--e2e-out", choices=["f32", "f64"], default="f32", help="placement dtype of the e2e leg")
     ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
                     help="kernel option (gift_ctx_set_option), e.g. tile_rows=4096; repeatable")
@@ -417,7 +418,7 @@ def main() -> None:
         _lib.set_option(name, int(val))
     args.zero_copy = _lib._options.get("zero_copy", 1) != 0
     t0 = time.perf_counter()
-    fd = synth.generate(args.config, seed=args.seed)
+    fd = synth.generate(args.config, seed=args.seed, scale=args.scale)
     gen_s = time.perf_counter() - t0
     cap = fd.meta["max_clique_pins"]
     torch.cuda.synchronize()
@@ -493,9 +494,10 @@ def main() -> None:
     # ---- timed region: K steps, device events, max over ranks ----
     # Per-launch CUDA events (the roofline's kernel times) ride inside the
     # timed region, except on graphs small enough for the bank's CUDA-graph
-    # replay (< 262144 rows): per-launch events disable the replay, so there
+    # replay (below the tiled hop's row threshold): per-launch events disable the replay, so there
     # the kernel times come from a profiled pass right after the timed one.
-    graph_replay = world == 1 and n < 262144
+    tiled_thr = _lib._options.get("tiled_min_rows", _lib.DEFAULT_OPTIONS["tiled_min_rows"])
+    graph_replay = world == 1 and n < min(tiled_thr, 262144)
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.2)
@@ -712,7 +714,7 @@ def main() -> None:
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "scaling": "strong" if world > 1 else "weak",
             "config": {
-                "workload": f"{args.config}: {fd.meta['n_mov']} movable + {fd.meta['n_macros']} macros + "
+                "workload": f"{args.config}{'' if args.scale == 1.0 else f' x{args.scale}'}: {fd.meta['n_mov']} movable + {fd.meta['n_macros']} macros + "
                             f"{fd.meta['n_pads']} pads, {fd.meta['n_nets']} nets, max_clique_pins={cap}, "
                             f"default bank (6 hops), fp32 fused path",
                 "n": n, "nnz": adj.nnz, "nnz_op": nnz_op, "hops": HOPS, "seed": args.seed,

@@ -202,7 +202,7 @@ def set_tiled_policy(policy: str) -> None:
         check(lib.gift_ctx_set_tiled_policy(ctx, _policy))
 
 
-DEFAULT_OPTIONS = {"tiled": 1, "tiled_min_rows": 262144, "tiled_min_mean": 32, "tile_rows": 0, "col_bits": 0,
+DEFAULT_OPTIONS = {"tiled": 1, "tiled_min_rows": 98304, "tiled_min_mean": 32, "tile_rows": 0, "col_bits": 0,
                    "barrier_free": 1, "graphs": 1, "fused": 1, "zero_copy": 1, "schedule": 2, "row_lanes": 0,
                    "codes": 0, "prefetch": 0, "stream": 0, "balance": 1, "implicit_above": 0}
 

@@ -127,11 +127,7 @@ void set_option(Ctx* ctx, const std::string& name, int64_t v) {
     if (v < 0) bad();
     o.tiled_min_mean = v;
   } else if (name == "tile_rows") {
-#ifdef GIFT_TUNING
     const int64_t lo = 1024;
-#else
-    const int64_t lo = 2048;
-#endif
     if (v != 0 && (v < lo || v > 16384 || v % 32 != 0)) bad();
     o.tile_rows = v;
   } else if (name == "col_bits") {

@@ -112,14 +112,16 @@ BmtShape bmt_shape_for(const Ctx* ctx, int64_t n, double mean_row, bool wide_blo
   // DRAM -- loses that idle time (the DRAM-bound F = 2 pass does not: fewer
   // SMs share the same bandwidth).  The tile height shrinks to the smallest
   // multiple of 32 that keeps the wave count: 7424 rows = 296 tiles = 2 x 148.
-  // Graphs with fewer tiles than SMs get shorter tiles (down to 2048 rows) so
-  // every SM has one.
+  // Graphs with fewer tiles than SMs get shorter tiles (down to 1024 rows) so
+  // every SM has one: c1 (211k rows) runs 147 tiles of 1440 rows, 0.199 ->
+  // 0.182 ms per bank; at 105k rows 1024-row tiles beat the row kernel 0.138
+  // to 0.181 (profiles/r02_ab_small_tiles.txt).
   if (!ctx->opt.tile_rows && ctx->opt.balance && n > 0) {
     const int64_t sms = ctx->num_sms > 0 ? ctx->num_sms : 148;
     const int64_t waves = (n + (int64_t)s.kR * sms - 1) / ((int64_t)s.kR * sms);
     int64_t kr = (n + waves * sms - 1) / (waves * sms);
     kr = (kr + 31) / 32 * 32;
-    s.kR = (int)std::min<int64_t>(s.kR, std::max<int64_t>(kr, 2048));
+    s.kR = (int)std::min<int64_t>(s.kR, std::max<int64_t>(kr, 1024));
   }
   return s;
 }

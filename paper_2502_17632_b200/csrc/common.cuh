@@ -60,7 +60,8 @@ struct Ctx {
   // reads them from GIFT_* environment variables at context creation)
   struct Options {
     int64_t tiled = 1;              // "tiled": 0 = row kernel only
-    int64_t tiled_min_rows = 262144;  // "tiled_min_rows": smaller graphs stay on the row kernel
+    int64_t tiled_min_rows = 98304;   // "tiled_min_rows": smaller graphs stay on the row kernel (measured
+                                      // crossover with wave-balanced tiles: between 53k and 105k rows)
     int64_t tiled_min_mean = 32;    // "tiled_min_mean": mean row length below which too
     int64_t tile_rows = 0;          // "tile_rows": force the tile height (multiple of 32 in 2048..16384), 0 = per graph
     int64_t balance = 1;            // "balance": shrink the default tile height to fill whole waves of SMs

@@ -261,7 +261,7 @@ FULL_SHAPES = {"c3": ((8192, 4096), (8192, 16384)), "c4": ((4096, 8192), (8192, 
 def _balanced_rows(n, rows, sms):
     waves = -(-n // (rows * sms))
     kr = -(-n // (waves * sms))
-    return min(rows, max(-(-kr // 32) * 32, 2048))
+    return min(rows, max(-(-kr // 32) * 32, 1024))
 
 
 @pytest.mark.parametrize("config", ["c3", "c4"])

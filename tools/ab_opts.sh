@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 for c in $cfgs; do for set in "$@"; do
   args=""; for kv in ${set//,/ }; do args="$args --option $kv"; done
   log=gpurun_out/abo_${c}_$(echo "$set" | tr ',=' '_-').log
-  timeout 600 python bench.py --config $c --steps $steps --no-cpu-baseline --no-oneshot --no-factored $args > $log 2>&1
+  timeout 600 python bench.py --config $c --steps $steps --no-cpu-baseline --no-oneshot --no-factored ${AB_EXTRA:-} $args > $log 2>&1
   python - "$c" "$set" "$log" <<'PY'
 import json, sys
 c, v, f = sys.argv[1:]
