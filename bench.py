@@ -402,9 +402,18 @@ def main() -> None:
 
     world, rank, local = dist_env()
     n_formed = 1
+    # GIFT_BENCH_SHARE_GPU=1 (launcher smoke test on a one-GPU box only): every
+    # rank uses cuda:0 and the control group is gloo (NCCL refuses two ranks on
+    # one device); the numbers of such a run mean nothing.
+    share_gpu = os.environ.get("GIFT_BENCH_SHARE_GPU") == "1"
+    if share_gpu:
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+        if share_gpu:
+            dist.init_process_group("gloo", init_method="env://")
+        else:
+            dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
         n_formed = dist.get_world_size()  # the group NCCL actually formed
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
